@@ -1,0 +1,238 @@
+/*
+ * ignis_b200.h — C ABI of the B200-native RHS + SSP-RK3 path.
+ *
+ * Drop-in boundary for the reference's C++ `ignis::Simulation`
+ * (/root/reference/proj/include/ignis/solver.hpp:53-853).  Every entry point
+ * below replaces one public member of that class (cited per function); the
+ * configuration structs are POD restatements of the reference's config types.
+ * No torch or CUDA types appear in any signature: plain pointers, sizes and
+ * status codes.  One context per GPU (or per ensemble member).
+ *
+ * Array convention (host side, identical to ignis::Field::raw(),
+ * field.hpp:45-47): each field is one contiguous padded buffer of
+ * (nx+2g)*(ny+2g) doubles, row-major, i fastest, element (i,j) at
+ * (j+g)*(nx+2g)+(i+g).  Multi-component arguments are the component buffers
+ * concatenated in component order [rhoY_0..rhoY_{ns-1}, rho u, rho v, E]
+ * (flux.hpp:13), i.e. component c starts at c*(nx+2g)*(ny+2g).
+ *
+ * Errors: every call returns an ign_status.  The reference's exception
+ * types (errors.hpp:10-47) map 1:1 onto IGN_CONFIG_ERROR ... IGN_USAGE_ERROR;
+ * ign_last_error() returns the message and, for IGN_STEP_FAILURE, the
+ * (stage, i, j) the reference's StepFailure carries.
+ */
+#ifndef IGNIS_B200_H
+#define IGNIS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IGN_ABI_VERSION 1
+#define IGN_MAX_SPECIES 8   /* thermo.hpp:16 kMaxSpecies */
+#define IGN_MAX_COMP 11     /* flux.hpp:14 kMaxComp */
+#define IGN_MAX_PIECES 4    /* polynomial ranges per species */
+#define IGN_MAX_SEGMENTS 4  /* inflow segments per edge */
+#define IGN_NAME_LEN 16
+
+typedef enum {
+    IGN_OK = 0,
+    IGN_CONFIG_ERROR = 1,   /* ignis::ConfigError   errors.hpp:11 */
+    IGN_STATE_ERROR = 2,    /* ignis::StateError    errors.hpp:17 */
+    IGN_NUMERICS_ERROR = 3, /* ignis::NumericsError errors.hpp:23 */
+    IGN_STEP_FAILURE = 4,   /* ignis::StepFailure   errors.hpp:29 */
+    IGN_FORMAT_ERROR = 5,   /* ignis::FormatError   errors.hpp:39 */
+    IGN_USAGE_ERROR = 6,    /* ignis::UsageError    errors.hpp:45 */
+    IGN_CUDA_ERROR = 7,     /* device/runtime failure (no reference analogue) */
+    IGN_INTERNAL_ERROR = 8
+} ign_status;
+
+/* thermo.hpp:23-39 ThermoPiece */
+typedef struct {
+    double t_lo, t_hi;
+    double cm2, cm1, c0, c1, c2, c3, c4, b;
+} ign_thermo_piece;
+
+/* thermo.hpp:41-58 SpeciesData */
+typedef struct {
+    char name[IGN_NAME_LEN];
+    double W, mu_ref, t_ref, n_exp;
+    int32_t npieces;
+    int32_t _pad;
+    ign_thermo_piece pieces[IGN_MAX_PIECES];
+} ign_species;
+
+/* thermo.hpp:66-104 MixtureModel; mode 0 = CaloricallyPerfect, 1 = MultiSpecies */
+typedef struct {
+    int32_t mode;
+    int32_t ns;
+    double R, Le, Pr;
+    ign_species species[IGN_MAX_SPECIES];
+} ign_mixture;
+
+/* reconstruction.hpp:202-230 SchemeConfig.
+ * scheme: 0 = WENO3Z, 1 = TENO6; split: 0 = Componentwise, 1 = Characteristic;
+ * metrics: 0 = Scheme, 1 = AnalyticSkew, 2 = Central2 */
+typedef struct {
+    int32_t scheme;
+    int32_t split;
+    double teno_ct, eps, cfl;
+    int32_t metrics;
+    int32_t _pad;
+} ign_scheme;
+
+/* boundary.hpp:25-32 InflowSegment */
+typedef struct {
+    double lo, hi, u, v, T;
+    double Y[IGN_MAX_SPECIES];
+} ign_inflow_segment;
+
+/* boundary.hpp:16-41 BCType/EdgeSpec.
+ * type: 0 Periodic, 1 NoslipIsothermal, 2 NoslipAdiabatic, 3 Inflow, 4 Outflow */
+typedef struct {
+    int32_t type;
+    int32_t nseg;
+    double T_wall;
+    ign_inflow_segment seg[IGN_MAX_SEGMENTS];
+    double smooth_width, p_target, sigma_out;
+} ign_edge;
+
+/* boundary.hpp:45-89 BoundarySpec */
+typedef struct {
+    ign_edge left, right, bottom, top;
+} ign_bc;
+
+/* chemistry.hpp:16-24 ReactionMechanism (present = 0 means std::nullopt) */
+typedef struct {
+    int32_t present;
+    int32_t i_fuel, i_ox, i_co2, i_h2o;
+    int32_t _pad;
+    double A, Ta, a, b, T_cutoff;
+    double nu[IGN_MAX_SPECIES];
+} ign_mechanism;
+
+/* laser.hpp:99-127 LaserParams + ShapedProfile (present = 0 means nullopt).
+ * kernel: 0 = Gaussian, 1 = Shaped */
+typedef struct {
+    int32_t present;
+    int32_t kernel;
+    double energy, sigma_r, sigma_t, x0, y0, t0, edot_rate;
+    double lobe_sep, width_up, width_down, amp_down, width_radial;
+} ign_laser;
+
+/* solver.hpp:29-35 IntegratorConfig */
+typedef struct {
+    double fixed_dt, t_end;
+    int64_t max_iter;
+    int32_t chem_dt_limit;
+    int32_t _pad;
+    double chem_dt_factor;
+} ign_integrator;
+
+/* Everything Simulation::init (solver.hpp:82-101) and its public knobs
+ * (solver.hpp:55-76) receive.  The mesh is build_uniform (mesh.hpp:48-77),
+ * optionally followed by apply_skew(skew_beta) (mesh.hpp:92-117). */
+typedef struct {
+    int32_t abi_version;         /* must be IGN_ABI_VERSION */
+    int32_t nx, ny, g;           /* g = 3 (mesh.hpp:14) */
+    double lx, ly, center_x, center_y;
+    int32_t periodic_x, periodic_y;
+    int32_t apply_skew;          /* 1: apply_skew(mesh, skew_beta) */
+    int32_t metric_mode;         /* -1: Simulation::metric_mode_for(scheme);
+                                    0 Central2, 1 Order4, 2 Order6, 3 AnalyticSkew */
+    double skew_beta;
+    ign_mixture mix;
+    ign_scheme scheme;
+    ign_bc bc;
+    ign_mechanism mech;
+    ign_laser laser;
+    int32_t viscous;
+    int32_t partitions;          /* ThreadTeam workers (CPU oracle only) */
+    ign_integrator integ;
+    int32_t device;              /* CUDA device ordinal */
+    int32_t _pad;
+} ign_config;
+
+/* errors.hpp:29-35 StepFailure payload + message */
+typedef struct {
+    int32_t status;
+    int32_t stage, i, j;
+    char msg[256];
+} ign_error;
+
+/* solver.hpp:114-128: primitive point of set_initial_condition's callback */
+typedef struct {
+    double rho, u, v, p, T;
+    double Y[IGN_MAX_SPECIES];
+} ign_prim_point;
+
+typedef void (*ign_ic_fn)(double x, double y, void* user, ign_prim_point* out);
+/* advance's step_hook (solver.hpp:336,347); return nonzero to stop. */
+typedef int (*ign_step_hook)(void* ctx, void* user);
+
+typedef struct ign_context ign_context;
+
+/* ---- lifecycle -------------------------------------------------------- */
+uint64_t ign_config_size(void); /* sizeof(ign_config), ABI self-check */
+/* Simulation::init (solver.hpp:82-101) incl. scheme/bc validation */
+int ign_create(const ign_config* cfg, ign_context** out);
+void ign_destroy(ign_context* ctx);
+int ign_last_error(const ign_context* ctx, ign_error* err);
+int ign_dims(const ign_context* ctx, int32_t* nx, int32_t* ny, int32_t* g,
+             int32_t* ns);
+
+/* ---- setup / host mirrors --------------------------------------------- */
+/* mesh.x/mesh.y padded arrays (mesh.hpp:295-296) */
+int ign_get_mesh(const ign_context* ctx, double* x, double* y);
+/* which 0: met (solver.hpp:56), 1: met_v (solver.hpp:57); out = 5 padded
+ * fields [jac, m_xi_x, m_xi_y, m_eta_x, m_eta_y] (metrics.hpp:28-35) */
+int ign_get_metrics(const ign_context* ctx, int which, double* out);
+/* Simulation::set_initial_condition (solver.hpp:115-128), callback form */
+int ign_set_initial_condition(ign_context* ctx, ign_ic_fn fn, void* user);
+/* Same, from padded primitive arrays rho,u,v,T then Y_0..Y_{ns-1}
+ * ((4+ns) fields); p is not used by conservative_from_primitives. */
+int ign_set_initial_primitives(ign_context* ctx, const double* prim);
+/* Direct Ut write (nc fields) plus optional primitive T cache (1 field,
+ * NULL keeps the current cache). Mirrors mutating sim.Ut / sim.T. */
+int ign_set_state(ign_context* ctx, const double* Ut, const double* Tcache);
+int ign_get_state(ign_context* ctx, double* Ut);
+/* Primitive cache (solver.hpp:79-80): rho,u,v,p,T,c then Y_s ((6+ns) fields) */
+int ign_get_cache(ign_context* ctx, double* prim);
+int ign_get_time(const ign_context* ctx, double* time, int64_t* iter);
+int ign_set_time(ign_context* ctx, double time, int64_t iter);
+int ign_set_integrator(ign_context* ctx, const ign_integrator* integ);
+
+/* ---- the hot path ----------------------------------------------------- */
+int ign_refill_ghosts(ign_context* ctx);                 /* solver.hpp:144 */
+int ign_refresh_primitives(ign_context* ctx, int stage); /* solver.hpp:148-177 */
+int ign_prepare_stage(ign_context* ctx, int stage);      /* solver.hpp:422-425 */
+/* solver.hpp:185-232; rhs = nc padded fields (interior written, ghosts 0);
+ * rhs may be NULL (result stays on the device). */
+int ign_compute_rhs(ign_context* ctx, double t_stage, int stage, double* rhs);
+int ign_stable_dt(ign_context* ctx, double* dt);          /* solver.hpp:240-299 */
+int ign_rk3_step(ign_context* ctx, double dt);            /* solver.hpp:304-332 */
+int ign_advance(ign_context* ctx, ign_step_hook hook, void* user); /* :336-349 */
+/* n steps of rk3_step(dt) with no host round trip in between (fixed dt). */
+int ign_rk3_steps(ign_context* ctx, double dt, int64_t nsteps);
+
+/* ---- diagnostics ------------------------------------------------------ */
+int ign_conserved_totals(ign_context* ctx, double* tot);  /* solver.hpp:411-418 */
+int ign_product_mole_fraction(ign_context* ctx, double* out); /* :387-407 */
+int ign_last_clip(const ign_context* ctx, double* clip);  /* solver.hpp:75 */
+
+/* ---- host-only helpers (no device needed; used by the CPU tests) ------- */
+/* compute_metrics over the configured mesh: which 0 = inviscid set, 1 = Central2 */
+int ign_host_metrics(const ign_config* cfg, int which, double* out,
+                     ign_error* err);
+int ign_host_mesh(const ign_config* cfg, double* x, double* y, ign_error* err);
+
+/* ---- device statistics (bench evidence) -------------------------------- */
+/* Number of kernels this context has launched since creation. */
+int64_t ign_kernel_launches(const ign_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IGNIS_B200_H */

@@ -1,0 +1,774 @@
+// kernels.cuh — the sm_100a kernels of one RK stage (FP64, -fmad=false).
+//
+// Data layout in HBM: structure-of-arrays, one padded plane of
+// (nx+2g)*(ny+2g) doubles per field, i fastest — the reference's Field layout
+// (field.hpp:45-47) so host<->device transfers are single copies.  Face fluxes
+// live in their own face-indexed planes (x: (nx+1) x ny, y: nx x (ny+1)) so
+// each face is evaluated exactly once.
+//
+// Per stage the launch sequence is
+//   k_bc_x, k_bc_y        ghost fill            (boundary.hpp:136-258)
+//   k_prim                primitive cache       (solver.hpp:148-177)
+//   k_faces<x>, k_faces<y> inviscid face fluxes (solver.hpp:441-579)
+//   k_visc                viscous node fluxes   (solver.hpp:588-696)
+//   k_assemble            RHS assembly + LODI + sources + RK update + clip/
+//                         validate              (solver.hpp:185-232, 717-849)
+// and k_dt reduces the CFL/chemistry limit (solver.hpp:240-299).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "flux.cuh"
+#include "physics.cuh"
+
+namespace ign {
+
+// ---------------------------------------------------------------- errors
+// Device error word: the first failure in the reference's own order wins via
+// atomicMin on key = stage<<60 | phase<<52 | index<<4 | sub.
+enum Phase : unsigned {
+    PH_BC = 1,     // StateError from fill_ghosts' prim_at (boundary.hpp:151-156)
+    PH_PRIM = 2,   // StepFailure "stage state failure" (solver.hpp:162-165)
+    PH_INVX = 3,   // NumericsError from inviscid x faces (solver.hpp:522-524, flux.hpp:78,99)
+    PH_INVY = 4,
+    PH_RHS = 5,    // StepFailure "non-finite RHS" (solver.hpp:225-228)
+    PH_POST = 6,   // StepFailure post_stage (solver.hpp:840-844)
+};
+constexpr unsigned long long kNoError = ~0ull;
+
+struct ErrRec {
+    unsigned long long key;
+    int32_t step;
+    int32_t _pad;
+};
+
+__device__ __forceinline__ bool failed(const ErrRec* e) {
+    return *reinterpret_cast<const volatile unsigned long long*>(&e->key) != kNoError;
+}
+
+__device__ __forceinline__ void report(ErrRec* e, unsigned stage, unsigned phase,
+                                       unsigned long long idx, unsigned sub, int step) {
+    const unsigned long long key = ((unsigned long long)stage << 60) |
+                                   ((unsigned long long)phase << 52) | (idx << 4) | sub;
+    atomicMin(&e->key, key);
+    e->step = step;
+}
+
+// ---------------------------------------------------------------- params
+struct KParams {
+    int32_t nx, ny, g, sx;
+    long long plane;
+    int32_t ns, viscous;
+    int32_t bc_type[4];  // left, right, bottom, top
+    double T_wall[4];
+    double sigma_out_right, p_target_right;
+    double lx, ly, cx, cy;
+    double ct, eps;
+    int32_t chem_dt_limit, lodi;
+    double chem_dt_factor;
+    // primitive cache block: rho,u,v,p,T,c then Y_s, then X_s (viscous)
+    double* prim;
+    const double *jac, *mxx, *mxy, *mex, *mey;       // met (inviscid)
+    const double *vjac, *vmxx, *vmxy, *vmex, *vmey;  // met_v (Central2)
+    const double *xc, *yc;                           // mesh.x, mesh.y
+    double *Fx, *Gy, *Fv, *Gv;
+    const double* inflow[4];  // per edge [t][k][u,v,T,Y_s] profile tables
+    ErrRec* err;
+    unsigned long long* red;  // [0] lam_max bits, [1] dt_chem bits, [2..7] clip bits
+    DMix mix;
+    DMech mech;
+    DLaser laser;
+};
+
+__device__ __forceinline__ long long pidx(const KParams& P, int i, int j) {
+    return (long long)(j + P.g) * P.sx + (i + P.g);
+}
+
+// primitive cache planes
+#define PRHO(P) ((P).prim)
+#define PU(P) ((P).prim + (P).plane)
+#define PV(P) ((P).prim + 2 * (P).plane)
+#define PP(P) ((P).prim + 3 * (P).plane)
+#define PT(P) ((P).prim + 4 * (P).plane)
+#define PC(P) ((P).prim + 5 * (P).plane)
+#define PY(P, s) ((P).prim + (6 + (s)) * (P).plane)
+#define PX(P, s) ((P).prim + (6 + (P).ns + (s)) * (P).plane)
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------- ghost fill
+// fill_ghosts (boundary.hpp:136-258).  One thread per (edge, t) runs the
+// reference's k = 1..g loop.  x edges cover rows 0..ny-1 (launch 1), y edges
+// the full padded range -g..nx+g-1 (launch 2), so corners take the y rule.
+template <int NS>
+__device__ int bc_prim_at(const KParams& P, const double* Ut, int i, int j, Prim<NS>& pt,
+                          double& rs) {
+    const long long id = pidx(P, i, j);
+    const double J = P.jac[id];
+    double U[NS + 3];
+#pragma unroll
+    for (int c = 0; c < NS + 3; ++c) U[c] = Ut[c * P.plane + id] * J;
+    return primitives_from_conservative<NS>(U, P.mix, 300.0, pt, &rs);
+}
+
+template <int NS>
+__device__ void bc_store(const KParams& P, double* Ut, const Prim<NS>& pt, int i, int j) {
+    double U[NS + 3];
+    conservative_from_primitives<NS>(pt, P.mix, U);
+    const long long id = pidx(P, i, j);
+    const double invJ = 1.0 / P.jac[id];
+#pragma unroll
+    for (int c = 0; c < NS + 3; ++c) Ut[c * P.plane + id] = U[c] * invJ;
+}
+
+template <int NS>
+__device__ void bc_copy_scaled(const KParams& P, double* Ut, int is, int js, int id_, int jd) {
+    const long long s = pidx(P, is, js), d = pidx(P, id_, jd);
+    const double ratio = P.jac[s] / P.jac[d];
+#pragma unroll
+    for (int c = 0; c < NS + 3; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, double* Ut,
+                                            int ypass, int stage, int step) {
+    if (failed(P.err)) return;
+    const int g = P.g, nx = P.nx, ny = P.ny;
+    const int tlo = ypass ? -g : 0;
+    const int ntr = ypass ? nx + 2 * g : ny;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= 2 * ntr) return;
+    const int side = tid / ntr;  // 0: left/bottom, 1: right/top
+    const int t = tlo + tid % ntr;
+    const int edge = (ypass ? 2 : 0) + side;
+    const int type = P.bc_type[edge];
+    const int n = ypass ? ny : nx;
+    // ghost / mirror / wrap / interior index along the edge normal
+    auto ij = [&](int a, int& i, int& j) {
+        if (ypass) { i = t; j = a; } else { i = a; j = t; }
+    };
+    int gi, gj;
+    switch (type) {
+    case 0: {  // Periodic (boundary.hpp:203-209)
+        for (int k = 1; k <= g; ++k) {
+            int si, sj;
+            ij(side == 0 ? n - k : k - 1, si, sj);
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            bc_copy_scaled<NS>(P, Ut, si, sj, gi, gj);
+        }
+        break;
+    }
+    case 1:
+    case 2: {  // No-slip walls (boundary.hpp:210-226)
+        for (int k = 1; k <= g; ++k) {
+            int mi, mj;
+            ij(side == 0 ? k - 1 : n - k, mi, mj);
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            Prim<NS> pt;
+            double rs;
+            const int st = bc_prim_at<NS>(P, Ut, mi, mj, pt, rs);
+            if (st) {
+                report(P.err, stage, PH_BC,
+                       ((unsigned long long)edge * (nx + 2 * g + ny) + (t - tlo)) * (g + 1) + k,
+                       st, step);
+                return;
+            }
+            pt.u = -pt.u;
+            pt.v = -pt.v;
+            if (type == 1) {
+                const double tg = 2.0 * P.T_wall[edge] - pt.T;
+                pt.T = smax(tg, 0.05 * P.T_wall[edge]);
+            }
+            pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
+            bc_store<NS>(P, Ut, pt, gi, gj);
+        }
+        break;
+    }
+    case 3: {  // Inflow (boundary.hpp:227-241), profile precomputed on the host
+        int ii, ji;
+        ij(side == 0 ? 0 : n - 1, ii, ji);
+        Prim<NS> inner;
+        double rs;
+        const int st = bc_prim_at<NS>(P, Ut, ii, ji, inner, rs);
+        if (st) {
+            report(P.err, stage, PH_BC,
+                   ((unsigned long long)edge * (nx + 2 * g + ny) + (t - tlo)) * (g + 1), st,
+                   step);
+            return;
+        }
+        const double* prof = P.inflow[edge] + (long long)(t - tlo) * g * (3 + NS);
+        for (int k = 1; k <= g; ++k) {
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            const double* q = prof + (k - 1) * (3 + NS);
+            Prim<NS> pt;
+            pt.u = q[0];
+            pt.v = q[1];
+            pt.T = q[2];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) pt.Y[s] = q[3 + s];
+            pt.p = inner.p;
+            pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
+            bc_store<NS>(P, Ut, pt, gi, gj);
+        }
+        break;
+    }
+    default: {  // Outflow (boundary.hpp:242-249)
+        int ii, ji;
+        ij(side == 0 ? 0 : n - 1, ii, ji);
+        for (int k = 1; k <= g; ++k) {
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            bc_copy_scaled<NS>(P, Ut, ii, ji, gi, gj);
+        }
+        break;
+    }
+    }
+}
+
+// ---------------------------------------------------------------- primitives
+// refresh_primitives (solver.hpp:148-177) over the padded box; the cached T
+// is the Newton guess (thermo.hpp:196).
+template <int NS, bool WX>
+__global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
+                                              const double* __restrict__ Ut, int stage,
+                                              int step) {
+    if (failed(P.err)) return;
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= P.plane) return;
+    const double J = P.jac[id];
+    double U[NS + 3];
+#pragma unroll
+    for (int c = 0; c < NS + 3; ++c) U[c] = Ut[c * P.plane + id] * J;
+    Prim<NS> pt;
+    double rs;
+    const int st = primitives_from_conservative<NS>(U, P.mix, PT(P)[id], pt, &rs);
+    if (st) {
+        report(P.err, stage, PH_PRIM, (unsigned long long)id, st, step);
+        return;
+    }
+    PRHO(P)[id] = pt.rho;
+    PU(P)[id] = pt.u;
+    PV(P)[id] = pt.v;
+    PP(P)[id] = pt.p;
+    PT(P)[id] = pt.T;
+    PC(P)[id] = sound_speed_rs<NS>(pt.T, pt.Y, rs, P.mix);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) PY(P, s)[id] = pt.Y[s];
+    if (WX) {
+        double X[NS];
+        mole_fractions<NS>(pt.Y, P.mix, X);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) PX(P, s)[id] = X[s];
+    }
+}
+
+// ---------------------------------------------------------------- inviscid faces
+// One thread per face m+1/2 of one line (solver.hpp:481-568).  DIR 0: x faces
+// f = m+1 in [0, nx] of row j; DIR 1: y faces of column i (threads along i
+// for coalesced stencil loads).
+template <int NS, int DIR, bool TENO, bool CHAR>
+__global__ void __launch_bounds__(128) k_faces(const __grid_constant__ KParams P,
+                                               const double* __restrict__ Ut, int stage,
+                                               int step) {
+    constexpr int NC = NS + 3;
+    constexpr int H = TENO ? 3 : 2;
+    constexpr int W = 2 * H;
+    if (failed(P.err)) return;
+    int line, f;
+    if (DIR == 0) {
+        f = blockIdx.x * blockDim.x + threadIdx.x;
+        line = blockIdx.y;
+        if (f > P.nx) return;
+    } else {
+        line = blockIdx.x * blockDim.x + threadIdx.x;
+        f = blockIdx.y;
+        if (line >= P.nx) return;
+    }
+    const int m = f - 1;  // face between nodes m and m+1
+    const long long step_n = DIR == 0 ? 1 : P.sx;  // node stride along the line
+    const long long base = DIR == 0 ? pidx(P, m, line) : pidx(P, line, m);
+    const double* m1a = DIR == 0 ? P.mxx : P.mex;
+    const double* m2a = DIR == 0 ? P.mxy : P.mey;
+    const long long il = base, ir = base + step_n;
+    const double m1f = 0.5 * (ldg(m1a + il) + ldg(m1a + ir));
+    const double m2f = 0.5 * (ldg(m2a + il) + ldg(m2a + ir));
+
+    // Node pass (solver.hpp:466-479) for the 2h stencil nodes m-h+1..m+h.
+    double Fk[W][NC], Uk[W][NC], unk[W], ck[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const long long id = base + (long long)(k - H + 1) * step_n;
+        const double J = ldg(P.jac + id);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) Uk[k][c] = ldg(Ut + c * P.plane + id) * J;
+        mapped_flux<NS>(Uk[k], ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk[k]);
+        unk[k] = ldg(PU(P) + id);  // cached u; v folded in below
+        ck[k] = ldg(PV(P) + id);
+    }
+    double Fh[NC];
+    const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
+    const unsigned long long eidx = (unsigned long long)line * ((DIR == 0 ? P.nx : P.ny) + 1) + f;
+
+    if (CHAR) {
+        // roe_average + EigenSystem::at_state at the face (solver.hpp:493-502)
+        double Yl[NS], Yr[NS], Ya[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            Yl[s] = ldg(PY(P, s) + il);
+            Yr[s] = ldg(PY(P, s) + ir);
+        }
+        double Ta, ua, va;
+        roe_average<NS>(ldg(PRHO(P) + il), Yl, ldg(PT(P) + il), ldg(PU(P) + il),
+                        ldg(PV(P) + il), ldg(PRHO(P) + ir), Yr, ldg(PT(P) + ir),
+                        ldg(PU(P) + ir), ldg(PV(P) + ir), P.mix, Ya, Ta, ua, va);
+        Eigen<NS> es;
+        const int est = eigen_at_state<NS>(Ya, Ta, ua, va, m1f, m2f, P.mix, es);
+        if (est) {
+            report(P.err, stage, phase, eidx, 1 + est, step);
+            return;
+        }
+        // per-node normal speed with the face normal, cached c (solver.hpp:505-515)
+        double lf[W][NC], lu[W][NC];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const long long id = base + (long long)(k - H + 1) * step_n;
+            unk[k] = es.n1 * unk[k] + es.n2 * ck[k];
+            ck[k] = ldg(PC(P) + id);
+            eigen_project<NS>(es, Fk[k], lf[k]);
+            eigen_project<NS>(es, Uk[k], lu[k]);
+        }
+        double amp[NC];
+#pragma unroll
+        for (int fl = 0; fl < NC; ++fl) {
+            double alpha = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                alpha = smax(alpha, fabs(field_speed<NS>(es, fl, unk[k], ck[k])));
+            if (!isfinite(alpha)) {
+                report(P.err, stage, phase, eidx, 1, step);
+                return;
+            }
+            double wp[W], wm[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                wp[k] = 0.5 * (lf[k][fl] + alpha * lu[k][fl]);
+                wm[k] = 0.5 * (lf[k][fl] - alpha * lu[k][fl]);
+            }
+            amp[fl] = face_pm<TENO>(wp, wm, P.ct, P.eps);
+        }
+        eigen_assemble<NS>(es, amp, Fh);
+    } else {
+        // componentwise LLF (solver.hpp:536-567)
+        const double sf = hypot(m1f, m2f);
+        double alpha = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const long long id = base + (long long)(k - H + 1) * step_n;
+            const double un = (m1f * unk[k] + m2f * ck[k]) / sf;
+            alpha = smax(alpha, sf * (fabs(un) + ldg(PC(P) + id)));
+        }
+        if (!isfinite(alpha)) {
+            report(P.err, stage, phase, eidx, 1, step);
+            return;
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            double wp[W], wm[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                wp[k] = 0.5 * (Fk[k][c] + alpha * Uk[k][c]);
+                wm[k] = 0.5 * (Fk[k][c] - alpha * Uk[k][c]);
+            }
+            Fh[c] = face_pm<TENO>(wp, wm, P.ct, P.eps);
+        }
+    }
+    double* out = DIR == 0 ? P.Fx : P.Gy;
+    const long long fplane = (long long)(P.nx + 1 - DIR) * (P.ny + DIR);
+    const long long o = DIR == 0 ? (long long)line * (P.nx + 1) + f : (long long)f * P.nx + line;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[c * fplane + o] = Fh[c];
+}
+
+// ---------------------------------------------------------------- viscous
+// compute_viscous node fluxes over ring 1 (solver.hpp:610-696).
+template <int NS>
+__global__ void __launch_bounds__(128) k_visc(const __grid_constant__ KParams P, int stage,
+                                              int step) {
+    constexpr int NC = NS + 3;
+    if (failed(P.err)) return;
+    const int w = P.nx + 2;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)w * (P.ny + 2)) return;
+    const int i = (int)(t % w) - 1, j = (int)(t / w) - 1;
+    const long long id = pidx(P, i, j);
+    const long long ie = id + 1, iw = id - 1, in = id + P.sx, is = id - P.sx;
+    auto ddxi = [&](const double* f) { return 0.5 * (ldg(f + ie) - ldg(f + iw)); };
+    auto ddeta = [&](const double* f) { return 0.5 * (ldg(f + in) - ldg(f + is)); };
+    const double vj = ldg(P.vjac + id);
+    const double xi_x = ldg(P.vmxx + id) * vj;
+    const double xi_y = ldg(P.vmxy + id) * vj;
+    const double eta_x = ldg(P.vmex + id) * vj;
+    const double eta_y = ldg(P.vmey + id) * vj;
+    auto gradx = [&](const double* f) { return xi_x * ddxi(f) + eta_x * ddeta(f); };
+    auto grady = [&](const double* f) { return xi_y * ddxi(f) + eta_y * ddeta(f); };
+    const double ux = gradx(PU(P)), uy = grady(PU(P));
+    const double vx = gradx(PV(P)), vy = grady(PV(P));
+    const double Tx = gradx(PT(P)), Ty = grady(PT(P));
+    const double T = ldg(PT(P) + id), rho = ldg(PRHO(P) + id);
+    double Y[NS], X[NS], gx[NS], gy[NS], hs[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        Y[s] = ldg(PY(P, s) + id);
+        X[s] = ldg(PX(P, s) + id);
+        gx[s] = gradx(PX(P, s));
+        gy[s] = grady(PX(P, s));
+        hs[s] = h_species(T, P.mix.sp[s], P.mix.R);
+    }
+    double mu, lambda, D, cp;
+    transport<NS>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
+    const double div = ux + vy;
+    const double txx = mu * (2.0 * ux - (2.0 / 3.0) * div);
+    const double tyy = mu * (2.0 * vy - (2.0 / 3.0) * div);
+    const double txy = mu * (uy + vx);
+    const double wbar = mean_molar_mass<NS>(Y, P.mix);
+    double ucx = 0.0, ucy = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        ucx += (P.mix.sp[s].W / wbar) * D * gx[s];
+        ucy += (P.mix.sp[s].W / wbar) * D * gy[s];
+    }
+    double ex = lambda * Tx, ey = lambda * Ty;
+    double Fd[NC], Gd[NC];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const double jsx = rho * ((P.mix.sp[s].W / wbar) * D * gx[s] - Y[s] * ucx);
+        const double jsy = rho * ((P.mix.sp[s].W / wbar) * D * gy[s] - Y[s] * ucy);
+        ex += jsx * hs[s];
+        ey += jsy * hs[s];
+        Fd[s] = jsx;
+        Gd[s] = jsy;
+    }
+    const double u = ldg(PU(P) + id), v = ldg(PV(P) + id);
+    Fd[NS] = txx;
+    Fd[NS + 1] = txy;
+    Fd[NS + 2] = u * txx + v * txy + ex;
+    Gd[NS] = txy;
+    Gd[NS + 1] = tyy;
+    Gd[NS + 2] = u * txy + v * tyy + ey;
+    const double a = ldg(P.vmxx + id), b = ldg(P.vmxy + id);
+    const double c2 = ldg(P.vmex + id), d = ldg(P.vmey + id);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        P.Fv[c * P.plane + id] = a * Fd[c] + b * Gd[c];
+        P.Gv[c * P.plane + id] = c2 * Fd[c] + d * Gd[c];
+    }
+}
+
+// ---------------------------------------------------------------- LODI
+// lodi_outflow_override (solver.hpp:717-788) for cell (nx-1, j): dFx values.
+template <int NS>
+__device__ void lodi_dfx(const KParams& P, int j, double* dF) {
+    const int i = P.nx - 1;
+    const long long id = pidx(P, i, j), i1 = id - 1, i2 = id - 2;
+    const double vj = ldg(P.vjac + id);
+    const double xi_x = ldg(P.vmxx + id) * vj;
+    const double xi_y = ldg(P.vmxy + id) * vj;
+    const double sn = hypot(xi_x, xi_y);
+    const double n1 = xi_x / sn, n2 = xi_y / sn;
+    auto ddn = [&](const double* f) {
+        return sn * 0.5 * (3.0 * ldg(f + id) - 4.0 * ldg(f + i1) + ldg(f + i2));
+    };
+    const double rr = ldg(PRHO(P) + id), cc0 = ldg(PC(P) + id), pp = ldg(PP(P) + id);
+    const double uu = ldg(PU(P) + id), vv = ldg(PV(P) + id);
+    const double un = n1 * uu + n2 * vv;
+    const double M = smin(fabs(un) / cc0, 0.99);
+    const double drdn = ddn(PRHO(P));
+    const double dpdn = ddn(PP(P));
+    const double dundn = n1 * ddn(PU(P)) + n2 * ddn(PV(P));
+    const double dutdn = -n2 * ddn(PU(P)) + n1 * ddn(PV(P));
+    const double K = P.sigma_out_right * cc0 * (1.0 - M * M) / P.lx;
+    const double L1 = K * (pp - P.p_target_right);
+    const double out = un > 0.0 ? un : 0.0;
+    const double L2 = out * (cc0 * cc0 * drdn - dpdn);
+    const double L3 = out * dutdn;
+    const double L5 = (un + cc0) * (dpdn + rr * cc0 * dundn);
+    const double drdt = -(L2 + 0.5 * (L5 + L1)) / (cc0 * cc0);
+    const double dundt = -(L5 - L1) / (2.0 * rr * cc0);
+    const double dutdt = -L3;
+    const double dpdt = -0.5 * (L5 + L1);
+    double Y[NS], dYdt[NS];
+    double sumRdY = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        Y[s] = ldg(PY(P, s) + id);
+        dYdt[s] = -out * ddn(PY(P, s));
+        sumRdY += divW(P.mix.sp[s], P.mix.R) * dYdt[s];
+    }
+    const double rbar = r_specific<NS>(Y, P.mix);
+    const double Tt = ldg(PT(P) + id);
+    const double dTdt = Tt * (dpdt / pp - drdt / rr - sumRdY / rbar);
+    const double dudt = n1 * dundt - n2 * dutdt;
+    const double dvdt = n2 * dundt + n1 * dutdt;
+    const double k = 0.5 * (uu * uu + vv * vv);
+    const double e = e_mass_rs<NS>(Tt, Y, rbar, P.mix);
+    const double cv = cp_mass<NS>(Tt, Y, P.mix) - rbar;
+    double sum_es_dY = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const double esn = h_species(Tt, P.mix.sp[s], P.mix.R) - divW(P.mix.sp[s], P.mix.R) * Tt;
+        sum_es_dY += esn * dYdt[s];
+    }
+    double dU[NS + 3];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) dU[s] = Y[s] * drdt + rr * dYdt[s];
+    dU[NS] = uu * drdt + rr * dudt;
+    dU[NS + 1] = vv * drdt + rr * dvdt;
+    dU[NS + 2] = (e + k) * drdt + rr * cv * dTdt + rr * sum_es_dY + rr * (uu * dudt + vv * dvdt);
+    const double invJ = 1.0 / ldg(P.jac + id);
+#pragma unroll
+    for (int c = 0; c < NS + 3; ++c) dF[c] = -dU[c] * invJ;
+}
+
+// ---------------------------------------------------------------- assemble + update
+// MODE 0: rhs only (compute_rhs, solver.hpp:185-232).  MODE 1: stage 1
+// U <- U0 + dt r (axpy_interior :799-807).  MODE 2: U <- U0 + w((U-U0) + dt r)
+// (blend_interior :810-821).  MODE 1/2 also clip + validate (post_stage
+// :826-849) and carry the ghost ring of Ucur into Uout.
+template <int NS, int MODE>
+__global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParams P,
+                                                  const double* __restrict__ U0,
+                                                  const double* __restrict__ Ucur,
+                                                  double* __restrict__ Uout, double dt,
+                                                  double w, double t_stage, int stage,
+                                                  int step, int clip_slot) {
+    constexpr int NC = NS + 3;
+    __shared__ unsigned long long s_clip;
+    if (threadIdx.x == 0) s_clip = 0ull;
+    __syncthreads();
+    const bool dead = failed(P.err);
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double clip = 0.0;
+    if (!dead && id < P.plane) {
+        const int ip = (int)(id % P.sx), jp = (int)(id / P.sx);
+        const int i = ip - P.g, j = jp - P.g;
+        const bool interior = i >= 0 && i < P.nx && j >= 0 && j < P.ny;
+        if (!interior) {
+            if (MODE != 0) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = Ucur[c * P.plane + id];
+            }
+        } else {
+            double r[NC];
+            const long long fxp = (long long)(P.nx + 1) * P.ny;
+            const long long fyp = (long long)P.nx * (P.ny + 1);
+            const long long fx = (long long)j * (P.nx + 1) + i;
+            const long long fy = (long long)j * P.nx + i;
+            double dFl[NC];
+            const bool lodi = P.lodi && i == P.nx - 1;
+            if (lodi) lodi_dfx<NS>(P, j, dFl);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const double dF = lodi ? dFl[c] : P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
+                const double dG = P.Gy[c * fyp + fy + P.nx] - P.Gy[c * fyp + fy];
+                r[c] = -(dF + dG);
+            }
+            if (P.viscous) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double* Fv = P.Fv + c * P.plane;
+                    const double* Gv = P.Gv + c * P.plane;
+                    const double dVx = 0.5 * (Fv[id + 1] - Fv[id - 1]);
+                    const double dVy = 0.5 * (Gv[id + P.sx] - Gv[id - P.sx]);
+                    r[c] += dVx + dVy;
+                }
+            }
+            const double J = ldg(P.jac + id);
+            const double invJ = 1.0 / J;
+            if (P.mech.present) {
+                double Y[NS], wdot[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) Y[s] = ldg(PY(P, s) + id);
+                source_terms<NS>(ldg(PRHO(P) + id), ldg(PT(P) + id), Y, P.mix, P.mech, wdot);
+#pragma unroll
+                for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
+            }
+            if (P.laser.on)
+                r[NS + 2] += laser_power(ldg(P.xc + id), ldg(P.yc + id), t_stage, P.laser) * invJ;
+            const unsigned long long cell = (unsigned long long)j * P.nx + i;
+            bool bad = false;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) bad |= !isfinite(r[c]);
+            if (bad) {
+                report(P.err, stage, PH_RHS, cell, 0, step);
+            } else if (MODE == 0) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = r[c];
+            } else {
+                double o[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double b = U0[c * P.plane + id];
+                    if (MODE == 1) o[c] = b + dt * r[c];
+                    else o[c] = b + w * ((Ucur[c * P.plane + id] - b) + dt * r[c]);
+                }
+                double rsum = 0.0;
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    if (o[s] < 0.0) {
+                        clip = smax(clip, -o[s] * J);
+                        o[s] = 0.0;
+                    }
+                    rsum += o[s];
+                }
+                bool fin = true;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) fin &= isfinite(o[c]);
+                if (!(rsum > 0.0)) report(P.err, stage, PH_POST, cell * 2, 0, step);
+                else if (!fin) report(P.err, stage, PH_POST, cell * 2 + 1, 0, step);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = o[c];
+            }
+        }
+    }
+    if (MODE != 0) {
+        if (clip > 0.0) atomicMax(&s_clip, (unsigned long long)__double_as_longlong(clip));
+        __syncthreads();
+        if (threadIdx.x == 0 && s_clip) atomicMax(&P.red[2 + clip_slot], s_clip);
+    }
+}
+
+// ---------------------------------------------------------------- stable dt
+// stable_dt's per-cell spectra (solver.hpp:246-289); max/min are order-free,
+// so the reduction is bit-identical to the serial loop.
+template <int NS>
+__global__ void __launch_bounds__(256) k_dt(const __grid_constant__ KParams P) {
+    __shared__ unsigned long long s_lam, s_chem;
+    if (threadIdx.x == 0) {
+        s_lam = 0ull;
+        s_chem = 0x7ff0000000000000ull;  // +inf
+    }
+    __syncthreads();
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double lam_loc = 0.0, chem_loc = __longlong_as_double(0x7ff0000000000000ll);
+    if (t < (long long)P.nx * P.ny) {
+        const int i = (int)(t % P.nx), j = (int)(t / P.nx);
+        const long long id = pidx(P, i, j);
+        const double J = ldg(P.jac + id);
+        const double mxx = ldg(P.mxx + id), mxy = ldg(P.mxy + id);
+        const double mex = ldg(P.mex + id), mey = ldg(P.mey + id);
+        const double sx = hypot(mxx, mxy);
+        const double sy = hypot(mex, mey);
+        const double u = ldg(PU(P) + id), v = ldg(PV(P) + id), c = ldg(PC(P) + id);
+        const double ux = mxx * u + mxy * v;
+        const double uy = mex * u + mey * v;
+        double lam = (fabs(ux) + c * sx + fabs(uy) + c * sy) * J;
+        double Y[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) Y[s] = ldg(PY(P, s) + id);
+        const double rho = ldg(PRHO(P) + id), T = ldg(PT(P) + id);
+        if (P.viscous) {
+            double X[NS];
+            mole_fractions<NS>(Y, P.mix, X);
+            double mu, lambda, D, cp;
+            transport<NS>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
+            const double nu = smax(2.0 * mu / rho, smax(lambda / (rho * cp), D));
+            lam += 2.0 * nu * (sx * sx + sy * sy) * J * J;
+        }
+        lam_loc = smax(0.0, lam);
+        if (P.mech.present && P.chem_dt_limit) {
+            double wdot[NS];
+            source_terms<NS>(rho, T, Y, P.mix, P.mech, wdot);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const double wv = fabs(wdot[s]);
+                if (wv > 0.0) {
+                    const double mass = rho * smax(Y[s], 1e-3);
+                    chem_loc = smin(chem_loc, P.chem_dt_factor * mass / wv);
+                }
+            }
+        }
+    }
+    if (lam_loc > 0.0) atomicMax(&s_lam, (unsigned long long)__double_as_longlong(lam_loc));
+    if (chem_loc < __longlong_as_double(0x7ff0000000000000ll))
+        atomicMin(&s_chem, (unsigned long long)__double_as_longlong(chem_loc));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_lam) atomicMax(&P.red[0], s_lam);
+        if (s_chem != 0x7ff0000000000000ull) atomicMin(&P.red[1], s_chem);
+    }
+}
+
+// ---------------------------------------------------------------- launcher table
+struct KernelSet {
+    int (*bc)(const KParams&, double* Ut, int stage, int step, cudaStream_t);
+    int (*prim)(const KParams&, const double* Ut, int stage, int step, cudaStream_t);
+    int (*faces)(const KParams&, int teno, int chr, const double* Ut, int stage, int step,
+                 cudaStream_t);
+    int (*visc)(const KParams&, int stage, int step, cudaStream_t);
+    int (*assemble)(const KParams&, int mode, const double* U0, const double* Ucur,
+                    double* Uout, double dt, double w, double t_stage, int stage, int step,
+                    int clip_slot, cudaStream_t);
+    int (*dt)(const KParams&, cudaStream_t);
+};
+
+template <int NS> struct Launch {
+    static int bc(const KParams& P, double* Ut, int stage, int step, cudaStream_t s) {
+        const int nxp = P.ny, nyp = P.nx + 2 * P.g;
+        k_bc<NS><<<(2 * nxp + 127) / 128, 128, 0, s>>>(P, Ut, 0, stage, step);
+        k_bc<NS><<<(2 * nyp + 127) / 128, 128, 0, s>>>(P, Ut, 1, stage, step);
+        return 2;
+    }
+    static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
+        const unsigned nb = (unsigned)((P.plane + 255) / 256);
+        if (P.viscous) k_prim<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step);
+        else k_prim<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step);
+        return 1;
+    }
+    template <bool TENO, bool CHAR>
+    static void faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
+        dim3 gx((P.nx + 1 + 127) / 128, P.ny);
+        k_faces<NS, 0, TENO, CHAR><<<gx, 128, 0, s>>>(P, Ut, stage, step);
+        dim3 gy((P.nx + 127) / 128, P.ny + 1);
+        k_faces<NS, 1, TENO, CHAR><<<gy, 128, 0, s>>>(P, Ut, stage, step);
+    }
+    static int faces(const KParams& P, int teno, int chr, const double* Ut, int stage, int step,
+                     cudaStream_t s) {
+        if (teno && chr) faces_t<true, true>(P, Ut, stage, step, s);
+        else if (teno) faces_t<true, false>(P, Ut, stage, step, s);
+        else if (chr) faces_t<false, true>(P, Ut, stage, step, s);
+        else faces_t<false, false>(P, Ut, stage, step, s);
+        return 2;
+    }
+    static int visc(const KParams& P, int stage, int step, cudaStream_t s) {
+        const long long n = (long long)(P.nx + 2) * (P.ny + 2);
+        k_visc<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, stage, step);
+        return 1;
+    }
+    static int assemble(const KParams& P, int mode, const double* U0, const double* Ucur,
+                        double* Uout, double dt, double w, double t_stage, int stage, int step,
+                        int clip_slot, cudaStream_t s) {
+        const unsigned nb = (unsigned)((P.plane + 255) / 256);
+        if (mode == 0)
+            k_assemble<NS, 0><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
+                                                 clip_slot);
+        else if (mode == 1)
+            k_assemble<NS, 1><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
+                                                 clip_slot);
+        else
+            k_assemble<NS, 2><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
+                                                 clip_slot);
+        return 1;
+    }
+    static int dt(const KParams& P, cudaStream_t s) {
+        const long long n = (long long)P.nx * P.ny;
+        k_dt<NS><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P);
+        return 1;
+    }
+    static KernelSet make() {
+        return KernelSet{&bc, &prim, &faces, &visc, &assemble, &dt};
+    }
+};
+
+KernelSet kernel_set(int ns);
+
+}  // namespace ign

@@ -1,0 +1,206 @@
+"""Host-side mirror of ``ignis::Simulation`` (solver.hpp:53-853) over the C ABI.
+
+Method names, argument meaning and error behaviour follow the reference class
+so parity tests read like the reference's own usage:
+
+    sim = Simulation(case.cfg)
+    sim.set_initial_condition(case.ic)
+    sim.prepare_stage(1)
+    rhs = sim.compute_rhs(t, 1)
+    sim.rk3_step(dt)
+
+The same wrapper drives the B200 library (``ign_*``) and, in tests/bench
+only, the CPU oracle (``ignref_*``) — it is handed a bound function table.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import abi
+from .errors import UsageError, raise_for
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Simulation:
+    def __init__(self, cfg: abi.Config, api: Optional[dict] = None):
+        if api is None:
+            from . import native
+            api = native.api()
+        self._api = api
+        self.cfg = cfg
+        h = C.c_void_p()
+        self._err = abi.Error()
+        st = api["create"](C.byref(cfg), C.byref(h))
+        if st != abi.IGN_OK:
+            # creation errors carry no context; re-run the host validation for text
+            raise_for(st, self._create_error(st))
+        self._h = h
+        nx, ny, g, ns = (C.c_int32() for _ in range(4))
+        api["dims"](h, C.byref(nx), C.byref(ny), C.byref(g), C.byref(ns))
+        self.nx, self.ny, self.g, self.ns = nx.value, ny.value, g.value, ns.value
+        self.nc = self.ns + 3
+        self.shape = (self.ny + 2 * self.g, self.nx + 2 * self.g)
+        self.plane = self.shape[0] * self.shape[1]
+
+    def _create_error(self, st):
+        e = abi.Error()
+        e.status = st
+        e.msg = b"ign_create failed (configuration rejected)"
+        return e
+
+    # ------------------------------------------------------------ plumbing
+    def _check(self, st: int):
+        if st != abi.IGN_OK:
+            self._api["last_error"](self._h, C.byref(self._err))
+            raise_for(st, self._err)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._api["destroy"](self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ------------------------------------------------------------ setup
+    def mesh_xy(self):
+        x = np.empty(self.plane)
+        y = np.empty(self.plane)
+        self._check(self._api["get_mesh"](self._h, _dptr(x), _dptr(y)))
+        return x.reshape(self.shape), y.reshape(self.shape)
+
+    def metrics(self, which: int = 0) -> np.ndarray:
+        out = np.empty(5 * self.plane)
+        self._check(self._api["get_metrics"](self._h, which, _dptr(out)))
+        return out.reshape((5,) + self.shape)
+
+    def set_initial_condition(self, ic: Callable):
+        """solver.hpp:115-128 with a vectorised primitive function of the
+        physical node coordinates: ic(X, Y) -> (rho, u, v, T, [Y_s])."""
+        X, Y = self.mesh_xy()
+        rho, u, v, T, Ys = ic(X, Y)
+        prim = np.empty((4 + self.ns,) + self.shape)
+        prim[0], prim[1], prim[2], prim[3] = rho, u, v, T
+        for s in range(self.ns):
+            prim[4 + s] = Ys[s]
+        prim = np.ascontiguousarray(prim)
+        self._check(self._api["set_initial_primitives"](self._h, _dptr(prim)))
+
+    def set_state(self, Ut: np.ndarray, T: Optional[np.ndarray] = None):
+        Ut = np.ascontiguousarray(Ut, dtype=np.float64).reshape(-1)
+        if Ut.size != self.nc * self.plane:
+            raise UsageError("set_state: wrong Ut size")
+        Tp = None
+        if T is not None:
+            T = np.ascontiguousarray(T, dtype=np.float64).reshape(-1)
+            Tp = _dptr(T)
+        self._check(self._api["set_state"](self._h, _dptr(Ut), Tp))
+
+    @property
+    def Ut(self) -> np.ndarray:
+        out = np.empty(self.nc * self.plane)
+        self._check(self._api["get_state"](self._h, _dptr(out)))
+        return out.reshape((self.nc,) + self.shape)
+
+    def cache(self) -> dict:
+        out = np.empty((6 + self.ns) * self.plane)
+        self._check(self._api["get_cache"](self._h, _dptr(out)))
+        out = out.reshape((6 + self.ns,) + self.shape)
+        d = {k: out[i] for i, k in enumerate(("rho", "u", "v", "p", "T", "c"))}
+        d["Y"] = out[6:]
+        return d
+
+    @property
+    def time(self) -> float:
+        t, it = C.c_double(), C.c_int64()
+        self._api["get_time"](self._h, C.byref(t), C.byref(it))
+        return t.value
+
+    @property
+    def iter(self) -> int:
+        t, it = C.c_double(), C.c_int64()
+        self._api["get_time"](self._h, C.byref(t), C.byref(it))
+        return it.value
+
+    def set_time(self, t: float, it: int = 0):
+        self._check(self._api["set_time"](self._h, t, it))
+
+    def set_integrator(self, fixed_dt=0.0, t_end=0.0, max_iter=2**63 - 1,
+                       chem_dt_limit=True, chem_dt_factor=0.1):
+        ig = abi.Integrator(fixed_dt, t_end, max_iter, int(chem_dt_limit), 0,
+                            chem_dt_factor)
+        self._check(self._api["set_integrator"](self._h, C.byref(ig)))
+
+    # ------------------------------------------------------------ hot path
+    def refill_ghosts(self):
+        self._check(self._api["refill_ghosts"](self._h))
+
+    def refresh_primitives(self, stage: int = 0):
+        self._check(self._api["refresh_primitives"](self._h, stage))
+
+    def prepare_stage(self, stage: int = 1):
+        self._check(self._api["prepare_stage"](self._h, stage))
+
+    def compute_rhs(self, t_stage: float, stage: int = 0) -> np.ndarray:
+        out = np.empty(self.nc * self.plane)
+        self._check(self._api["compute_rhs"](self._h, t_stage, stage, _dptr(out)))
+        return out.reshape((self.nc,) + self.shape)
+
+    def stable_dt(self) -> float:
+        dt = C.c_double()
+        self._check(self._api["stable_dt"](self._h, C.byref(dt)))
+        return dt.value
+
+    def rk3_step(self, dt: float):
+        self._check(self._api["rk3_step"](self._h, dt))
+
+    def rk3_steps(self, dt: float, n: int):
+        """n x (rk3_step(dt); prepare_stage(1)) — advance()'s loop body with a
+        pinned step (solver.hpp:344-345), no host round trip in between."""
+        self._check(self._api["rk3_steps"](self._h, dt, n))
+
+    def advance(self, hook: Optional[Callable] = None):
+        if hook is None:
+            cb = abi.STEP_HOOK()
+        else:
+            cb = abi.STEP_HOOK(lambda ctx, user: int(hook(self) or 0))
+        self._check(self._api["advance"](self._h, cb, None))
+
+    # ------------------------------------------------------------ diagnostics
+    def conserved_totals(self) -> np.ndarray:
+        out = np.empty(self.nc)
+        self._check(self._api["conserved_totals"](self._h, _dptr(out)))
+        return out
+
+    def product_mole_fraction(self) -> float:
+        out = C.c_double()
+        self._check(self._api["product_mole_fraction"](self._h, C.byref(out)))
+        return out.value
+
+    @property
+    def last_clip(self) -> float:
+        out = C.c_double()
+        self._check(self._api["last_clip"](self._h, C.byref(out)))
+        return out.value
+
+    def kernel_launches(self) -> int:
+        return int(self._api["kernel_launches"](self._h))
