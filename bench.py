@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 RHS + SSP-RK3 path (BASELINE.json metric:
+"FP64 cell-updates/s per RK step").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--n 4096]
+
+A "step" is one full SSP-RK3 step (three RHS evaluations + updates + the
+advance-loop prepare_stage(1), solver.hpp:304-345) over the whole grid.
+
+Workload (config.workload): 2D compressible viscous Taylor-Green vortex at
+4096^2 interior cells = 16.8 M cells, the same cell count as BASELINE
+configs[1] (TGV 256^3); the reference is 2D-only so its 3D case has no oracle
+(SURVEY §0).  γ-gas, TENO6 characteristic, Re 1600, Ma 0.1, fixed dt.
+The state (4 x 538 MB) is far larger than the 126 MB L2, so no flush is needed.
+
+value   = cells x K / device time of K steps, inputs resident in HBM (CUDA
+          events on the library's stream, max over ranks);
+e2e     = same metric through the C ABI with host buffers: every step copies
+          the state in from pinned host memory and back out;
+roofline = the dominant kernel class (inviscid faces) against the measured
+          FP64 peak (DFMA microbenchmark run here), algorithmic FP64 ops per
+          cell-stage from the reference's own code;
+cpu_baseline = the CPU oracle (unmodified reference, all host cores) on a
+          bounded sample of the same workload.
+
+Multi-GPU (torchrun): one rank per GPU, weak scaling.  Until the slab halo
+exchange lands each rank advances an independent replica of the per-GPU
+problem (parallelism "replicas"); no collective is on the data path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 cell-updates/s per RK step, TGV 256^3 & H2/O2 flame, 1/2/4/8 B200"
+UNIT = "cell-updates/s"
+# algorithmic FP64 ops (add+mul+div, reference's own code) per
+# cell and stage for the inviscid part of the 2D γ-gas TENO6 characteristic
+# case, and per cell-step for the whole step (TENO6 char + viscous).
+INVISCID_OPS_PER_CELL_STAGE = 4274
+STEP_OPS_PER_CELL = 14333
+BYTES_PER_CELL_STEP = lambda nc: 8 * (8 * nc + 6)  # noqa: E731  SURVEY §8d B_alg
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for k, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_case(args):
+    from paper_2202_02319_b200 import configs
+    if args.case == "h2o2":
+        return configs.h2o2_counterflow(args.n), f"H2/O2 one-step counterflow flame {args.n}^2 (configs[2])"
+    return (configs.tgv2d(args.n),
+            f"TGV 2D {args.n}x{args.n} viscous, TENO6 characteristic, gamma-gas, fixed dt "
+            f"(2D analogue of configs[1] TGV 256^3: same {args.n * args.n / 1e6:.1f}M cells; "
+            "the reference is 2D-only)")
+
+
+def cpu_reference_rate(n: int, target_s: float, threads: int, case: str = "tgv"):
+    """Times the CPU oracle (the unmodified reference) on an n^2 sample."""
+    from oracle import ref
+    from paper_2202_02319_b200 import configs
+    c = configs.tgv2d(n) if case == "tgv" else configs.h2o2_counterflow(n)
+    sim = ref.simulation(c.cfg, partitions=threads)
+    sim.set_initial_condition(c.ic)
+    sim.prepare_stage(1)
+    t0 = time.perf_counter()
+    sim.rk3_steps(c.dt, 1)
+    one = time.perf_counter() - t0
+    k = max(1, int(target_s / max(one, 1e-6)))
+    t0 = time.perf_counter()
+    sim.rk3_steps(c.dt, k)
+    el = time.perf_counter() - t0
+    return n * n * k / el, k, el
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU implementation on the host cores."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from oracle import ref
+    from paper_2202_02319_b200 import configs
+    n = min(args.n, 1024)
+    c = configs.tgv2d(n) if args.case == "tgv" else configs.h2o2_counterflow(n)
+    sim = ref.simulation(c.cfg, partitions=threads)
+    sim.set_initial_condition(c.ic)
+    sim.prepare_stage(1)
+    sim.rk3_steps(c.dt, args.warmup)
+    t0 = time.perf_counter()
+    sim.rk3_steps(c.dt, args.steps)
+    el = time.perf_counter() - t0
+    rate = n * n * args.steps / el
+    _, workload = make_case(args)
+    sample = (f"{n}x{n} sub-problem of the same workload per step (same physics and scheme), "
+              f"reference advance() loop body, {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload, "global_batch": n * n, "parallelism": "cpu-threads"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--case", default="tgv", choices=["tgv", "h2o2"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo" if args.impl == "reference" else "nccl")
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2202_02319_b200 import Simulation, native
+
+    case, workload = make_case(args)
+    case.cfg.device = local
+    sim = Simulation(case.cfg)
+    sim.set_initial_condition(case.ic)
+    sim.prepare_stage(1)
+    cells = case.cfg.nx * case.cfg.ny
+    nc = sim.nc
+    stream = torch.cuda.ExternalStream(sim.stream_handle(), device=local)
+
+    sim.rk3_steps(case.dt, args.warmup)  # untimed warm-up
+    launches0 = sim.kernel_launches()
+    sim.profile_enable(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        sim.rk3_steps(case.dt, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = sim.profile_read()
+    sim.profile_enable(False)
+    launches = sim.kernel_launches() - launches0
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = world * cells * args.steps / (ms_max / 1e3)
+
+    # ---------------- e2e through the C ABI with pinned host buffers
+    host = torch.empty(nc * sim.plane, dtype=torch.float64).pin_memory()
+    hbuf = host.numpy()
+    hbuf[:] = sim.Ut.reshape(-1)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        sim.set_state(hbuf)          # H2D of the step's input state
+        sim.rk3_steps(case.dt, 1)
+        sim._api["get_state"](sim.handle, hbuf.ctypes.data_as(
+            __import__("ctypes").POINTER(__import__("ctypes").c_double)))  # D2H result
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = world * cells * args.e2e_steps / (e2e_ms / 1e3)
+    bytes_state = nc * sim.plane * 8
+
+    # ---------------- roofline of the dominant kernel class (inviscid faces)
+    peak = __import__("ctypes").c_double()
+    native.api()["probe_fp64_peak"](local, __import__("ctypes").byref(peak))
+    total_prof = sum(v[0] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k][0])
+    f_ms, f_n = prof["faces"]
+    face_ops = cells * INVISCID_OPS_PER_CELL_STAGE  # per launch = one stage, x + y
+    achieved = face_ops / (f_ms / f_n / 1e3) / 1e12 if f_n else None
+    roofline = {
+        "bound": "fp64", "kernel": "k_faces<x>+k_faces<y> (inviscid TENO6 characteristic)",
+        "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+        "frac": achieved / peak.value if achieved and peak.value else None,
+        "traffic": None,
+        "ops_per_launch": face_ops, "avg_launch_ms": f_ms / f_n if f_n else None,
+        "share_of_step": f_ms / total_prof if total_prof else None,
+        "peak_source": "live DFMA-chain microbenchmark (ign_probe_fp64_peak), 2 flop/FMA",
+        "whole_step": {
+            "fp64_tflops": value / world * STEP_OPS_PER_CELL / 1e12,
+            "fp64_frac": value / world * STEP_OPS_PER_CELL / 1e12 / peak.value if peak.value else None,
+            "hbm_gbs": value / world * BYTES_PER_CELL_STEP(nc) / 1e9,
+            "hbm_frac": value / world * BYTES_PER_CELL_STEP(nc) / 1e9 / 6451.8,
+        },
+        "kernel_ms": {k: round(v[0], 3) for k, v in prof.items() if v[1]},
+        "kernel_launches": {k: v[1] for k, v in prof.items() if v[1]},
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            rate, k, el = cpu_reference_rate(512, args.cpu_seconds, threads, args.case)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"512x512 sub-problem of the same workload, {k} RK3 steps in "
+                             f"{el:.1f} s, unmodified reference via oracle/_ref, {threads} threads"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic TGV initial condition)",
+            "config": {"workload": workload, "global_batch": world * cells,
+                       "cells_per_gpu": cells, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "state 4x538 MB per buffer >> 126 MB L2, no flush needed",
+                       "dt": case.dt},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
+                    "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -231,6 +231,24 @@ int ign_host_mesh(const ign_config* cfg, double* x, double* y, ign_error* err);
 /* Number of kernels this context has launched since creation. */
 int64_t ign_kernel_launches(const ign_context* ctx);
 
+/* Live per-kernel-class device time: CUDA events recorded on the context's
+ * stream around every launch of a class while enabled (enable resets). */
+#define IGN_PROF_CLASSES 8
+#define IGN_PROF_BC 0       /* ghost fill (x+y passes)           */
+#define IGN_PROF_PRIM 1     /* primitive cache / Newton T solve  */
+#define IGN_PROF_FACES 2    /* inviscid faces, x and y           */
+#define IGN_PROF_VISC 3     /* viscous node fluxes               */
+#define IGN_PROF_ASSEMBLE 4 /* RHS assembly + RK update + clip   */
+#define IGN_PROF_DT 5       /* stable_dt reduction               */
+int ign_profile_enable(ign_context* ctx, int on);
+int ign_profile_read(ign_context* ctx, double* ms, int64_t* counts);
+/* The cudaStream_t every kernel of this context runs on (for external events). */
+void* ign_stream_handle(const ign_context* ctx);
+
+/* Measured FP64 FMA peak of a device: a DFMA-chain kernel over every SM
+ * (2 flops per FMA); the roofline denominator of the FP64-bound path. */
+int ign_probe_fp64_peak(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -164,14 +164,26 @@ SIGNATURES = {
     "kernel_launches": (C.c_int64, [_P]),
 }
 
+# measurement entry points only the B200 library has (no oracle analogue)
+PRODUCT_ONLY = {
+    "profile_enable": (_I, [_P, _I]),
+    "profile_read": (_I, [_P, _D, C.POINTER(C.c_int64)]),
+    "stream_handle": (C.c_void_p, [_P]),
+    "probe_fp64_peak": (_I, [_I, _D]),
+}
+PROF_CLASSES = ("bc", "prim", "faces", "visc", "assemble", "dt", "r6", "r7")
+
 # entry points of include/ignis_b200.h that every product build must export
-PUBLIC_SYMBOLS = sorted(SIGNATURES)
+PUBLIC_SYMBOLS = sorted(set(SIGNATURES) | set(PRODUCT_ONLY))
 
 
 def bind(lib: C.CDLL, prefix: str) -> dict:
     """Returns {name: bound function} for every ABI entry point."""
     out = {}
-    for name, (res, args) in SIGNATURES.items():
+    sigs = dict(SIGNATURES)
+    if prefix == "ign_":
+        sigs.update(PRODUCT_ONLY)
+    for name, (res, args) in sigs.items():
         fn = getattr(lib, prefix + name)
         fn.restype = res
         fn.argtypes = args

@@ -342,7 +342,7 @@ def h2o2_counterflow(n: int = 512, *, scheme: str = "teno6", split: str = "char"
         return rho, u, v, T, Ys
 
     dx = L / n
-    return Case(f"h2o2_{nx}x{ny}", cfg, ic, 0.15 * dx / 400.0)
+    return Case(f"h2o2_{nx}x{ny}", cfg, ic, min(0.15 * dx / 400.0, la.sigma_t / 6.0))
 
 
 def wall_channel(n: int = 48, isothermal: bool = True, scheme: str = "teno6",

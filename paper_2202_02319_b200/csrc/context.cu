@@ -71,6 +71,13 @@ struct ign_context {
     ign_integrator integ{};
     ign_error lasterr{};
     int64_t launches = 0;
+    // live per-kernel-class timing (CUDA events on this context's stream)
+    bool prof_on = false;
+    struct Rec { int cat; cudaEvent_t a, b; };
+    std::vector<Rec> prof_pending;
+    std::vector<cudaEvent_t> prof_pool;
+    double prof_ms[IGN_PROF_CLASSES] = {};
+    int64_t prof_n[IGN_PROF_CLASSES] = {};
 };
 
 namespace {
@@ -120,9 +127,44 @@ struct DevFail {
     int step = 0;
 };
 
+cudaEvent_t prof_event(ign_context* ctx) {
+    if (!ctx->prof_pool.empty()) {
+        cudaEvent_t e = ctx->prof_pool.back();
+        ctx->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+// Runs one launcher; with profiling on, brackets it with events on the stream.
+template <class F> int timed(ign_context* ctx, int cat, F&& f) {
+    if (!ctx->prof_on) return f();
+    cudaEvent_t a = prof_event(ctx), b = prof_event(ctx);
+    cuda_check(cudaEventRecord(a, ctx->stream), "event");
+    const int n = f();
+    cuda_check(cudaEventRecord(b, ctx->stream), "event");
+    ctx->prof_pending.push_back({cat, a, b});
+    return n;
+}
+
+void prof_harvest(ign_context* ctx) {
+    for (auto& r : ctx->prof_pending) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "event time");
+        ctx->prof_ms[r.cat] += ms;
+        ++ctx->prof_n[r.cat];
+        ctx->prof_pool.push_back(r.a);
+        ctx->prof_pool.push_back(r.b);
+    }
+    ctx->prof_pending.clear();
+}
+
 DevFail sync_and_read(ign_context* ctx) {
     cuda_check(cudaStreamSynchronize(ctx->stream), "kernel execution");
     cuda_check(cudaGetLastError(), "kernel launch");
+    prof_harvest(ctx);
     ErrRec h;
     cuda_check(cudaMemcpy(&h, ctx->err, sizeof(h), cudaMemcpyDeviceToHost), "error word");
     DevFail f;
@@ -252,14 +294,28 @@ __global__ void k_clip_reset(const ErrRec* err, unsigned long long* red, int slo
 }
 
 void launch_prepare(ign_context* ctx, double* U, int stage, int step) {
-    ctx->launches += ctx->ks.bc(ctx->kp, U, stage, step, ctx->stream);
-    ctx->launches += ctx->ks.prim(ctx->kp, U, stage, step, ctx->stream);
+    ctx->launches += timed(ctx, IGN_PROF_BC,
+                           [&] { return ctx->ks.bc(ctx->kp, U, stage, step, ctx->stream); });
+    ctx->launches += timed(ctx, IGN_PROF_PRIM,
+                           [&] { return ctx->ks.prim(ctx->kp, U, stage, step, ctx->stream); });
 }
 
 void launch_fluxes(ign_context* ctx, const double* U, int stage, int step) {
-    ctx->launches += ctx->ks.faces(ctx->kp, ctx->cfg.scheme.scheme, ctx->cfg.scheme.split, U,
-                                   stage, step, ctx->stream);
-    if (ctx->cfg.viscous) ctx->launches += ctx->ks.visc(ctx->kp, stage, step, ctx->stream);
+    ctx->launches += timed(ctx, IGN_PROF_FACES, [&] {
+        return ctx->ks.faces(ctx->kp, ctx->cfg.scheme.scheme, ctx->cfg.scheme.split, U, stage,
+                             step, ctx->stream);
+    });
+    if (ctx->cfg.viscous)
+        ctx->launches += timed(ctx, IGN_PROF_VISC,
+                               [&] { return ctx->ks.visc(ctx->kp, stage, step, ctx->stream); });
+}
+
+int launch_assemble(ign_context* ctx, int mode, const double* U0, const double* Ucur,
+                    double* Uout, double dt, double w, double t, int stage, int step, int slot) {
+    return timed(ctx, IGN_PROF_ASSEMBLE, [&] {
+        return ctx->ks.assemble(ctx->kp, mode, U0, Ucur, Uout, dt, w, t, stage, step, slot,
+                                ctx->stream);
+    });
 }
 
 // One rk3_step (solver.hpp:304-332) enqueued without a host round trip;
@@ -272,18 +328,17 @@ void launch_step(ign_context* ctx, int a, double time, double dt, int step, bool
     double** S = ctx->S;
     // Stage 1: U <- U0 + dt L(U0)   (ghosts/cache already fresh)
     launch_fluxes(ctx, S[a], 1, step);
-    ctx->launches += ctx->ks.assemble(ctx->kp, 1, S[a], S[a], S[b], dt, 0.0, time, 1, step,
-                                      slot + 0, ctx->stream);
+    ctx->launches += launch_assemble(ctx, 1, S[a], S[a], S[b], dt, 0.0, time, 1, step, slot + 0);
     launch_prepare(ctx, S[b], 2, step);
     // Stage 2: U <- U0 + 1/4 [(U1 - U0) + dt L(U1)]
     launch_fluxes(ctx, S[b], 2, step);
-    ctx->launches += ctx->ks.assemble(ctx->kp, 2, S[a], S[b], S[c], dt, 0.25, time + dt, 2,
-                                      step, slot + 1, ctx->stream);
+    ctx->launches += launch_assemble(ctx, 2, S[a], S[b], S[c], dt, 0.25, time + dt, 2, step,
+                                     slot + 1);
     launch_prepare(ctx, S[c], 3, step);
     // Stage 3: U <- U0 + 2/3 [(U2 - U0) + dt L(U2)]
     launch_fluxes(ctx, S[c], 3, step);
-    ctx->launches += ctx->ks.assemble(ctx->kp, 2, S[a], S[c], S[b], dt, 2.0 / 3.0,
-                                      time + 0.5 * dt, 3, step, slot + 2, ctx->stream);
+    ctx->launches += launch_assemble(ctx, 2, S[a], S[c], S[b], dt, 2.0 / 3.0, time + 0.5 * dt,
+                                     3, step, slot + 2);
     if (post_prepare) launch_prepare(ctx, S[b], 4, step);
 }
 
@@ -363,7 +418,7 @@ double stable_dt_impl(ign_context* ctx) {
     unsigned long long init[2] = {0ull, 0x7ff0000000000000ull};
     cuda_check(cudaMemcpyAsync(ctx->red, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream),
                "dt reset");
-    ctx->launches += ctx->ks.dt(ctx->kp, ctx->stream);
+    ctx->launches += timed(ctx, IGN_PROF_DT, [&] { return ctx->ks.dt(ctx->kp, ctx->stream); });
     check(ctx);
     unsigned long long red[2];
     cuda_check(cudaMemcpy(red, ctx->red, sizeof(red), cudaMemcpyDeviceToHost), "dt readback");
@@ -397,6 +452,11 @@ void destroy_impl(ign_context* ctx) {
     for (double* p : ctx->inflow) cudaFree(p);
     cudaFree(ctx->err);
     cudaFree(ctx->red);
+    for (auto& r : ctx->prof_pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -708,8 +768,7 @@ int ign_compute_rhs(ign_context* ctx, double t_stage, int stage, double* rhs) {
         cuda_check(cudaMemsetAsync(ctx->rhs, 0, n * sizeof(double), ctx->stream), "memset");
         const double* U = ctx->S[ctx->cur];
         launch_fluxes(ctx, U, stage, 0);
-        ctx->launches += ctx->ks.assemble(ctx->kp, 0, U, U, ctx->rhs, 0.0, 0.0, t_stage, stage,
-                                          0, 0, ctx->stream);
+        ctx->launches += launch_assemble(ctx, 0, U, U, ctx->rhs, 0.0, 0.0, t_stage, stage, 0, 0);
         check(ctx);
         if (rhs)
             cuda_check(cudaMemcpy(rhs, ctx->rhs, n * sizeof(double), cudaMemcpyDeviceToHost),
@@ -843,5 +902,30 @@ int ign_host_mesh(const ign_config* cfg, double* x, double* y, ign_error* err) {
 }
 
 int64_t ign_kernel_launches(const ign_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int ign_profile_enable(ign_context* ctx, int on) {
+    return guarded(ctx, [&] {
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        prof_harvest(ctx);
+        ctx->prof_on = on != 0;
+        for (int k = 0; k < IGN_PROF_CLASSES; ++k) {
+            ctx->prof_ms[k] = 0.0;
+            ctx->prof_n[k] = 0;
+        }
+    });
+}
+
+int ign_profile_read(ign_context* ctx, double* ms, int64_t* counts) {
+    return guarded(ctx, [&] {
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        prof_harvest(ctx);
+        for (int k = 0; k < IGN_PROF_CLASSES; ++k) {
+            ms[k] = ctx->prof_ms[k];
+            counts[k] = ctx->prof_n[k];
+        }
+    });
+}
+
+void* ign_stream_handle(const ign_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 }  // extern "C"

@@ -204,3 +204,17 @@ class Simulation:
 
     def kernel_launches(self) -> int:
         return int(self._api["kernel_launches"](self._h))
+
+    # ------------------------------------------------------------ measurement
+    def profile_enable(self, on: bool = True):
+        self._check(self._api["profile_enable"](self._h, int(on)))
+
+    def profile_read(self) -> dict:
+        ms = np.zeros(8)
+        n = np.zeros(8, dtype=np.int64)
+        self._check(self._api["profile_read"](self._h, _dptr(ms),
+                                              n.ctypes.data_as(C.POINTER(C.c_int64))))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(abi.PROF_CLASSES)}
+
+    def stream_handle(self) -> int:
+        return int(self._api["stream_handle"](self._h) or 0)

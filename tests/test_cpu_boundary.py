@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
 
 
 def test_python_binding_covers_header():
-    names = {"ign_" + n for n in abi.SIGNATURES}
+    names = {"ign_" + n for n in abi.PUBLIC_SYMBOLS}
     assert set(header_symbols()) == names
 
 
