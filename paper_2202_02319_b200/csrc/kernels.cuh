@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(128) k_faces(const __grid_constant__ KParams P
         eigen_assemble<NS>(es, amp, Fh);
     } else {
         // componentwise LLF (solver.hpp:536-567)
-        const double sf = hypot(m1f, m2f);
+        const double sf = ghypot(m1f, m2f);
         double alpha = 0.0;
 #pragma unroll
         for (int k = 0; k < W; ++k) {
@@ -473,7 +473,7 @@ __device__ void lodi_dfx(const KParams& P, int j, double* dF) {
     const double vj = ldg(P.vjac + id);
     const double xi_x = ldg(P.vmxx + id) * vj;
     const double xi_y = ldg(P.vmxy + id) * vj;
-    const double sn = hypot(xi_x, xi_y);
+    const double sn = ghypot(xi_x, xi_y);
     const double n1 = xi_x / sn, n2 = xi_y / sn;
     auto ddn = [&](const double* f) {
         return sn * 0.5 * (3.0 * ldg(f + id) - 4.0 * ldg(f + i1) + ldg(f + i2));
@@ -656,8 +656,8 @@ __global__ void __launch_bounds__(256) k_dt(const __grid_constant__ KParams P) {
         const double J = ldg(P.jac + id);
         const double mxx = ldg(P.mxx + id), mxy = ldg(P.mxy + id);
         const double mex = ldg(P.mex + id), mey = ldg(P.mey + id);
-        const double sx = hypot(mxx, mxy);
-        const double sy = hypot(mex, mey);
+        const double sx = ghypot(mxx, mxy);
+        const double sy = ghypot(mex, mey);
         const double u = ldg(PU(P) + id), v = ldg(PV(P) + id), c = ldg(PC(P) + id);
         const double ux = mxx * u + mxy * v;
         const double uy = mex * u + mey * v;
