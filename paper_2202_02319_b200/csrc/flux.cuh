@@ -55,6 +55,7 @@ IGN_HD void roe_average(double rho_l, const double* Yl, double Tl, double ul, do
 // EigenSystem (flux.hpp:55-148)
 template <int NS> struct Eigen {
     double n1, n2, s, u, v, un, ut, k, H, c, c2, kappa;
+    double c2x2, y2c2, yc2, ykappa;  // 2c^2 and RN reciprocals for fdiv
     double Y[NS];
     double Theta[NS];
 };
@@ -92,6 +93,10 @@ IGN_HD int eigen_at_state(const double* Y, double T, double uu, double vv, doubl
     if (!(c2 > 0.0)) return E_NONPOS_C2;
     e.c2 = c2;
     e.c = sqrt(c2);
+    e.c2x2 = 2.0 * c2;
+    e.y2c2 = 1.0 / e.c2x2;
+    e.yc2 = 1.0 / c2;
+    e.ykappa = 1.0 / e.kappa;
     e.H = h + e.k;
     return E_OK;
 }
@@ -107,11 +112,11 @@ IGN_HD void eigen_project(const Eigen<NS>& e, const double* q, double* w) {
     for (int sp = 0; sp < NS; ++sp) dp += e.Theta[sp] * q[sp];
     const double dun = e.n1 * q[NS] + e.n2 * q[NS + 1] - e.un * drho;
     const double dut = -e.n2 * q[NS] + e.n1 * q[NS + 1] - e.ut * drho;
-    w[0] = (dp - e.c * dun) / (2.0 * e.c2);
+    w[0] = fdiv(dp - e.c * dun, e.c2x2, e.y2c2);
 #pragma unroll
-    for (int sp = 0; sp < NS; ++sp) w[1 + sp] = q[sp] - e.Y[sp] * dp / e.c2;
+    for (int sp = 0; sp < NS; ++sp) w[1 + sp] = q[sp] - fdiv(e.Y[sp] * dp, e.c2, e.yc2);
     w[1 + NS] = dut;
-    w[2 + NS] = (dp + e.c * dun) / (2.0 * e.c2);
+    w[2 + NS] = fdiv(dp + e.c * dun, e.c2x2, e.y2c2);
 }
 
 // EigenSystem::assemble (flux.hpp:123-139): q = R w
@@ -130,7 +135,9 @@ IGN_HD void eigen_assemble(const Eigen<NS>& e, const double* w, double* q) {
     q[NS + 1] = (e.v - e.c * e.n2) * am + (e.v + e.c * e.n2) * ap + e.v * asum + e.n1 * at;
     double en = (e.H - e.c * e.un) * am + (e.H + e.c * e.un) * ap + e.ut * at;
 #pragma unroll
-    for (int sp = 0; sp < NS; ++sp) en += w[1 + sp] * (2.0 * e.k - e.Theta[sp] / e.kappa);
+    for (int sp = 0; sp < NS; ++sp)
+        en += w[1 + sp] * (2.0 * e.k - (NS > 1 ? fdiv(e.Theta[sp], e.kappa, e.ykappa)
+                                               : e.Theta[sp] / e.kappa));
     q[NS + 2] = en;
 }
 

@@ -212,6 +212,7 @@ DMix build_mix(const ign_mixture& mx) {
         d.n_exp = a.n_exp;
         d.npieces = a.npieces;
         d.unit_W = a.W == 1.0;
+        d.yW = 1.0 / a.W;
         for (int k = 0; k < a.npieces; ++k) {
             const ign_thermo_piece& q = a.pieces[k];
             DPiece& p = d.pc[k];

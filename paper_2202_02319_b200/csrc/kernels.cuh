@@ -19,83 +19,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "faces.cuh"
 #include "flux.cuh"
+#include "kernels_common.cuh"
 #include "physics.cuh"
 
 namespace ign {
-
-// ---------------------------------------------------------------- errors
-// Device error word: the first failure in the reference's own order wins via
-// atomicMin on key = stage<<60 | phase<<52 | index<<4 | sub.
-enum Phase : unsigned {
-    PH_BC = 1,     // StateError from fill_ghosts' prim_at (boundary.hpp:151-156)
-    PH_PRIM = 2,   // StepFailure "stage state failure" (solver.hpp:162-165)
-    PH_INVX = 3,   // NumericsError from inviscid x faces (solver.hpp:522-524, flux.hpp:78,99)
-    PH_INVY = 4,
-    PH_RHS = 5,    // StepFailure "non-finite RHS" (solver.hpp:225-228)
-    PH_POST = 6,   // StepFailure post_stage (solver.hpp:840-844)
-};
-constexpr unsigned long long kNoError = ~0ull;
-
-struct ErrRec {
-    unsigned long long key;
-    int32_t step;
-    int32_t _pad;
-};
-
-__device__ __forceinline__ bool failed(const ErrRec* e) {
-    return *reinterpret_cast<const volatile unsigned long long*>(&e->key) != kNoError;
-}
-
-__device__ __forceinline__ void report(ErrRec* e, unsigned stage, unsigned phase,
-                                       unsigned long long idx, unsigned sub, int step) {
-    const unsigned long long key = ((unsigned long long)stage << 60) |
-                                   ((unsigned long long)phase << 52) | (idx << 4) | sub;
-    atomicMin(&e->key, key);
-    e->step = step;
-}
-
-// ---------------------------------------------------------------- params
-struct KParams {
-    int32_t nx, ny, g, sx;
-    long long plane;
-    int32_t ns, viscous;
-    int32_t bc_type[4];  // left, right, bottom, top
-    double T_wall[4];
-    double sigma_out_right, p_target_right;
-    double lx, ly, cx, cy;
-    double ct, eps;
-    int32_t chem_dt_limit, lodi;
-    double chem_dt_factor;
-    // primitive cache block: rho,u,v,p,T,c then Y_s, then X_s (viscous)
-    double* prim;
-    const double *jac, *mxx, *mxy, *mex, *mey;       // met (inviscid)
-    const double *vjac, *vmxx, *vmxy, *vmex, *vmey;  // met_v (Central2)
-    const double *xc, *yc;                           // mesh.x, mesh.y
-    double *Fx, *Gy, *Fv, *Gv;
-    const double* inflow[4];  // per edge [t][k][u,v,T,Y_s] profile tables
-    ErrRec* err;
-    unsigned long long* red;  // [0] lam_max bits, [1] dt_chem bits, [2..7] clip bits
-    DMix mix;
-    DMech mech;
-    DLaser laser;
-};
-
-__device__ __forceinline__ long long pidx(const KParams& P, int i, int j) {
-    return (long long)(j + P.g) * P.sx + (i + P.g);
-}
-
-// primitive cache planes
-#define PRHO(P) ((P).prim)
-#define PU(P) ((P).prim + (P).plane)
-#define PV(P) ((P).prim + 2 * (P).plane)
-#define PP(P) ((P).prim + 3 * (P).plane)
-#define PT(P) ((P).prim + 4 * (P).plane)
-#define PC(P) ((P).prim + 5 * (P).plane)
-#define PY(P, s) ((P).prim + (6 + (s)) * (P).plane)
-#define PX(P, s) ((P).prim + (6 + (P).ns + (s)) * (P).plane)
-
-__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
 // ---------------------------------------------------------------- ghost fill
 // fill_ghosts (boundary.hpp:136-258).  One thread per (edge, t) runs the
@@ -267,7 +196,10 @@ __global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
 // f = m+1 in [0, nx] of row j; DIR 1: y faces of column i (threads along i
 // for coalesced stencil loads).
 template <int NS, int DIR, bool TENO, bool CHAR>
-__global__ void __launch_bounds__(128) k_faces(const __grid_constant__ KParams P,
+#ifndef IGN_FACES_MINB
+#define IGN_FACES_MINB 2
+#endif
+__global__ void __launch_bounds__(128, IGN_FACES_MINB) k_faces(const __grid_constant__ KParams P,
                                                const double* __restrict__ Ut, int stage,
                                                int step) {
     constexpr int NC = NS + 3;
@@ -293,18 +225,6 @@ __global__ void __launch_bounds__(128) k_faces(const __grid_constant__ KParams P
     const double m1f = 0.5 * (ldg(m1a + il) + ldg(m1a + ir));
     const double m2f = 0.5 * (ldg(m2a + il) + ldg(m2a + ir));
 
-    // Node pass (solver.hpp:466-479) for the 2h stencil nodes m-h+1..m+h.
-    double Fk[W][NC], Uk[W][NC], unk[W], ck[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        const long long id = base + (long long)(k - H + 1) * step_n;
-        const double J = ldg(P.jac + id);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) Uk[k][c] = ldg(Ut + c * P.plane + id) * J;
-        mapped_flux<NS>(Uk[k], ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk[k]);
-        unk[k] = ldg(PU(P) + id);  // cached u; v folded in below
-        ck[k] = ldg(PV(P) + id);
-    }
     double Fh[NC];
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
     const unsigned long long eidx = (unsigned long long)line * ((DIR == 0 ? P.nx : P.ny) + 1) + f;
@@ -327,15 +247,22 @@ __global__ void __launch_bounds__(128) k_faces(const __grid_constant__ KParams P
             report(P.err, stage, phase, eidx, 1 + est, step);
             return;
         }
-        // per-node normal speed with the face normal, cached c (solver.hpp:505-515)
-        double lf[W][NC], lu[W][NC];
+        // Node pass (solver.hpp:466-479) streamed one node at a time straight
+        // into the projections (solver.hpp:505-515), so only L F and L U of the
+        // 2h stencil nodes stay live.
+        double lf[W][NC], lu[W][NC], unk[W], ck[W];
 #pragma unroll
         for (int k = 0; k < W; ++k) {
             const long long id = base + (long long)(k - H + 1) * step_n;
-            unk[k] = es.n1 * unk[k] + es.n2 * ck[k];
+            const double J = ldg(P.jac + id);
+            double Uk[NC], Fk[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
+            mapped_flux<NS>(Uk, ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk);
+            unk[k] = es.n1 * ldg(PU(P) + id) + es.n2 * ldg(PV(P) + id);
             ck[k] = ldg(PC(P) + id);
-            eigen_project<NS>(es, Fk[k], lf[k]);
-            eigen_project<NS>(es, Uk[k], lu[k]);
+            eigen_project<NS>(es, Fk, lf[k]);
+            eigen_project<NS>(es, Uk, lu[k]);
         }
         double amp[NC];
 #pragma unroll
@@ -359,6 +286,17 @@ __global__ void __launch_bounds__(128) k_faces(const __grid_constant__ KParams P
         eigen_assemble<NS>(es, amp, Fh);
     } else {
         // componentwise LLF (solver.hpp:536-567)
+        double Fk[W][NC], Uk[W][NC], unk[W], ck[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {  // node pass (solver.hpp:466-479)
+            const long long id = base + (long long)(k - H + 1) * step_n;
+            const double J = ldg(P.jac + id);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Uk[k][c] = ldg(Ut + c * P.plane + id) * J;
+            mapped_flux<NS>(Uk[k], ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk[k]);
+            unk[k] = ldg(PU(P) + id);
+            ck[k] = ldg(PV(P) + id);
+        }
         const double sf = ghypot(m1f, m2f);
         double alpha = 0.0;
 #pragma unroll
@@ -726,10 +664,8 @@ template <int NS> struct Launch {
     }
     template <bool TENO, bool CHAR>
     static void faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        dim3 gx((P.nx + 1 + 127) / 128, P.ny);
-        k_faces<NS, 0, TENO, CHAR><<<gx, 128, 0, s>>>(P, Ut, stage, step);
-        dim3 gy((P.nx + 127) / 128, P.ny + 1);
-        k_faces<NS, 1, TENO, CHAR><<<gy, 128, 0, s>>>(P, Ut, stage, step);
+        launch_faces2<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
+        launch_faces2<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
     }
     static int faces(const KParams& P, int teno, int chr, const double* Ut, int stage, int step,
                      cudaStream_t s) {

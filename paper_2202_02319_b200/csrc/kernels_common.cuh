@@ -1,0 +1,86 @@
+// kernels_common.cuh — shared device plumbing of the stage kernels: the device
+// error word (first failure in the reference's own order) and the kernel
+// parameter block (mixture, mechanism, laser, BC data and array pointers).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "physics.cuh"
+
+namespace ign {
+
+// ---------------------------------------------------------------- errors
+// Device error word: the first failure in the reference's own order wins via
+// atomicMin on key = stage<<60 | phase<<52 | index<<4 | sub.
+enum Phase : unsigned {
+    PH_BC = 1,     // StateError from fill_ghosts' prim_at (boundary.hpp:151-156)
+    PH_PRIM = 2,   // StepFailure "stage state failure" (solver.hpp:162-165)
+    PH_INVX = 3,   // NumericsError from inviscid x faces (solver.hpp:522-524, flux.hpp:78,99)
+    PH_INVY = 4,
+    PH_RHS = 5,    // StepFailure "non-finite RHS" (solver.hpp:225-228)
+    PH_POST = 6,   // StepFailure post_stage (solver.hpp:840-844)
+};
+constexpr unsigned long long kNoError = ~0ull;
+
+struct ErrRec {
+    unsigned long long key;
+    int32_t step;
+    int32_t _pad;
+};
+
+__device__ __forceinline__ bool failed(const ErrRec* e) {
+    return *reinterpret_cast<const volatile unsigned long long*>(&e->key) != kNoError;
+}
+
+__device__ __forceinline__ void report(ErrRec* e, unsigned stage, unsigned phase,
+                                       unsigned long long idx, unsigned sub, int step) {
+    const unsigned long long key = ((unsigned long long)stage << 60) |
+                                   ((unsigned long long)phase << 52) | (idx << 4) | sub;
+    atomicMin(&e->key, key);
+    e->step = step;
+}
+
+// ---------------------------------------------------------------- params
+struct KParams {
+    int32_t nx, ny, g, sx;
+    long long plane;
+    int32_t ns, viscous;
+    int32_t bc_type[4];  // left, right, bottom, top
+    double T_wall[4];
+    double sigma_out_right, p_target_right;
+    double lx, ly, cx, cy;
+    double ct, eps;
+    int32_t chem_dt_limit, lodi;
+    double chem_dt_factor;
+    // primitive cache block: rho,u,v,p,T,c then Y_s, then X_s (viscous)
+    double* prim;
+    const double *jac, *mxx, *mxy, *mex, *mey;       // met (inviscid)
+    const double *vjac, *vmxx, *vmxy, *vmex, *vmey;  // met_v (Central2)
+    const double *xc, *yc;                           // mesh.x, mesh.y
+    double *Fx, *Gy, *Fv, *Gv;
+    const double* inflow[4];  // per edge [t][k][u,v,T,Y_s] profile tables
+    ErrRec* err;
+    unsigned long long* red;  // [0] lam_max bits, [1] dt_chem bits, [2..7] clip bits
+    DMix mix;
+    DMech mech;
+    DLaser laser;
+};
+
+__device__ __forceinline__ long long pidx(const KParams& P, int i, int j) {
+    return (long long)(j + P.g) * P.sx + (i + P.g);
+}
+
+// primitive cache planes
+#define PRHO(P) ((P).prim)
+#define PU(P) ((P).prim + (P).plane)
+#define PV(P) ((P).prim + 2 * (P).plane)
+#define PP(P) ((P).prim + 3 * (P).plane)
+#define PT(P) ((P).prim + 4 * (P).plane)
+#define PC(P) ((P).prim + 5 * (P).plane)
+#define PY(P, s) ((P).prim + (6 + (s)) * (P).plane)
+#define PX(P, s) ((P).prim + (6 + (P).ns + (s)) * (P).plane)
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+}  // namespace ign

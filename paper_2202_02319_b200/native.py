@@ -13,7 +13,7 @@ import subprocess
 from . import abi
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(PKG, "_lib", "libignis_b200.so")
+LIB = os.environ.get("IGN_LIB") or os.path.join(PKG, "_lib", "libignis_b200.so")
 _lib = None
 _api = None
 
