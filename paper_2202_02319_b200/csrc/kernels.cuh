@@ -664,8 +664,8 @@ template <int NS> struct Launch {
     }
     template <bool TENO, bool CHAR>
     static void faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        launch_faces2<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
-        launch_faces2<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
+        launch_faces3<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
+        launch_faces3<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
     }
     static int faces(const KParams& P, int teno, int chr, const double* Ut, int stage, int step,
                      cudaStream_t s) {
