@@ -572,8 +572,7 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     k.ly = cfg->ly;
     k.cx = cfg->center_x;
     k.cy = cfg->center_y;
-    k.ct = cfg->scheme.teno_ct;
-    k.eps = cfg->scheme.eps;
+    k.rp = make_recon_params(cfg->scheme.teno_ct, cfg->scheme.eps);
     k.chem_dt_limit = cfg->integ.chem_dt_limit;
     k.chem_dt_factor = cfg->integ.chem_dt_factor;
     k.prim = ctx->prim;

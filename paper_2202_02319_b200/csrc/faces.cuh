@@ -34,20 +34,20 @@ template <int NS, int DIR, bool TENO> struct FaceSmem {
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;  // faces per CTA
     static constexpr int NT = DIR == 0 ? NF + W - 1 : 32 * (NC + W - 1);
-    static constexpr int NE = 16 + 2 * NS;
+    static constexpr int NE = 14 + 2 * NS;
     static constexpr int NV = 2 * W;  // stencil vectors: F and U of each node
     double U[NC][NT];
     double F[NC][NT];
     double u[NT], v[NT], c[NT];
     double E[NE][NF];         // eigen data per face (char); [0] alpha, [1] sf (comp)
-    double L[NV][4][32];      // drho, dp, dun, dut of one group's vectors
+    double L[NV][3][32];      // dp, dun, dut of one group's vectors
     double amp[NC][NF];
     int bad[NF];
 };
 
 // Eigen data slots in FaceSmem::E
 enum : int {
-    EN1 = 0, EN2, ES, EU, EV, EUN, EUT, EK, EH, EC, EC2, EKAPPA, EC2X2, EY2C2, EYC2, EYKAPPA,
+    EN1 = 0, EN2, ES, EU, EV, EUN, EUT, EK, EH, EC, EC2, EKAPPA, EYC2, EYKAPPA,
     EY0  // then Y[NS], Theta[NS]
 };
 
@@ -157,8 +157,6 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             S.E[EC][t] = es.c;
             S.E[EC2][t] = es.c2;
             S.E[EKAPPA][t] = es.kappa;
-            S.E[EC2X2][t] = es.c2x2;
-            S.E[EY2C2][t] = es.y2c2;
             S.E[EYC2][t] = es.yc2;
             S.E[EYKAPPA][t] = es.ykappa;
 #pragma unroll
@@ -213,7 +211,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                     wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
                     wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
                 }
-                out[fl * fplane + o] = face_pm<TENO>(wp, wm, P.ct, P.eps);
+                out[fl * fplane + o] = face_pm<TENO>(wp, wm, P.rp);
             }
             continue;
         }
@@ -233,43 +231,53 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             double dp = kap * q[NS + 2] - kap * eu * q[NS] - kap * ev * q[NS + 1];
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) dp += S.E[EY0 + NS + sp][face] * q[sp];
-            S.L[vec][0][lane] = drho;
-            S.L[vec][1][lane] = dp;
-            S.L[vec][2][lane] = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
-            S.L[vec][3][lane] = -n2 * q[NS] + n1 * q[NS + 1] - ut * drho;
+            S.L[vec][0][lane] = dp;
+            S.L[vec][1][lane] = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
+            S.L[vec][2][lane] = -n2 * q[NS] + n1 * q[NS + 1] - ut * drho;
         }
         __syncthreads();
         // (b) row fl of L on the stencil, wave speed, split, reconstruction
         double amp = 0.0;
         if (live) {
             const double es = S.E[ES][face], ec = S.E[EC][face];
-            const double c2 = S.E[EC2][face], c2x2 = S.E[EC2X2][face];
-            const double y2c2 = S.E[EY2C2][face], yc2 = S.E[EYC2][face];
+            const double c2 = S.E[EC2][face], yc2 = S.E[EYC2][face];
+            // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
+            const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
             double lf[W], lu[W];
             // row fl of EigenSystem::project (flux.hpp:116-119); the field kind is
-            // warp-uniform, so the branch is hoisted out of the stencil loop
+            // warp-uniform, so the branch is hoisted out of the stencil loop, and
+            // the 2W quotients share one validity flag (one branch, exact redo)
             auto rows = [&](auto kind) {
                 constexpr int K = decltype(kind)::value;
+                bool ok = true;
+                auto row = [&](int k, int vu, bool exact) {
+                    const int t = tile_node<DIR>(g, lane, k);
+                    const int vec = 2 * k + vu;
+                    const double dp = S.L[vec][0][lane];
+                    if (K == 0) {
+                        const double a = dp - ec * S.L[vec][1][lane];
+                        return exact ? div_cold(a, c2x2) : fdiv_try(a, c2x2, y2c2, ok);
+                    } else if (K == 1) {
+                        const double a = dp + ec * S.L[vec][1][lane];
+                        return exact ? div_cold(a, c2x2) : fdiv_try(a, c2x2, y2c2, ok);
+                    } else if (K == 2) {
+                        return S.L[vec][2][lane];
+                    } else {
+                        const double qs = vu ? S.U[fl - 1][t] : S.F[fl - 1][t];
+                        const double a = S.E[EY0 + fl - 1][face] * dp;
+                        return qs - (exact ? div_cold(a, c2) : fdiv_try(a, c2, yc2, ok));
+                    }
+                };
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int t = tile_node<DIR>(g, lane, k);
+                    lf[k] = row(k, 0, false);
+                    lu[k] = row(k, 1, false);
+                }
+                if (K != 2 && !ok) {
 #pragma unroll
-                    for (int vu = 0; vu < 2; ++vu) {
-                        const int vec = 2 * k + vu;
-                        const double dp = S.L[vec][1][lane];
-                        double w;
-                        if (K == 0) {
-                            w = fdiv(dp - ec * S.L[vec][2][lane], c2x2, y2c2);
-                        } else if (K == 1) {
-                            w = fdiv(dp + ec * S.L[vec][2][lane], c2x2, y2c2);
-                        } else if (K == 2) {
-                            w = S.L[vec][3][lane];
-                        } else {
-                            const double qs = vu ? S.U[fl - 1][t] : S.F[fl - 1][t];
-                            w = qs - fdiv(S.E[EY0 + fl - 1][face] * dp, c2, yc2);
-                        }
-                        if (vu) lu[k] = w;
-                        else lf[k] = w;
+                    for (int k = 0; k < W; ++k) {
+                        lf[k] = row(k, 0, true);
+                        lu[k] = row(k, 1, true);
                     }
                 }
             };
@@ -298,7 +306,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                     wp[k] = 0.5 * (lf[k] + alpha * lu[k]);
                     wm[k] = 0.5 * (lf[k] - alpha * lu[k]);
                 }
-                amp = face_pm<TENO>(wp, wm, P.ct, P.eps);
+                amp = face_pm<TENO>(wp, wm, P.rp);
             }
         }
         S.amp[fl][face] = amp;

@@ -191,141 +191,7 @@ __global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
     }
 }
 
-// ---------------------------------------------------------------- inviscid faces
-// One thread per face m+1/2 of one line (solver.hpp:481-568).  DIR 0: x faces
-// f = m+1 in [0, nx] of row j; DIR 1: y faces of column i (threads along i
-// for coalesced stencil loads).
-template <int NS, int DIR, bool TENO, bool CHAR>
-#ifndef IGN_FACES_MINB
-#define IGN_FACES_MINB 2
-#endif
-__global__ void __launch_bounds__(128, IGN_FACES_MINB) k_faces(const __grid_constant__ KParams P,
-                                               const double* __restrict__ Ut, int stage,
-                                               int step) {
-    constexpr int NC = NS + 3;
-    constexpr int H = TENO ? 3 : 2;
-    constexpr int W = 2 * H;
-    if (failed(P.err)) return;
-    int line, f;
-    if (DIR == 0) {
-        f = blockIdx.x * blockDim.x + threadIdx.x;
-        line = blockIdx.y;
-        if (f > P.nx) return;
-    } else {
-        line = blockIdx.x * blockDim.x + threadIdx.x;
-        f = blockIdx.y;
-        if (line >= P.nx) return;
-    }
-    const int m = f - 1;  // face between nodes m and m+1
-    const long long step_n = DIR == 0 ? 1 : P.sx;  // node stride along the line
-    const long long base = DIR == 0 ? pidx(P, m, line) : pidx(P, line, m);
-    const double* m1a = DIR == 0 ? P.mxx : P.mex;
-    const double* m2a = DIR == 0 ? P.mxy : P.mey;
-    const long long il = base, ir = base + step_n;
-    const double m1f = 0.5 * (ldg(m1a + il) + ldg(m1a + ir));
-    const double m2f = 0.5 * (ldg(m2a + il) + ldg(m2a + ir));
-
-    double Fh[NC];
-    const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
-    const unsigned long long eidx = (unsigned long long)line * ((DIR == 0 ? P.nx : P.ny) + 1) + f;
-
-    if (CHAR) {
-        // roe_average + EigenSystem::at_state at the face (solver.hpp:493-502)
-        double Yl[NS], Yr[NS], Ya[NS];
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            Yl[s] = ldg(PY(P, s) + il);
-            Yr[s] = ldg(PY(P, s) + ir);
-        }
-        double Ta, ua, va;
-        roe_average<NS>(ldg(PRHO(P) + il), Yl, ldg(PT(P) + il), ldg(PU(P) + il),
-                        ldg(PV(P) + il), ldg(PRHO(P) + ir), Yr, ldg(PT(P) + ir),
-                        ldg(PU(P) + ir), ldg(PV(P) + ir), P.mix, Ya, Ta, ua, va);
-        Eigen<NS> es;
-        const int est = eigen_at_state<NS>(Ya, Ta, ua, va, m1f, m2f, P.mix, es);
-        if (est) {
-            report(P.err, stage, phase, eidx, 1 + est, step);
-            return;
-        }
-        // Node pass (solver.hpp:466-479) streamed one node at a time straight
-        // into the projections (solver.hpp:505-515), so only L F and L U of the
-        // 2h stencil nodes stay live.
-        double lf[W][NC], lu[W][NC], unk[W], ck[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const long long id = base + (long long)(k - H + 1) * step_n;
-            const double J = ldg(P.jac + id);
-            double Uk[NC], Fk[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
-            mapped_flux<NS>(Uk, ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk);
-            unk[k] = es.n1 * ldg(PU(P) + id) + es.n2 * ldg(PV(P) + id);
-            ck[k] = ldg(PC(P) + id);
-            eigen_project<NS>(es, Fk, lf[k]);
-            eigen_project<NS>(es, Uk, lu[k]);
-        }
-        double amp[NC];
-#pragma unroll
-        for (int fl = 0; fl < NC; ++fl) {
-            double alpha = 0.0;
-#pragma unroll
-            for (int k = 0; k < W; ++k)
-                alpha = smax(alpha, fabs(field_speed<NS>(es, fl, unk[k], ck[k])));
-            if (!isfinite(alpha)) {
-                report(P.err, stage, phase, eidx, 1, step);
-                return;
-            }
-            double wp[W], wm[W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                wp[k] = 0.5 * (lf[k][fl] + alpha * lu[k][fl]);
-                wm[k] = 0.5 * (lf[k][fl] - alpha * lu[k][fl]);
-            }
-            amp[fl] = face_pm<TENO>(wp, wm, P.ct, P.eps);
-        }
-        eigen_assemble<NS>(es, amp, Fh);
-    } else {
-        // componentwise LLF (solver.hpp:536-567)
-        double Fk[W][NC], Uk[W][NC], unk[W], ck[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) {  // node pass (solver.hpp:466-479)
-            const long long id = base + (long long)(k - H + 1) * step_n;
-            const double J = ldg(P.jac + id);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) Uk[k][c] = ldg(Ut + c * P.plane + id) * J;
-            mapped_flux<NS>(Uk[k], ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk[k]);
-            unk[k] = ldg(PU(P) + id);
-            ck[k] = ldg(PV(P) + id);
-        }
-        const double sf = ghypot(m1f, m2f);
-        double alpha = 0.0;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const long long id = base + (long long)(k - H + 1) * step_n;
-            const double un = (m1f * unk[k] + m2f * ck[k]) / sf;
-            alpha = smax(alpha, sf * (fabs(un) + ldg(PC(P) + id)));
-        }
-        if (!isfinite(alpha)) {
-            report(P.err, stage, phase, eidx, 1, step);
-            return;
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            double wp[W], wm[W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                wp[k] = 0.5 * (Fk[k][c] + alpha * Uk[k][c]);
-                wm[k] = 0.5 * (Fk[k][c] - alpha * Uk[k][c]);
-            }
-            Fh[c] = face_pm<TENO>(wp, wm, P.ct, P.eps);
-        }
-    }
-    double* out = DIR == 0 ? P.Fx : P.Gy;
-    const long long fplane = (long long)(P.nx + 1 - DIR) * (P.ny + DIR);
-    const long long o = DIR == 0 ? (long long)line * (P.nx + 1) + f : (long long)f * P.nx + line;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) out[c * fplane + o] = Fh[c];
-}
+// Inviscid faces: faces.cuh (k_faces3).
 
 // ---------------------------------------------------------------- viscous
 // compute_viscous node fluxes over ring 1 (solver.hpp:610-696).

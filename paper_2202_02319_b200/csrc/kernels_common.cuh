@@ -50,7 +50,7 @@ struct KParams {
     double T_wall[4];
     double sigma_out_right, p_target_right;
     double lx, ly, cx, cy;
-    double ct, eps;
+    ReconParams rp;  // ct, eps and the TENO cutoff decision band
     int32_t chem_dt_limit, lodi;
     double chem_dt_factor;
     // primitive cache block: rho,u,v,p,T,c then Y_s, then X_s (viscous)

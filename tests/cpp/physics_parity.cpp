@@ -161,7 +161,64 @@ static void check_mixture(const ignis::MixtureModel& mix, const char* name, unsi
     }
 }
 
+// TENO6's cutoff filter (physics.cuh teno_cutoff_filter) at the decision
+// boundary: for random stencils, ct is placed ON one candidate's exact ratio
+// g_k/gsum (times 1 + O(1e-6) jitter, inside and outside the filter band), so
+// every branch of the filter and its exact fallback is exercised.
+static void check_teno_cutoff_boundary() {
+    std::mt19937 rng(4242);
+    std::uniform_real_distribution<double> u(-2.0, 2.0), jit(-3e-7, 3e-7);
+    std::uniform_int_distribution<int> pick(0, 3);
+    std::uniform_real_distribution<double> lg(-12.0, 0.0);
+    int filtered = 0, exact = 0;
+    for (int trial = 0; trial < 300000; ++trial) {
+        double w[6];
+        const double amp = std::pow(10.0, lg(rng));  // discontinuity strength
+        for (int q = 0; q < 6; ++q) w[q] = (q < 3 ? 1.0 : 0.0) + amp * u(rng);
+        // exact ratios Q_k of the reference's sequence (reconstruction.hpp:257-289)
+        const double v0 = w[0] - w[2], v1 = w[1] - w[2], v3 = w[3] - w[2], v4 = w[4] - w[2],
+                     v5 = w[5] - w[2];
+        const double b[4] = {
+            (13.0 / 12.0) * (v0 - 2.0 * v1) * (v0 - 2.0 * v1) +
+                0.25 * (v0 - 4.0 * v1) * (v0 - 4.0 * v1),
+            (13.0 / 12.0) * (v1 + v3) * (v1 + v3) + 0.25 * (v1 - v3) * (v1 - v3),
+            (13.0 / 12.0) * (v4 - 2.0 * v3) * (v4 - 2.0 * v3) +
+                0.25 * (v4 - 4.0 * v3) * (v4 - 4.0 * v3),
+            (1.0 / 240.0) * (v3 * (11003.0 * v3 - 17246.0 * v4 + 4642.0 * v5) +
+                             v4 * (7043.0 * v4 - 3882.0 * v5) + 547.0 * v5 * v5)};
+        const double b6 =
+            (1.0 / 120960.0) *
+            (v0 * (271779.0 * v0 - 2380800.0 * v1 - 3462252.0 * v3 + 1458762.0 * v4 -
+                   245620.0 * v5) +
+             v1 * (5653317.0 * v1 + 17905032.0 * v3 - 7727988.0 * v4 + 1325006.0 * v5) +
+             v3 * (17195652.0 * v3 - 15880404.0 * v4 + 2863984.0 * v5) +
+             v4 * (3824847.0 * v4 - 1429976.0 * v5) + 139633.0 * v5 * v5);
+        const double tau = std::abs(b6 - (b[0] + 4.0 * b[1] + b[2]) / 6.0);
+        double g[4], gsum = 0.0;
+        for (int k = 0; k < 4; ++k) {
+            double t = 1.0 + tau / (b[k] + 1e-40);
+            const double t2 = t * t;
+            g[k] = t2 * t2 * t2;
+        }
+        gsum = g[0] + g[1] + g[2] + g[3];
+        const double Q = g[pick(rng)] / gsum;
+        // ct on the exact ratio, or 1 + O(1e-7) away from it on either side
+        const int mode = trial % 4;
+        double ct = mode == 0 ? Q : Q * (1.0 + (mode == 1 ? 1.0 : 10.0) * jit(rng));
+        if (!(ct > 0.0 && ct < 1.0)) continue;
+        const ign::ReconParams rp = ign::make_recon_params(ct, 1e-40);
+        const double B[4] = {b[0] + 1e-40, b[1] + 1e-40, b[2] + 1e-40, b[3] + 1e-40};
+        (ign::teno_cutoff_filter(tau, B[0], B[1], B[2], B[3], rp) < 0 ? exact : filtered) += 1;
+        EXPECT_BITWISE("teno6 cutoff boundary",
+                       ign::teno6_plus(w[0], w[1], w[2], w[3], w[4], w[5], rp),
+                       ignis::recon::teno6_plus(w + 2, ct, 1e-40));
+    }
+    std::printf("teno cutoff boundary: %d decided by the filter, %d exact fallbacks\n", filtered,
+                exact);
+}
+
 static void check_recon() {
+    const ign::ReconParams rp = ign::make_recon_params(1e-5, 1e-40);
     std::mt19937 rng(42);
     std::uniform_real_distribution<double> u(-2.0, 2.0);
     std::uniform_int_distribution<int> kind(0, 3);
@@ -174,18 +231,18 @@ static void check_recon() {
             if (k == 2) w[q] = 3.0 + 1e-9 * u(rng);             // near-constant
             if (k == 3) w[q] = std::sin(0.3 * q + u(rng));      // smooth
         }
-        EXPECT_BITWISE("teno6_plus", ign::teno6_plus(w[0], w[1], w[2], w[3], w[4], w[5], 1e-5, 1e-40),
+        EXPECT_BITWISE("teno6_plus", ign::teno6_plus(w[0], w[1], w[2], w[3], w[4], w[5], rp),
                        ignis::recon::teno6_plus(w + 2, 1e-5, 1e-40));
         EXPECT_BITWISE("weno3z_plus", ign::weno3z_plus(w[0], w[1], w[2], 1e-40),
                        ignis::recon::weno3z_plus(w + 1, 1e-40));
         double wm[6];
         for (int q = 0; q < 6; ++q) wm[q] = u(rng);
         EXPECT_BITWISE("face teno6",
-                       ign::face_pm<true>(w, wm, 1e-5, 1e-40),
+                       ign::face_pm<true>(w, wm, rp),
                        ignis::recon::face_plus(ignis::InviscidScheme::TENO6, w + 2, 1e-5, 1e-40) +
                            ignis::recon::face_minus(ignis::InviscidScheme::TENO6, wm + 2, 1e-5, 1e-40));
         EXPECT_BITWISE("face weno3z",
-                       ign::face_pm<false>(w, wm, 1e-5, 1e-40),
+                       ign::face_pm<false>(w, wm, rp),
                        ignis::recon::face_plus(ignis::InviscidScheme::WENO3Z, w + 1, 1e-5, 1e-40) +
                            ignis::recon::face_minus(ignis::InviscidScheme::WENO3Z, wm + 1, 1e-5, 1e-40));
     }
@@ -231,6 +288,7 @@ int main() {
     ignis::MixtureModel gas = ignis::MixtureModel::calorically_perfect(1.4, 1.0, 6.25e-4);
     gas.species[0].pieces[0].t_hi = 1e6;
     check_recon();
+    check_teno_cutoff_boundary();
     check_mixture<4>(ch4, "ch4_o2", 1234);
     check_mixture<1>(gas, "gamma_gas", 77);
     check_sources(ch4);
