@@ -244,57 +244,58 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
             const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
             double lf[W], lu[W];
-            // row fl of EigenSystem::project (flux.hpp:116-119); the field kind is
-            // warp-uniform, so the branch is hoisted out of the stencil loop, and
-            // the 2W quotients share one validity flag (one branch, exact redo)
-            auto rows = [&](auto kind) {
-                constexpr int K = decltype(kind)::value;
-                bool ok = true;
-                auto row = [&](int k, int vu, bool exact) {
-                    const int t = tile_node<DIR>(g, lane, k);
+            // Row fl of EigenSystem::project (flux.hpp:116-119) in ONE code path
+            // for every field kind (all NC warps of the CTA share the
+            // instructions): acoustic  w = (dp -+ c dun) / (2c^2), written as
+            // dp + s*(c dun) with s = -+1 (exact negation); species
+            // w = q_s - Y_s dp / c^2; shear w = dut.  The 2W quotients share one
+            // validity flag (one branch, exact redo on the rare failure).
+            const bool ac = fl == 0 || fl == NC - 1, sh = fl == NC - 2;
+            const int sp_i = ac || sh ? 0 : fl - 1;
+            const double sgn = fl == 0 ? -1.0 : 1.0;
+            const double Ys = S.E[EY0 + sp_i][face];
+            const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node<DIR>(g, lane, k);
+#pragma unroll
+                for (int vu = 0; vu < 2; ++vu) {
                     const int vec = 2 * k + vu;
                     const double dp = S.L[vec][0][lane];
-                    if (K == 0) {
-                        const double a = dp - ec * S.L[vec][1][lane];
-                        return exact ? div_cold(a, c2x2) : fdiv_try(a, c2x2, y2c2, ok);
-                    } else if (K == 1) {
-                        const double a = dp + ec * S.L[vec][1][lane];
-                        return exact ? div_cold(a, c2x2) : fdiv_try(a, c2x2, y2c2, ok);
-                    } else if (K == 2) {
-                        return S.L[vec][2][lane];
-                    } else {
-                        const double qs = vu ? S.U[fl - 1][t] : S.F[fl - 1][t];
-                        const double a = S.E[EY0 + fl - 1][face] * dp;
-                        return qs - (exact ? div_cold(a, c2) : fdiv_try(a, c2, yc2, ok));
-                    }
-                };
+                    const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
+                    const double fd = fdiv_try(num, den, yden, ok);
+                    const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
+                    const double w = ac ? fd : sh ? S.L[vec][2][lane] : qs - fd;
+                    if (vu) lu[k] = w;
+                    else lf[k] = w;
+                }
+            }
+            if (!sh && !ok) {  // exact redo (rare): plain IEEE quotients
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    lf[k] = row(k, 0, false);
-                    lu[k] = row(k, 1, false);
-                }
-                if (K != 2 && !ok) {
+                    const int t = tile_node<DIR>(g, lane, k);
 #pragma unroll
-                    for (int k = 0; k < W; ++k) {
-                        lf[k] = row(k, 0, true);
-                        lu[k] = row(k, 1, true);
+                    for (int vu = 0; vu < 2; ++vu) {
+                        const int vec = 2 * k + vu;
+                        const double dp = S.L[vec][0][lane];
+                        const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
+                        const double fd = div_cold(num, den);
+                        const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
+                        const double w = ac ? fd : qs - fd;
+                        if (vu) lu[k] = w;
+                        else lf[k] = w;
                     }
                 }
-            };
-            if (fl == 0) rows(std::integral_constant<int, 0>());
-            else if (fl == NC - 1) rows(std::integral_constant<int, 1>());
-            else if (fl == NC - 2) rows(std::integral_constant<int, 2>());
-            else rows(std::integral_constant<int, 3>());
+            }
             // EigenSystem::field_speed at each node's normal velocity (flux.hpp:143-147)
             double alpha = 0.0;
-            const double sg = fl == 0 ? -1.0 : fl == NC - 1 ? 1.0 : 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
                 const int t = tile_node<DIR>(g, lane, k);
                 const double unk = n1 * S.u[t] + n2 * S.v[t];
                 const double ck = S.c[t];
-                const double lam = sg < 0.0 ? es * (unk - ck) : sg > 0.0 ? es * (unk + ck)
-                                                                          : es * unk;
+                const double lam = es * (ac ? unk + sgn * ck : unk);
                 alpha = smax(alpha, fabs(lam));
             }
             if (!isfinite(alpha)) {
