@@ -114,3 +114,16 @@ def test_mixture_parser_reads_h2o2_table():
     assert [s.name for s in sp] == ["H2", "O2", "H2O", "N2"]
     W = {s.name: s.W for s in sp}
     assert 2 * W["H2"] + W["O2"] == pytest.approx(2 * W["H2O"], abs=1e-15)
+
+
+def test_cpp_facade_example_compiles_and_links(tmp_path):
+    """a C++ caller of the facade builds against the library."""
+    import subprocess
+    root = os.path.dirname(HEADER)
+    lib = os.path.dirname(native.LIB)
+    exe = str(tmp_path / "facade_example")
+    subprocess.run(["g++", "-std=c++17", "-O2", f"-I{root}",
+                    os.path.join(os.path.dirname(root), "tests", "cpp", "facade_example.cpp"),
+                    f"-L{lib}", "-lignis_b200", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode in (0, 2), r.stdout + r.stderr
