@@ -151,6 +151,11 @@ typedef struct {
     int32_t partitions;          /* ThreadTeam workers (CPU oracle only) */
     ign_integrator integ;
     int32_t device;              /* CUDA device ordinal */
+    /* Slab decomposition along y (rows) across GPUs: ny is the
+     * GLOBAL row count; this context owns slab slab_rank of slab_count
+     * (ThreadTeam's block split, thread_team.hpp:63-69).  0 or 1 = whole mesh. */
+    int32_t slab_count;
+    int32_t slab_rank;
     int32_t _pad;
 } ign_config;
 
@@ -248,6 +253,29 @@ void* ign_stream_handle(const ign_context* ctx);
 /* Measured FP64 FMA peak of a device: a DFMA-chain kernel over every SM
  * (2 flops per FMA); the roofline denominator of the FP64-bound path. */
 int ign_probe_fp64_peak(int device, double* tflops);
+
+/* ---- multi-GPU slabs --------------------------------------- */
+/* One process per GPU: rank 0 creates an NCCL unique id, every rank passes it
+ * to ign_attach_nccl with its slab config (slab_count/slab_rank).  Halo rows
+ * (g rows of every component) then travel by ncclSend/ncclRecv between the
+ * x- and y-edge ghost passes of every prepare_stage; stable_dt, the error word
+ * and the clip diagnostics are all-reduced (MIN/MAX, exact); conserved_totals
+ * and product_mole_fraction fold rank by rank in the reference's serial order. */
+#define IGN_NCCL_ID_BYTES 128
+int ign_nccl_unique_id(uint8_t* id);
+int ign_attach_nccl(ign_context* ctx, const uint8_t* id, int nranks, int rank);
+
+/* Single-process slab group (validation on one GPU): the members (slab
+ * contexts of one config, ranks 0..n-1, same device) run in lockstep on one
+ * stream; halo rows move by device-to-device copies. */
+typedef struct ign_group ign_group;
+int ign_group_create(ign_context** members, int n, ign_group** out);
+void ign_group_destroy(ign_group* grp);
+int ign_group_last_error(const ign_group* grp, ign_error* err);
+int ign_group_prepare_stage(ign_group* grp, int stage);
+int ign_group_rk3_steps(ign_group* grp, double dt, int64_t nsteps);
+int ign_group_stable_dt(ign_group* grp, double* dt);
+int ign_group_conserved_totals(ign_group* grp, double* tot);
 
 #ifdef __cplusplus
 }

@@ -110,7 +110,8 @@ class Config(C.Structure):
                 ("mech", Mechanism), ("laser", Laser),
                 ("viscous", C.c_int32), ("partitions", C.c_int32),
                 ("integ", Integrator),
-                ("device", C.c_int32), ("_pad", C.c_int32)]
+                ("device", C.c_int32), ("slab_count", C.c_int32),
+                ("slab_rank", C.c_int32), ("_pad", C.c_int32)]
 
 
 class Error(C.Structure):
@@ -170,7 +171,18 @@ PRODUCT_ONLY = {
     "profile_read": (_I, [_P, _D, C.POINTER(C.c_int64)]),
     "stream_handle": (C.c_void_p, [_P]),
     "probe_fp64_peak": (_I, [_I, _D]),
+    # multi-GPU slabs
+    "nccl_unique_id": (_I, [C.c_char_p]),
+    "attach_nccl": (_I, [_P, C.c_char_p, _I, _I]),
+    "group_create": (_I, [C.POINTER(_P), _I, C.POINTER(_P)]),
+    "group_destroy": (None, [_P]),
+    "group_last_error": (_I, [_P, C.POINTER(Error)]),
+    "group_prepare_stage": (_I, [_P, _I]),
+    "group_rk3_steps": (_I, [_P, C.c_double, C.c_int64]),
+    "group_stable_dt": (_I, [_P, _D]),
+    "group_conserved_totals": (_I, [_P, _D]),
 }
+IGN_NCCL_ID_BYTES = 128
 PROF_CLASSES = ("bc", "prim", "faces", "visc", "assemble", "dt", "r6", "r7")
 
 # entry points of include/ignis_b200.h that every product build must export

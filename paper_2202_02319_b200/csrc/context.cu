@@ -1,20 +1,32 @@
 // context.cu — the C-ABI (include/ignis_b200.h) over the sm_100a kernels.
 //
-// One ign_context = one ignis::Simulation (solver.hpp:53-853) on one GPU.
-// The conservative state lives in three rotating device buffers S[0..2]; an
-// RK3 step reads U0 from S[a], writes U1 to S[b], U2 to S[c] and U3 back into
-// S[b], so no copy_interior (solver.hpp:310) is ever needed and U0 stays intact
-// for the StepFailure restore (solver.hpp:326-329).  Errors raised on the
-// device are collected in one error word and decoded here into the
-// reference's exception kinds after the stream synchronises.
+// One ign_context = one ignis::Simulation (solver.hpp:53-853) on one GPU, or
+// one slab of a domain decomposed along y across GPUs.  The conservative state
+// lives in three rotating device buffers S[0..2]; an RK3 step reads U0 from
+// S[a], writes U1 to S[b], U2 to S[c] and U3 back into S[b], so no
+// copy_interior (solver.hpp:310) is ever needed and U0 stays intact for the
+// StepFailure restore (solver.hpp:326-329).  Errors raised on the device are
+// collected in one error word and decoded here into the reference's exception
+// kinds after the stream synchronises.
+//
+// Orchestration runs over a "team": one context (optionally exchanging halo
+// rows with other processes through NCCL), or a single-process group of slab
+// contexts sharing one stream (validation on one GPU).  Both execute the same
+// phase sequence per stage:
+//   ghost x-pass -> halo exchange -> ghost y-pass -> primitives -> faces ->
+//   viscous -> assemble/update (+ error-word MIN all-reduce across slabs).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen'ed on attach
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "host_core.hpp"
@@ -47,6 +59,8 @@ KernelSet kernel_set(int ns) {
 
 using namespace ign;
 
+struct ign_group;
+
 struct ign_context {
     ign_config cfg;
     HMesh mesh;
@@ -56,14 +70,16 @@ struct ign_context {
     int nx = 0, ny = 0, g = 0, ns = 0, nc = 0;
     size_t plane = 0;
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, own_stream = nullptr;
     double* S[3] = {nullptr, nullptr, nullptr};
     int cur = 0;
     double* prim = nullptr;
     double* geom = nullptr;  // met(5), met_v(5), mesh x, y
     double *Fx = nullptr, *Gy = nullptr, *Fv = nullptr, *Gv = nullptr, *rhs = nullptr;
     double* inflow[4] = {nullptr, nullptr, nullptr, nullptr};
-    ErrRec* err = nullptr;
+    double* wrap[2] = {nullptr, nullptr};
+    ErrRec* err = nullptr;      // the word the kernels report into
+    ErrRec* own_err = nullptr;  // this context's allocation
     unsigned long long* red = nullptr;
     double time = 0.0;
     int64_t iter = 0;
@@ -71,6 +87,11 @@ struct ign_context {
     ign_integrator integ{};
     ign_error lasterr{};
     int64_t launches = 0;
+    // slab decomposition
+    int nranks = 1, rank = 0;
+    int lo_peer = -1, hi_peer = -1;  // ranks owning our ghost rows (-1: physical edge)
+    ncclComm_t comm = nullptr;
+    ign_group* group = nullptr;
     // live per-kernel-class timing (CUDA events on this context's stream)
     bool prof_on = false;
     struct Rec { int cat; cudaEvent_t a, b; };
@@ -80,11 +101,73 @@ struct ign_context {
     int64_t prof_n[IGN_PROF_CLASSES] = {};
 };
 
+struct ign_group {
+    std::vector<ign_context*> m;
+    ign_error lasterr{};
+};
+
 namespace {
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                              ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi load_nccl() {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        a.why = std::string("libnccl not loadable: ") + dlerror();
+        return a;
+    }
+    bool all = true;
+    auto sym = [&](auto& f, const char* n) {
+        f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, n));
+        all = all && f;
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.AllReduce, "ncclAllReduce");
+    sym(a.Broadcast, "ncclBroadcast");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = all;
+    if (!all) a.why = "libnccl lacks an entry point";
+    return a;
+}
+
+NcclApi& nccl() {
+    static NcclApi a = load_nccl();
+    return a;
+}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
         throw Error(IGN_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw Error(IGN_CUDA_ERROR, std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
 void set_error(ign_error* out, const Error& e) {
@@ -96,19 +179,27 @@ void set_error(ign_error* out, const Error& e) {
     std::snprintf(out->msg, sizeof(out->msg), "%s", e.what());
 }
 
-template <class F> int guarded(ign_context* ctx, F&& f) {
+template <class F> int guarded_err(ign_error* err, int device, F&& f) {
     try {
-        if (ctx) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (device >= 0) cuda_check(cudaSetDevice(device), "cudaSetDevice");
         f();
-        if (ctx) std::memset(&ctx->lasterr, 0, sizeof(ctx->lasterr));
+        if (err) std::memset(err, 0, sizeof(*err));
         return IGN_OK;
     } catch (const Error& e) {
-        if (ctx) set_error(&ctx->lasterr, e);
+        set_error(err, e);
         return e.status;
     } catch (const std::exception& e) {
-        if (ctx) set_error(&ctx->lasterr, Error(IGN_INTERNAL_ERROR, e.what()));
+        set_error(err, Error(IGN_INTERNAL_ERROR, e.what()));
         return IGN_INTERNAL_ERROR;
     }
+}
+
+template <class F> int guarded(ign_context* ctx, F&& f) {
+    return guarded_err(ctx ? &ctx->lasterr : nullptr, ctx ? ctx->device : -1, [&] {
+        if (ctx && ctx->group)
+            throw usage_error("context belongs to a slab group: drive it through ign_group_*");
+        f();
+    });
 }
 
 const char* pstatus_msg(unsigned sub) {
@@ -118,14 +209,6 @@ const char* pstatus_msg(unsigned sub) {
     default: return "temperature_from_energy: no convergence";
     }
 }
-
-// Decoded device failure.
-struct DevFail {
-    bool any = false;
-    unsigned stage = 0, phase = 0, sub = 0;
-    unsigned long long idx = 0;
-    int step = 0;
-};
 
 cudaEvent_t prof_event(ign_context* ctx) {
     if (!ctx->prof_pool.empty()) {
@@ -161,25 +244,52 @@ void prof_harvest(ign_context* ctx) {
     ctx->prof_pending.clear();
 }
 
-DevFail sync_and_read(ign_context* ctx) {
-    cuda_check(cudaStreamSynchronize(ctx->stream), "kernel execution");
+double* dalloc(size_t n) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)), "cudaMalloc");
+    return static_cast<double*>(p);
+}
+
+// ---------------------------------------------------------------- teams
+struct Team {
+    std::vector<ign_context*> m;  // slab order (rank 0 first)
+    ign_context* lead() const { return m[0]; }
+    bool local() const { return m.size() > 1; }
+    cudaStream_t stream() const { return m[0]->stream; }
+};
+
+Team solo(ign_context* c) { return Team{{c}}; }
+
+// Decoded device failure (key layout: kernels_common.cuh report()).
+struct DevFail {
+    bool any = false;
+    unsigned stage = 0, phase = 0, sub = 0;
+    unsigned long long idx = 0;
+    int step = 0;
+};
+
+DevFail sync_and_read(const Team& T) {
+    cuda_check(cudaStreamSynchronize(T.stream()), "kernel execution");
     cuda_check(cudaGetLastError(), "kernel launch");
-    prof_harvest(ctx);
+    for (ign_context* c : T.m) prof_harvest(c);
     ErrRec h;
-    cuda_check(cudaMemcpy(&h, ctx->err, sizeof(h), cudaMemcpyDeviceToHost), "error word");
+    ign_context* L = T.lead();
+    cuda_check(cudaMemcpy(&h, L->err, sizeof(h), cudaMemcpyDeviceToHost), "error word");
     DevFail f;
     if (h.key == kNoError) return f;
     f.any = true;
-    f.stage = (unsigned)(h.key >> 60);
-    f.phase = (unsigned)((h.key >> 52) & 0xff);
-    f.idx = (h.key >> 4) & ((1ull << 48) - 1);
-    f.sub = (unsigned)(h.key & 0xf);
-    f.step = h.step;
-    cuda_check(cudaMemset(ctx->err, 0xff, sizeof(ErrRec)), "error reset");
+    f.step = (int)(h.key >> 44);
+    f.stage = (unsigned)((h.key >> 41) & 7);
+    f.phase = (unsigned)((h.key >> 38) & 7);
+    f.idx = (h.key >> 3) & ((1ull << 35) - 1);
+    f.sub = (unsigned)(h.key & 7);
+    for (ign_context* c : T.m)
+        cuda_check(cudaMemset(c->own_err, 0xff, sizeof(ErrRec)), "error reset");
     return f;
 }
 
-// Maps a device failure onto the exception the reference throws there.
+// Maps a device failure onto the exception the reference throws there
+// (indices are global: the reference runs the undecomposed domain).
 Error to_error(const ign_context* ctx, const DevFail& f) {
     const int rep_stage = f.stage == 4 ? 1 : (int)f.stage;
     switch (f.phase) {
@@ -208,17 +318,396 @@ Error to_error(const ign_context* ctx, const DevFail& f) {
     }
 }
 
-void check(ign_context* ctx) {
-    const DevFail f = sync_and_read(ctx);
-    if (f.any) throw to_error(ctx, f);
+void check(const Team& T) {
+    const DevFail f = sync_and_read(T);
+    if (f.any) throw to_error(T.lead(), f);
 }
 
-double* dalloc(size_t n) {
-    void* p = nullptr;
-    cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)), "cudaMalloc");
-    return static_cast<double*>(p);
+// Cross-slab consistency of the error word: MIN all-reduce (NCCL teams only;
+// a local group shares one word).
+void t_errsync(const Team& T) {
+    ign_context* c = T.lead();
+    if (T.local() || !c->comm) return;
+    nccl_check(nccl().AllReduce(&c->err->key, &c->err->key, 1, ncclUint64, ncclMin, c->comm,
+                                c->stream),
+               "ncclAllReduce(error word)");
 }
 
+// Halo rows of state buffer `buf`: our g bottom/top interior rows to the
+// neighbours, their rows into our ghost rows (all components; rows are
+// contiguous in the padded planes, so every transfer is one contiguous chunk).
+void t_exchange(const Team& T, int buf) {
+    if (T.local()) {
+        for (ign_context* c : T.m) {
+            const size_t chunk = size_t(c->g) * c->kp.sx;
+            for (int comp = 0; comp < c->nc; ++comp) {
+                if (c->lo_peer >= 0) {
+                    const ign_context* s = T.m[c->lo_peer];
+                    cuda_check(cudaMemcpyAsync(c->S[buf] + comp * c->plane,
+                                               s->S[buf] + comp * s->plane + size_t(s->ny) * s->kp.sx,
+                                               chunk * sizeof(double), cudaMemcpyDeviceToDevice,
+                                               T.stream()),
+                               "halo copy");
+                }
+                if (c->hi_peer >= 0) {
+                    const ign_context* s = T.m[c->hi_peer];
+                    cuda_check(cudaMemcpyAsync(c->S[buf] + comp * c->plane +
+                                                   size_t(c->ny + c->g) * c->kp.sx,
+                                               s->S[buf] + comp * s->plane + chunk,
+                                               chunk * sizeof(double), cudaMemcpyDeviceToDevice,
+                                               T.stream()),
+                               "halo copy");
+                }
+            }
+        }
+        return;
+    }
+    ign_context* c = T.lead();
+    if (c->lo_peer < 0 && c->hi_peer < 0) return;
+    if (!c->comm)
+        throw usage_error("slab context without a transport: call ign_attach_nccl or use a group");
+    NcclApi& n = nccl();
+    const size_t chunk = size_t(c->g) * c->kp.sx;
+    nccl_check(n.GroupStart(), "ncclGroupStart");
+    for (int comp = 0; comp < c->nc; ++comp) {
+        double* base = c->S[buf] + comp * c->plane;
+        // per peer pair the order is [top, bottom] sends against [lo, hi]
+        // receives, so a two-slab periodic ring matches correctly
+        if (c->hi_peer >= 0)
+            nccl_check(n.Send(base + size_t(c->ny) * c->kp.sx, chunk, ncclFloat64, c->hi_peer,
+                              c->comm, c->stream), "ncclSend");
+        if (c->lo_peer >= 0)
+            nccl_check(n.Send(base + chunk, chunk, ncclFloat64, c->lo_peer, c->comm, c->stream),
+                       "ncclSend");
+        if (c->lo_peer >= 0)
+            nccl_check(n.Recv(base, chunk, ncclFloat64, c->lo_peer, c->comm, c->stream),
+                       "ncclRecv");
+        if (c->hi_peer >= 0)
+            nccl_check(n.Recv(base + size_t(c->ny + c->g) * c->kp.sx, chunk, ncclFloat64,
+                              c->hi_peer, c->comm, c->stream), "ncclRecv");
+    }
+    nccl_check(n.GroupEnd(), "ncclGroupEnd");
+}
+
+// prepare_stage (solver.hpp:422-425): fill_ghosts (x edges, halo, y edges)
+// then refresh_primitives
+void t_prepare(const Team& T, int buf, int stage, int step) {
+    for (ign_context* c : T.m)
+        c->launches += timed(c, IGN_PROF_BC, [&] {
+            return c->ks.bc(c->kp, c->S[buf], 0, stage, step, c->stream);
+        });
+    t_exchange(T, buf);
+    for (ign_context* c : T.m)
+        c->launches += timed(c, IGN_PROF_BC, [&] {
+            return c->ks.bc(c->kp, c->S[buf], 1, stage, step, c->stream);
+        });
+    for (ign_context* c : T.m)
+        c->launches += timed(c, IGN_PROF_PRIM, [&] {
+            return c->ks.prim(c->kp, c->S[buf], stage, step, c->stream);
+        });
+    t_errsync(T);
+}
+
+void t_fluxes(const Team& T, int buf, int stage, int step) {
+    for (ign_context* c : T.m) {
+        c->launches += timed(c, IGN_PROF_FACES, [&] {
+            return c->ks.faces(c->kp, c->cfg.scheme.scheme, c->cfg.scheme.split, c->S[buf], stage,
+                               step, c->stream);
+        });
+        if (c->cfg.viscous)
+            c->launches += timed(c, IGN_PROF_VISC,
+                                 [&] { return c->ks.visc(c->kp, stage, step, c->stream); });
+    }
+}
+
+void t_assemble(const Team& T, int mode, int a, int cur, int out, double dt, double w, double t,
+                int stage, int step, int slot) {
+    for (ign_context* c : T.m)
+        c->launches += timed(c, IGN_PROF_ASSEMBLE, [&] {
+            return c->ks.assemble(c->kp, mode, c->S[a], c->S[cur], c->S[out], dt, w, t, stage,
+                                  step, slot, c->stream);
+        });
+    t_errsync(T);
+}
+
+// Zeroes one step's clip slots unless a failure is pending (a pending failure
+// must keep the previous step's clips for last_clip, solver.hpp:847).
+__global__ void k_clip_reset(const ErrRec* err, unsigned long long* red, int slot) {
+    if (failed(err)) return;
+    red[2 + slot + threadIdx.x] = 0ull;
+}
+
+// One rk3_step (solver.hpp:304-332) enqueued without a host round trip;
+// post_prepare appends advance()'s prepare_stage(1) (solver.hpp:345).
+void t_step(const Team& T, int a, double time, double dt, int step, bool post_prepare) {
+    const int b = (a + 1) % 3, c = (a + 2) % 3;
+    const int slot = (step & 1) * 3;
+    for (ign_context* x : T.m) {
+        k_clip_reset<<<1, 3, 0, x->stream>>>(x->err, x->red, slot);
+        ++x->launches;
+    }
+    // Stage 1: U <- U0 + dt L(U0)   (ghosts/cache already fresh)
+    t_fluxes(T, a, 1, step);
+    t_assemble(T, 1, a, a, b, dt, 0.0, time, 1, step, slot + 0);
+    t_prepare(T, b, 2, step);
+    // Stage 2: U <- U0 + 1/4 [(U1 - U0) + dt L(U1)]
+    t_fluxes(T, b, 2, step);
+    t_assemble(T, 2, a, b, c, dt, 0.25, time + dt, 2, step, slot + 1);
+    t_prepare(T, c, 3, step);
+    // Stage 3: U <- U0 + 2/3 [(U2 - U0) + dt L(U2)]
+    t_fluxes(T, c, 3, step);
+    t_assemble(T, 2, a, c, b, dt, 2.0 / 3.0, time + 0.5 * dt, 3, step, slot + 2);
+    if (post_prepare) t_prepare(T, b, 4, step);
+}
+
+// Clip slots of all slabs (MAX over slabs: the reference's clip is a max).
+void read_clips(const Team& T, unsigned long long red[8]) {
+    ign_context* L = T.lead();
+    if (!T.local() && L->comm) {
+        nccl_check(nccl().AllReduce(L->red + 2, L->red + 2, 6, ncclUint64, ncclMax, L->comm,
+                                    L->stream),
+                   "ncclAllReduce(clip)");
+        cuda_check(cudaStreamSynchronize(L->stream), "clip reduce");
+    }
+    std::memset(red, 0, 8 * sizeof(unsigned long long));
+    for (ign_context* c : T.m) {
+        unsigned long long r[8];
+        cuda_check(cudaMemcpy(r, c->red, sizeof(r), cudaMemcpyDeviceToHost), "reductions");
+        for (int k = 2; k < 8; ++k) red[k] = std::max(red[k], r[k]);
+    }
+}
+
+double clip_of(const unsigned long long* red, int slot) {
+    double d;
+    std::memcpy(&d, &red[2 + slot], sizeof(d));
+    return d;
+}
+
+void for_all(const Team& T, const std::function<void(ign_context*)>& f) {
+    for (ign_context* c : T.m) f(c);
+}
+
+// n consecutive steps; on a device failure reproduces the reference's state,
+// time/iter and last_clip at the point it would have thrown.
+void t_run_steps(const Team& T, double dt, int64_t n, bool post_prepare) {
+    if (n <= 0) return;
+    const int a0 = T.lead()->cur;
+    double t = T.lead()->time;
+    int64_t done = 0;
+    while (done < n) {
+        const int64_t chunk = std::min<int64_t>(n - done, 256);
+        for (int64_t k = 0; k < chunk; ++k) {
+            const int64_t s = done + k;
+            t_step(T, (int)((a0 + s) % 3), t, dt, (int)(s - done), post_prepare);
+            t += dt;
+        }
+        cuda_check(cudaGetLastError(), "kernel launch");
+        const DevFail f = sync_and_read(T);
+        unsigned long long red[8];
+        read_clips(T, red);
+        if (!f.any) {
+            const int last = (int)(chunk - 1);
+            const int slot = (last & 1) * 3;
+            const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
+                                       clip_of(red, slot + 2));
+            for_all(T, [&](ign_context* c) {
+                for (int64_t k = 0; k < chunk; ++k) {
+                    c->time += dt;
+                    ++c->iter;
+                }
+                c->last_clip = lc;
+                c->cur = (int)((a0 + done + chunk) % 3);
+            });
+            done += chunk;
+            continue;
+        }
+        const int64_t kk = f.step;  // failing step within this chunk
+        const int64_t k = done + kk;
+        double clip_prev = T.lead()->last_clip;
+        if (kk > 0) {
+            const int slot = ((int)(kk - 1) & 1) * 3;
+            clip_prev = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
+                                 clip_of(red, slot + 2));
+        }
+        const int ak = (int)((a0 + k) % 3);
+        const int slot = ((int)kk & 1) * 3;
+        const Error e = to_error(T.lead(), f);
+        if (f.stage == 4) {  // advance's prepare_stage(1) after a completed step
+            const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
+                                       clip_of(red, slot + 2));
+            for_all(T, [&](ign_context* c) {
+                for (int64_t q = done; q <= k; ++q) {
+                    c->time += dt;
+                    ++c->iter;
+                }
+                c->cur = (ak + 1) % 3;
+                c->last_clip = lc;
+            });
+            throw e;
+        }
+        // inside rk3_step: last_clip covers the stages that completed post_stage
+        double lc = clip_prev;
+        for (unsigned s = 1; s < f.stage; ++s)
+            lc = s == 1 ? clip_of(red, slot) : std::max(lc, clip_of(red, slot + s - 1));
+        const int cur = e.status == IGN_STEP_FAILURE ? ak  // restore U0
+                        : f.stage <= 1               ? ak
+                        : f.stage == 2               ? (ak + 1) % 3
+                                                     : (ak + 2) % 3;
+        for_all(T, [&](ign_context* c) {
+            for (int64_t q = done; q < k; ++q) {
+                c->time += dt;
+                ++c->iter;
+            }
+            c->last_clip = lc;
+            c->cur = cur;
+        });
+        throw e;
+    }
+}
+
+double t_stable_dt(const Team& T) {
+    unsigned long long init[2] = {0ull, 0x7ff0000000000000ull};
+    for (ign_context* c : T.m) {
+        cuda_check(cudaMemcpyAsync(c->red, init, sizeof(init), cudaMemcpyHostToDevice, c->stream),
+                   "dt reset");
+        c->launches += timed(c, IGN_PROF_DT, [&] { return c->ks.dt(c->kp, c->stream); });
+    }
+    ign_context* L = T.lead();
+    if (!T.local() && L->comm) {  // max/min are exact in any order
+        nccl_check(nccl().AllReduce(L->red, L->red, 1, ncclUint64, ncclMax, L->comm, L->stream),
+                   "ncclAllReduce(lam)");
+        nccl_check(nccl().AllReduce(L->red + 1, L->red + 1, 1, ncclUint64, ncclMin, L->comm,
+                                    L->stream),
+                   "ncclAllReduce(dt_chem)");
+    }
+    check(T);
+    unsigned long long lam_bits = 0ull, chem_bits = 0x7ff0000000000000ull;
+    for (ign_context* c : T.m) {
+        unsigned long long r[2];
+        cuda_check(cudaMemcpy(r, c->red, sizeof(r), cudaMemcpyDeviceToHost), "dt readback");
+        lam_bits = std::max(lam_bits, r[0]);
+        chem_bits = std::min(chem_bits, r[1]);
+    }
+    double lam_max, dt_chem;
+    std::memcpy(&lam_max, &lam_bits, sizeof(double));
+    std::memcpy(&dt_chem, &chem_bits, sizeof(double));
+    double dt = L->cfg.scheme.cfl / lam_max;
+    dt = smin(dt, dt_chem);
+    const ign_laser& las = L->cfg.laser;
+    if (las.present && las.energy != 0.0 && L->time - las.t0 < 6.0 * las.sigma_t &&
+        L->time + dt > las.t0 - 6.0 * las.sigma_t)
+        dt = smin(dt, las.sigma_t / 5.0);
+    return dt;
+}
+
+void t_prepare_sync(const Team& T, int stage) {
+    t_prepare(T, T.lead()->cur, stage, 0);
+    check(T);
+}
+
+// Serial left folds in the reference's order (solver.hpp:387-418) across
+// slabs: each slab continues the running accumulators of the slab below, so
+// the decomposed result is bit-identical to the single-domain one.
+void fold_ranks(const Team& T, std::vector<double>& acc,
+                const std::function<void(ign_context*, std::vector<double>&)>& fold) {
+    if (T.local()) {
+        for (ign_context* c : T.m) fold(c, acc);
+        return;
+    }
+    ign_context* c = T.lead();
+    if (!c->comm || c->nranks == 1) {
+        fold(c, acc);
+        return;
+    }
+    NcclApi& n = nccl();
+    double* d = dalloc(acc.size());
+    try {
+        if (c->rank > 0) {
+            nccl_check(n.Recv(d, acc.size(), ncclFloat64, c->rank - 1, c->comm, c->stream),
+                       "ncclRecv(fold)");
+            cuda_check(cudaMemcpyAsync(acc.data(), d, acc.size() * 8, cudaMemcpyDeviceToHost,
+                                       c->stream), "fold");
+            cuda_check(cudaStreamSynchronize(c->stream), "fold");
+        }
+        fold(c, acc);
+        cuda_check(cudaMemcpyAsync(d, acc.data(), acc.size() * 8, cudaMemcpyHostToDevice,
+                                   c->stream), "fold");
+        if (c->rank + 1 < c->nranks)
+            nccl_check(n.Send(d, acc.size(), ncclFloat64, c->rank + 1, c->comm, c->stream),
+                       "ncclSend(fold)");
+        nccl_check(n.Broadcast(d, d, acc.size(), ncclFloat64, c->nranks - 1, c->comm, c->stream),
+                   "ncclBroadcast(fold)");
+        cuda_check(cudaMemcpyAsync(acc.data(), d, acc.size() * 8, cudaMemcpyDeviceToHost,
+                                   c->stream), "fold");
+        cuda_check(cudaStreamSynchronize(c->stream), "fold");
+    } catch (...) {
+        cudaFree(d);
+        throw;
+    }
+    cudaFree(d);
+}
+
+// conserved_totals (solver.hpp:411-418)
+void t_conserved_totals(const Team& T, double* tot) {
+    const int nc = T.lead()->nc;
+    std::vector<double> acc(nc, 0.0);
+    // component-major in the reference: fold per component across slabs
+    for (int comp = 0; comp < nc; ++comp) {
+        std::vector<double> a1(1, 0.0);
+        fold_ranks(T, a1, [&](ign_context* c, std::vector<double>& a) {
+            const size_t P = c->plane;
+            std::vector<double> U(P);
+            cuda_check(cudaMemcpy(U.data(), c->S[c->cur] + comp * P, P * 8, cudaMemcpyDeviceToHost),
+                       "totals");
+            const int sx = c->nx + 2 * c->g, g = c->g;
+            double s = a[0];
+            for (int j = 0; j < c->ny; ++j)
+                for (int i = 0; i < c->nx; ++i) s += U[(size_t)(j + g) * sx + (i + g)];
+            a[0] = s;
+        });
+        tot[comp] = a1[0];
+    }
+}
+
+// product_mole_fraction (solver.hpp:387-407)
+double t_product_fraction(const Team& T) {
+    ign_context* L = T.lead();
+    int ico2 = -1, ih2o = -1;
+    for (int s = 0; s < L->ns; ++s) {
+        const char* nm = L->cfg.mix.species[s].name;
+        if (std::strncmp(nm, "CO2", IGN_NAME_LEN) == 0) ico2 = s;
+        if (std::strncmp(nm, "H2O", IGN_NAME_LEN) == 0) ih2o = s;
+    }
+    if (ico2 < 0 && ih2o < 0) return 0.0;
+    std::vector<double> acc(2, 0.0);
+    fold_ranks(T, acc, [&](ign_context* c, std::vector<double>& a) {
+        const size_t P = c->plane;
+        std::vector<double> Y(c->ns * P);
+        cuda_check(cudaMemcpy(Y.data(), c->prim + 6 * P, Y.size() * 8, cudaMemcpyDeviceToHost),
+                   "Y readback");
+        const DMix& m = c->kp.mix;
+        const int sx = c->nx + 2 * c->g, g = c->g;
+        double num = a[0], den = a[1];
+        for (int j = 0; j < c->ny; ++j)
+            for (int i = 0; i < c->nx; ++i) {
+                const size_t id = (size_t)(j + g) * sx + (i + g);
+                double y[kMaxSpecies], x[kMaxSpecies];
+                for (int s = 0; s < c->ns; ++s) y[s] = Y[s * P + id];
+                double inv = 0.0;
+                for (int s = 0; s < c->ns; ++s) inv += divW(m.sp[s], y[s]);
+                const double wbar = 1.0 / inv;
+                for (int s = 0; s < c->ns; ++s) x[s] = divW(m.sp[s], y[s] * wbar);
+                const double w = 1.0 / c->met.jac(i, j);
+                num += w * ((ico2 >= 0 ? x[ico2] : 0.0) + (ih2o >= 0 ? x[ih2o] : 0.0));
+                den += w;
+            }
+        a[0] = num;
+        a[1] = den;
+    });
+    return acc[0] / acc[1];
+}
+
+// ---------------------------------------------------------------- setup
 // detail::inflow_profile (boundary.hpp:94-124) — host side, glibc tanh.
 void inflow_profile(const ign_edge& es, double yc, int ns, double& u, double& v, double& T,
                     double* Y) {
@@ -285,160 +774,6 @@ void upload_state(ign_context* ctx, const std::vector<double>& Ut) {
                "state upload");
 }
 
-// ---------------------------------------------------------------- stage plumbing
-// Zeroes one step's clip slots unless a failure is pending (a pending failure
-// must keep the previous step's clips for last_clip, solver.hpp:847).
-__global__ void k_clip_reset(const ErrRec* err, unsigned long long* red, int slot) {
-    if (failed(err)) return;
-    red[2 + slot + threadIdx.x] = 0ull;
-}
-
-void launch_prepare(ign_context* ctx, double* U, int stage, int step) {
-    ctx->launches += timed(ctx, IGN_PROF_BC,
-                           [&] { return ctx->ks.bc(ctx->kp, U, stage, step, ctx->stream); });
-    ctx->launches += timed(ctx, IGN_PROF_PRIM,
-                           [&] { return ctx->ks.prim(ctx->kp, U, stage, step, ctx->stream); });
-}
-
-void launch_fluxes(ign_context* ctx, const double* U, int stage, int step) {
-    ctx->launches += timed(ctx, IGN_PROF_FACES, [&] {
-        return ctx->ks.faces(ctx->kp, ctx->cfg.scheme.scheme, ctx->cfg.scheme.split, U, stage,
-                             step, ctx->stream);
-    });
-    if (ctx->cfg.viscous)
-        ctx->launches += timed(ctx, IGN_PROF_VISC,
-                               [&] { return ctx->ks.visc(ctx->kp, stage, step, ctx->stream); });
-}
-
-int launch_assemble(ign_context* ctx, int mode, const double* U0, const double* Ucur,
-                    double* Uout, double dt, double w, double t, int stage, int step, int slot) {
-    return timed(ctx, IGN_PROF_ASSEMBLE, [&] {
-        return ctx->ks.assemble(ctx->kp, mode, U0, Ucur, Uout, dt, w, t, stage, step, slot,
-                                ctx->stream);
-    });
-}
-
-// One rk3_step (solver.hpp:304-332) enqueued without a host round trip;
-// post_prepare appends advance()'s prepare_stage(1) (solver.hpp:345).
-void launch_step(ign_context* ctx, int a, double time, double dt, int step, bool post_prepare) {
-    const int b = (a + 1) % 3, c = (a + 2) % 3;
-    const int slot = (step & 1) * 3;
-    k_clip_reset<<<1, 3, 0, ctx->stream>>>(ctx->err, ctx->red, slot);
-    ++ctx->launches;
-    double** S = ctx->S;
-    // Stage 1: U <- U0 + dt L(U0)   (ghosts/cache already fresh)
-    launch_fluxes(ctx, S[a], 1, step);
-    ctx->launches += launch_assemble(ctx, 1, S[a], S[a], S[b], dt, 0.0, time, 1, step, slot + 0);
-    launch_prepare(ctx, S[b], 2, step);
-    // Stage 2: U <- U0 + 1/4 [(U1 - U0) + dt L(U1)]
-    launch_fluxes(ctx, S[b], 2, step);
-    ctx->launches += launch_assemble(ctx, 2, S[a], S[b], S[c], dt, 0.25, time + dt, 2, step,
-                                     slot + 1);
-    launch_prepare(ctx, S[c], 3, step);
-    // Stage 3: U <- U0 + 2/3 [(U2 - U0) + dt L(U2)]
-    launch_fluxes(ctx, S[c], 3, step);
-    ctx->launches += launch_assemble(ctx, 2, S[a], S[c], S[b], dt, 2.0 / 3.0, time + 0.5 * dt,
-                                     3, step, slot + 2);
-    if (post_prepare) launch_prepare(ctx, S[b], 4, step);
-}
-
-double clip_of(const unsigned long long* red, int slot) {
-    double d;
-    std::memcpy(&d, &red[2 + slot], sizeof(d));
-    return d;
-}
-
-// n consecutive steps; on a device failure reproduces the reference's state,
-// time/iter and last_clip at the point it would have thrown.
-void run_steps(ign_context* ctx, double dt, int64_t n, bool post_prepare) {
-    if (n <= 0) return;
-    const int a0 = ctx->cur;
-    double t = ctx->time;
-    int64_t done = 0;
-    while (done < n) {
-        const int64_t chunk = std::min<int64_t>(n - done, 256);
-        for (int64_t k = 0; k < chunk; ++k) {
-            const int64_t s = done + k;
-            launch_step(ctx, (int)((a0 + s) % 3), t, dt, (int)s, post_prepare);
-            t += dt;
-        }
-        cuda_check(cudaGetLastError(), "kernel launch");
-        const DevFail f = sync_and_read(ctx);
-        unsigned long long red[8];
-        cuda_check(cudaMemcpy(red, ctx->red, sizeof(red), cudaMemcpyDeviceToHost), "reductions");
-        if (!f.any) {
-            // bookkeeping for the whole chunk
-            for (int64_t k = 0; k < chunk; ++k) {
-                ctx->time += dt;
-                ++ctx->iter;
-            }
-            const int last = (int)(done + chunk - 1);
-            const int slot = (last & 1) * 3;
-            ctx->last_clip = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
-                                      clip_of(red, slot + 2));
-            ctx->cur = (int)((a0 + done + chunk) % 3);
-            done += chunk;
-            continue;
-        }
-        const int64_t k = f.step;
-        // completed steps before the failing one
-        double clip_prev = ctx->last_clip;
-        if (k > done) {
-            const int slot = ((int)(k - 1) & 1) * 3;
-            clip_prev = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
-                                 clip_of(red, slot + 2));
-        }
-        for (int64_t q = done; q < k; ++q) {
-            ctx->time += dt;
-            ++ctx->iter;
-        }
-        const int ak = (int)((a0 + k) % 3);
-        const int slot = ((int)k & 1) * 3;
-        const Error e = to_error(ctx, f);
-        if (f.stage == 4) {  // advance's prepare_stage(1) after a completed step
-            ctx->time += dt;
-            ++ctx->iter;
-            ctx->cur = (ak + 1) % 3;
-            ctx->last_clip = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
-                                      clip_of(red, slot + 2));
-            throw e;
-        }
-        // inside rk3_step: last_clip covers the stages that completed post_stage
-        double lc = clip_prev;
-        for (unsigned s = 1; s < f.stage; ++s)
-            lc = s == 1 ? clip_of(red, slot) : std::max(lc, clip_of(red, slot + s - 1));
-        ctx->last_clip = lc;
-        if (e.status == IGN_STEP_FAILURE) ctx->cur = ak;  // restore U0
-        else ctx->cur = f.stage <= 1 ? ak : f.stage == 2 ? (ak + 1) % 3 : (ak + 2) % 3;
-        throw e;
-    }
-}
-
-double stable_dt_impl(ign_context* ctx) {
-    unsigned long long init[2] = {0ull, 0x7ff0000000000000ull};
-    cuda_check(cudaMemcpyAsync(ctx->red, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream),
-               "dt reset");
-    ctx->launches += timed(ctx, IGN_PROF_DT, [&] { return ctx->ks.dt(ctx->kp, ctx->stream); });
-    check(ctx);
-    unsigned long long red[2];
-    cuda_check(cudaMemcpy(red, ctx->red, sizeof(red), cudaMemcpyDeviceToHost), "dt readback");
-    double lam_max, dt_chem;
-    std::memcpy(&lam_max, &red[0], sizeof(double));
-    std::memcpy(&dt_chem, &red[1], sizeof(double));
-    double dt = ctx->cfg.scheme.cfl / lam_max;
-    dt = smin(dt, dt_chem);
-    const ign_laser& L = ctx->cfg.laser;
-    if (L.present && L.energy != 0.0 && ctx->time - L.t0 < 6.0 * L.sigma_t &&
-        ctx->time + dt > L.t0 - 6.0 * L.sigma_t)
-        dt = smin(dt, L.sigma_t / 5.0);
-    return dt;
-}
-
-void prepare_impl(ign_context* ctx, int stage) {
-    launch_prepare(ctx, ctx->S[ctx->cur], stage, 0);
-    check(ctx);
-}
-
 void destroy_impl(ign_context* ctx) {
     if (!ctx) return;
     for (double* p : ctx->S) cudaFree(p);
@@ -450,14 +785,16 @@ void destroy_impl(ign_context* ctx) {
     cudaFree(ctx->Gv);
     cudaFree(ctx->rhs);
     for (double* p : ctx->inflow) cudaFree(p);
-    cudaFree(ctx->err);
+    for (double* p : ctx->wrap) cudaFree(p);
+    cudaFree(ctx->own_err);
     cudaFree(ctx->red);
     for (auto& r : ctx->prof_pending) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
     for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
 
@@ -467,13 +804,23 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->cfg = *cfg;
     ctx->device = cfg->device;
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    // Simulation::init (solver.hpp:82-101)
-    ctx->mesh = build_mesh(*cfg);
+    ctx->nranks = cfg->slab_count > 1 ? cfg->slab_count : 1;
+    ctx->rank = ctx->nranks > 1 ? cfg->slab_rank : 0;
+    if (ctx->rank < 0 || ctx->rank >= ctx->nranks) throw usage_error("slab_rank out of range");
+    // Simulation::init (solver.hpp:82-101), on this slab's rows
+    ctx->mesh = build_mesh(*cfg, ctx->nranks, ctx->rank);
     validate_config(*cfg, ctx->mesh);
-    ctx->met = compute_metrics(ctx->mesh, inviscid_metric_mode(*cfg), cfg->skew_beta);
+    const int imode = inviscid_metric_mode(*cfg);
+    ctx->met = compute_metrics(ctx->mesh, imode, cfg->skew_beta);
     ctx->metv = compute_metrics(ctx->mesh, MM_CENTRAL2, 0.0);
     ctx->integ = cfg->integ;
-    const int nx = cfg->nx, ny = cfg->ny, g = cfg->g, ns = cfg->mix.ns, nc = ns + 3;
+    const int nx = cfg->nx, ny = ctx->mesh.ny, g = cfg->g, ns = cfg->mix.ns, nc = ns + 3;
+    const int N = ctx->nranks, r = ctx->rank;
+    const bool py = cfg->periodic_y != 0;
+    if (N > 1) {
+        ctx->lo_peer = r > 0 ? r - 1 : (py ? N - 1 : -1);
+        ctx->hi_peer = r < N - 1 ? r + 1 : (py ? 0 : -1);
+    }
     ctx->nx = nx;
     ctx->ny = ny;
     ctx->g = g;
@@ -481,7 +828,8 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->nc = nc;
     const size_t P = static_cast<size_t>(nx + 2 * g) * (ny + 2 * g);
     ctx->plane = P;
-    cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+    ctx->stream = ctx->own_stream;
     for (auto& s : ctx->S) {
         s = dalloc(nc * P);
         cuda_check(cudaMemset(s, 0, nc * P * sizeof(double)), "memset");
@@ -515,8 +863,11 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     }
     // inflow profile tables (boundary.hpp:227-241 ghost targets)
     const ign_edge* edges[4] = {&cfg->bc.left, &cfg->bc.right, &cfg->bc.bottom, &cfg->bc.top};
+    int bc_type[4] = {edges[0]->type, edges[1]->type, edges[2]->type, edges[3]->type};
+    if (ctx->lo_peer >= 0) bc_type[2] = (r == 0) ? BC_HALO_WRAP : BC_HALO;
+    if (ctx->hi_peer >= 0) bc_type[3] = (r == N - 1) ? BC_HALO_WRAP : BC_HALO;
     for (int e = 0; e < 4; ++e) {
-        if (edges[e]->type != 3) continue;
+        if (bc_type[e] != 3) continue;
         const bool xedge = e < 2;
         const int tlo = xedge ? 0 : -g, ntr = xedge ? ny : nx + 2 * g;
         std::vector<double> tab(static_cast<size_t>(ntr) * g * (3 + ns));
@@ -543,9 +894,34 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
                               cudaMemcpyHostToDevice),
                    "inflow upload");
     }
+    // periodic wrap across slabs: ratio J(src)/J(dst) of the reference's
+    // periodic copy (boundary.hpp:146-149); src rows belong to the far slab
+    const int sx = nx + 2 * g;
+    for (int side = 0; side < 2; ++side) {
+        if (bc_type[2 + side] != BC_HALO_WRAP) continue;
+        const int NG = ctx->mesh.ny_glob;
+        // dst global rows: bottom -g..-1, top NG..NG+g-1; src: NG-g..NG-1 / 0..g-1
+        const int dlo = side == 0 ? -g : NG, slo = side == 0 ? NG - g : 0;
+        const std::vector<double> Jd = jac_rows(ctx->mesh, imode, cfg->skew_beta, dlo, dlo + g);
+        const std::vector<double> Js = jac_rows(ctx->mesh, imode, cfg->skew_beta, slo, slo + g);
+        std::vector<double> tab(size_t(g) * sx);
+        for (int k = 1; k <= g; ++k) {
+            // ghost layer k: dst row (bottom) -k / (top) NG-1+k; src row NG-k / k-1
+            const int drow = side == 0 ? -k - dlo : NG - 1 + k - dlo;
+            const int srow = side == 0 ? NG - k - slo : k - 1 - slo;
+            for (int t = -g; t < nx + g; ++t)
+                tab[size_t(k - 1) * sx + (t + g)] =
+                    Js[size_t(srow) * sx + (t + g)] / Jd[size_t(drow) * sx + (t + g)];
+        }
+        ctx->wrap[side] = dalloc(tab.size());
+        cuda_check(cudaMemcpy(ctx->wrap[side], tab.data(), tab.size() * sizeof(double),
+                              cudaMemcpyHostToDevice),
+                   "wrap upload");
+    }
     void* p = nullptr;
     cuda_check(cudaMalloc(&p, sizeof(ErrRec)), "cudaMalloc");
-    ctx->err = static_cast<ErrRec*>(p);
+    ctx->own_err = static_cast<ErrRec*>(p);
+    ctx->err = ctx->own_err;
     cuda_check(cudaMemset(ctx->err, 0xff, sizeof(ErrRec)), "memset");
     cuda_check(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc");
     ctx->red = static_cast<unsigned long long*>(p);
@@ -556,15 +932,19 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     k.nx = nx;
     k.ny = ny;
     k.g = g;
-    k.sx = nx + 2 * g;
+    k.sx = sx;
     k.plane = static_cast<long long>(P);
+    k.j0 = ctx->mesh.j0;
+    k.ny_glob = ctx->mesh.ny_glob;
     k.ns = ns;
     k.viscous = cfg->viscous;
     for (int e = 0; e < 4; ++e) {
-        k.bc_type[e] = edges[e]->type;
+        k.bc_type[e] = bc_type[e];
         k.T_wall[e] = edges[e]->T_wall;
         k.inflow[e] = ctx->inflow[e];
     }
+    k.wrap[0] = ctx->wrap[0];
+    k.wrap[1] = ctx->wrap[1];
     k.sigma_out_right = cfg->bc.right.sigma_out;
     k.p_target_right = cfg->bc.right.p_target;
     k.lodi = cfg->bc.right.type == 4;
@@ -607,6 +987,34 @@ void metrics_out(const HMetrics& m, double* out, size_t P) {
     for (int k = 0; k < 5; ++k) copy_hfield(*f[k], out + k * P);
 }
 
+// advance (solver.hpp:336-349) over a team
+void t_advance(const Team& T, ign_step_hook hook, void* user) {
+    ign_context* L = T.lead();
+    t_prepare_sync(T, 1);
+    const ign_integrator& in = L->integ;
+    const double t_eps = 1e-12 * std::max(1.0, std::abs(in.t_end));
+    if (in.fixed_dt > 0.0 && !hook) {
+        // pinned step, no hook: the step count is known up front
+        int64_t n = 0;
+        double t = L->time;
+        int64_t it = L->iter;
+        while (it < in.max_iter && t < in.t_end - t_eps) {
+            t += in.fixed_dt;
+            ++it;
+            ++n;
+        }
+        t_run_steps(T, in.fixed_dt, n, true);
+        return;
+    }
+    while (L->iter < in.max_iter && L->time < in.t_end - t_eps) {
+        double dt = in.fixed_dt > 0.0 ? in.fixed_dt : t_stable_dt(T);
+        if (in.fixed_dt <= 0.0) dt = smin(dt, in.t_end - L->time);
+        t_run_steps(T, dt, 1, false);
+        t_prepare_sync(T, 1);
+        if (hook) hook(L, user);
+    }
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -618,7 +1026,7 @@ int ign_create(const ign_config* cfg, ign_context** out) {
     if (!out) return IGN_USAGE_ERROR;
     *out = nullptr;
     ign_context* ctx = new ign_context();
-    const int st = guarded(nullptr, [&] { create_impl(cfg, ctx); });
+    const int st = guarded_err(nullptr, -1, [&] { create_impl(cfg, ctx); });
     if (st != IGN_OK) {
         destroy_impl(ctx);
         return st;
@@ -628,7 +1036,9 @@ int ign_create(const ign_config* cfg, ign_context** out) {
 }
 
 void ign_destroy(ign_context* ctx) {
-    if (ctx) cudaSetDevice(ctx->device);
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->group) return;  // owned by its group until ign_group_destroy
     destroy_impl(ctx);
 }
 
@@ -658,8 +1068,8 @@ int ign_get_metrics(const ign_context* ctx, int which, double* out) {
 }
 
 int ign_set_initial_condition(ign_context* ctx, ign_ic_fn fn, void* user) {
-    return guarded(ctx, [&] {
-        const int g = ctx->g, ns = ctx->ns, nc = ctx->nc;
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
+        const int g = ctx->g, nc = ctx->nc;
         const size_t P = ctx->plane;
         std::vector<double> Ut(nc * P);
         size_t k = 0;
@@ -672,13 +1082,12 @@ int ign_set_initial_condition(ign_context* ctx, ign_ic_fn fn, void* user) {
                 const double invJ = 1.0 / ctx->met.jac(i, j);
                 for (int c = 0; c < nc; ++c) Ut[c * P + k] = U[c] * invJ;
             }
-        (void)ns;
         upload_state(ctx, Ut);
     });
 }
 
 int ign_set_initial_primitives(ign_context* ctx, const double* prim) {
-    return guarded(ctx, [&] {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
         const int ns = ctx->ns, nc = ctx->nc;
         const size_t P = ctx->plane;
         std::vector<double> Ut(nc * P);
@@ -696,7 +1105,7 @@ int ign_set_initial_primitives(ign_context* ctx, const double* prim) {
 }
 
 int ign_set_state(ign_context* ctx, const double* Ut, const double* Tc) {
-    return guarded(ctx, [&] {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
         cuda_check(cudaMemcpy(ctx->S[ctx->cur], Ut, ctx->nc * ctx->plane * sizeof(double),
                               cudaMemcpyHostToDevice),
                    "set_state");
@@ -708,7 +1117,7 @@ int ign_set_state(ign_context* ctx, const double* Ut, const double* Tc) {
 }
 
 int ign_get_state(ign_context* ctx, double* Ut) {
-    return guarded(ctx, [&] {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
         cuda_check(cudaMemcpy(Ut, ctx->S[ctx->cur], ctx->nc * ctx->plane * sizeof(double),
                               cudaMemcpyDeviceToHost),
                    "get_state");
@@ -716,7 +1125,7 @@ int ign_get_state(ign_context* ctx, double* Ut) {
 }
 
 int ign_get_cache(ign_context* ctx, double* prim) {
-    return guarded(ctx, [&] {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
         cuda_check(cudaMemcpy(prim, ctx->prim, (6 + ctx->ns) * ctx->plane * sizeof(double),
                               cudaMemcpyDeviceToHost),
                    "get_cache");
@@ -744,31 +1153,41 @@ int ign_set_integrator(ign_context* ctx, const ign_integrator* in) {
 
 int ign_refill_ghosts(ign_context* ctx) {
     return guarded(ctx, [&] {
-        ctx->launches += ctx->ks.bc(ctx->kp, ctx->S[ctx->cur], 0, 0, ctx->stream);
-        check(ctx);
+        const Team T = solo(ctx);
+        ctx->launches += ctx->ks.bc(ctx->kp, ctx->S[ctx->cur], 0, 0, 0, ctx->stream);
+        t_exchange(T, ctx->cur);
+        ctx->launches += ctx->ks.bc(ctx->kp, ctx->S[ctx->cur], 1, 0, 0, ctx->stream);
+        t_errsync(T);
+        check(T);
     });
 }
 
 int ign_refresh_primitives(ign_context* ctx, int stage) {
     return guarded(ctx, [&] {
         ctx->launches += ctx->ks.prim(ctx->kp, ctx->S[ctx->cur], stage, 0, ctx->stream);
-        check(ctx);
+        t_errsync(solo(ctx));
+        check(solo(ctx));
     });
 }
 
 int ign_prepare_stage(ign_context* ctx, int stage) {
-    return guarded(ctx, [&] { prepare_impl(ctx, stage); });
+    return guarded(ctx, [&] { t_prepare_sync(solo(ctx), stage); });
 }
 
 int ign_compute_rhs(ign_context* ctx, double t_stage, int stage, double* rhs) {
     return guarded(ctx, [&] {
+        const Team T = solo(ctx);
         const size_t n = ctx->nc * ctx->plane;
         if (!ctx->rhs) ctx->rhs = dalloc(n);
         cuda_check(cudaMemsetAsync(ctx->rhs, 0, n * sizeof(double), ctx->stream), "memset");
         const double* U = ctx->S[ctx->cur];
-        launch_fluxes(ctx, U, stage, 0);
-        ctx->launches += launch_assemble(ctx, 0, U, U, ctx->rhs, 0.0, 0.0, t_stage, stage, 0, 0);
-        check(ctx);
+        t_fluxes(T, ctx->cur, stage, 0);
+        ctx->launches += timed(ctx, IGN_PROF_ASSEMBLE, [&] {
+            return ctx->ks.assemble(ctx->kp, 0, U, U, ctx->rhs, 0.0, 0.0, t_stage, stage, 0, 0,
+                                    ctx->stream);
+        });
+        t_errsync(T);
+        check(T);
         if (rhs)
             cuda_check(cudaMemcpy(rhs, ctx->rhs, n * sizeof(double), cudaMemcpyDeviceToHost),
                        "rhs readback");
@@ -776,98 +1195,27 @@ int ign_compute_rhs(ign_context* ctx, double t_stage, int stage, double* rhs) {
 }
 
 int ign_stable_dt(ign_context* ctx, double* dt) {
-    return guarded(ctx, [&] { *dt = stable_dt_impl(ctx); });
+    return guarded(ctx, [&] { *dt = t_stable_dt(solo(ctx)); });
 }
 
 int ign_rk3_step(ign_context* ctx, double dt) {
-    return guarded(ctx, [&] { run_steps(ctx, dt, 1, false); });
+    return guarded(ctx, [&] { t_run_steps(solo(ctx), dt, 1, false); });
 }
 
 int ign_rk3_steps(ign_context* ctx, double dt, int64_t n) {
-    return guarded(ctx, [&] { run_steps(ctx, dt, n, true); });
+    return guarded(ctx, [&] { t_run_steps(solo(ctx), dt, n, true); });
 }
 
-// Simulation::advance (solver.hpp:336-349).  With a pinned step and no hook the
-// step count is known up front, so the steps are enqueued back to back.
 int ign_advance(ign_context* ctx, ign_step_hook hook, void* user) {
-    return guarded(ctx, [&] {
-        prepare_impl(ctx, 1);
-        const ign_integrator& in = ctx->integ;
-        const double t_eps = 1e-12 * std::max(1.0, std::abs(in.t_end));
-        if (in.fixed_dt > 0.0 && !hook) {
-            int64_t n = 0;
-            double t = ctx->time;
-            int64_t it = ctx->iter;
-            while (it < in.max_iter && t < in.t_end - t_eps) {
-                t += in.fixed_dt;
-                ++it;
-                ++n;
-            }
-            run_steps(ctx, in.fixed_dt, n, true);
-            return;
-        }
-        while (ctx->iter < in.max_iter && ctx->time < in.t_end - t_eps) {
-            double dt = in.fixed_dt > 0.0 ? in.fixed_dt : stable_dt_impl(ctx);
-            if (in.fixed_dt <= 0.0) dt = smin(dt, in.t_end - ctx->time);
-            run_steps(ctx, dt, 1, false);
-            prepare_impl(ctx, 1);
-            if (hook) hook(ctx, user);
-        }
-    });
+    return guarded(ctx, [&] { t_advance(solo(ctx), hook, user); });
 }
 
-// conserved_totals (solver.hpp:411-418): serial host sum in the reference order
 int ign_conserved_totals(ign_context* ctx, double* tot) {
-    return guarded(ctx, [&] {
-        const size_t P = ctx->plane;
-        std::vector<double> Ut(ctx->nc * P);
-        cuda_check(cudaMemcpy(Ut.data(), ctx->S[ctx->cur], Ut.size() * 8, cudaMemcpyDeviceToHost),
-                   "totals");
-        const int sx = ctx->nx + 2 * ctx->g, g = ctx->g;
-        for (int c = 0; c < ctx->nc; ++c) {
-            double s = 0.0;
-            for (int j = 0; j < ctx->ny; ++j)
-                for (int i = 0; i < ctx->nx; ++i) s += Ut[c * P + (size_t)(j + g) * sx + (i + g)];
-            tot[c] = s;
-        }
-    });
+    return guarded(ctx, [&] { t_conserved_totals(solo(ctx), tot); });
 }
 
-// product_mole_fraction (solver.hpp:387-407), serial host sum
 int ign_product_mole_fraction(ign_context* ctx, double* out) {
-    return guarded(ctx, [&] {
-        int ico2 = -1, ih2o = -1;
-        for (int s = 0; s < ctx->ns; ++s) {
-            const char* nm = ctx->cfg.mix.species[s].name;
-            if (std::strncmp(nm, "CO2", IGN_NAME_LEN) == 0) ico2 = s;
-            if (std::strncmp(nm, "H2O", IGN_NAME_LEN) == 0) ih2o = s;
-        }
-        if (ico2 < 0 && ih2o < 0) {
-            *out = 0.0;
-            return;
-        }
-        const size_t P = ctx->plane;
-        std::vector<double> Y(ctx->ns * P);
-        cuda_check(cudaMemcpy(Y.data(), ctx->prim + 6 * P, Y.size() * 8, cudaMemcpyDeviceToHost),
-                   "Y readback");
-        const DMix& m = ctx->kp.mix;
-        const int sx = ctx->nx + 2 * ctx->g, g = ctx->g;
-        double num = 0.0, den = 0.0;
-        for (int j = 0; j < ctx->ny; ++j)
-            for (int i = 0; i < ctx->nx; ++i) {
-                const size_t id = (size_t)(j + g) * sx + (i + g);
-                double y[kMaxSpecies], x[kMaxSpecies];
-                for (int s = 0; s < ctx->ns; ++s) y[s] = Y[s * P + id];
-                double inv = 0.0;
-                for (int s = 0; s < ctx->ns; ++s) inv += divW(m.sp[s], y[s]);
-                const double wbar = 1.0 / inv;
-                for (int s = 0; s < ctx->ns; ++s) x[s] = divW(m.sp[s], y[s] * wbar);
-                const double w = 1.0 / ctx->met.jac(i, j);
-                num += w * ((ico2 >= 0 ? x[ico2] : 0.0) + (ih2o >= 0 ? x[ih2o] : 0.0));
-                den += w;
-            }
-        *out = num / den;
-    });
+    return guarded(ctx, [&] { *out = t_product_fraction(solo(ctx)); });
 }
 
 int ign_last_clip(const ign_context* ctx, double* clip) {
@@ -876,34 +1224,28 @@ int ign_last_clip(const ign_context* ctx, double* clip) {
 }
 
 int ign_host_metrics(const ign_config* cfg, int which, double* out, ign_error* err) {
-    try {
-        const HMesh m = build_mesh(*cfg);
+    return guarded_err(err, -1, [&] {
+        const int nr = cfg->slab_count > 1 ? cfg->slab_count : 1;
+        const HMesh m = build_mesh(*cfg, nr, nr > 1 ? cfg->slab_rank : 0);
         const HMetrics mf = which == 0 ? compute_metrics(m, inviscid_metric_mode(*cfg), cfg->skew_beta)
                                        : compute_metrics(m, MM_CENTRAL2, 0.0);
         metrics_out(mf, out, mf.jac.d.size());
-        return IGN_OK;
-    } catch (const Error& e) {
-        set_error(err, e);
-        return e.status;
-    }
+    });
 }
 
 int ign_host_mesh(const ign_config* cfg, double* x, double* y, ign_error* err) {
-    try {
-        const HMesh m = build_mesh(*cfg);
+    return guarded_err(err, -1, [&] {
+        const int nr = cfg->slab_count > 1 ? cfg->slab_count : 1;
+        const HMesh m = build_mesh(*cfg, nr, nr > 1 ? cfg->slab_rank : 0);
         copy_hfield(m.x, x);
         copy_hfield(m.y, y);
-        return IGN_OK;
-    } catch (const Error& e) {
-        set_error(err, e);
-        return e.status;
-    }
+    });
 }
 
 int64_t ign_kernel_launches(const ign_context* ctx) { return ctx ? ctx->launches : 0; }
 
 int ign_profile_enable(ign_context* ctx, int on) {
-    return guarded(ctx, [&] {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
         cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
         prof_harvest(ctx);
         ctx->prof_on = on != 0;
@@ -915,7 +1257,7 @@ int ign_profile_enable(ign_context* ctx, int on) {
 }
 
 int ign_profile_read(ign_context* ctx, double* ms, int64_t* counts) {
-    return guarded(ctx, [&] {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
         cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
         prof_harvest(ctx);
         for (int k = 0; k < IGN_PROF_CLASSES; ++k) {
@@ -926,5 +1268,92 @@ int ign_profile_read(ign_context* ctx, double* ms, int64_t* counts) {
 }
 
 void* ign_stream_handle(const ign_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+// ---------------------------------------------------------------- slabs over NCCL
+int ign_nccl_unique_id(uint8_t* id) {
+    ign_error e{};
+    return guarded_err(&e, -1, [&] {
+        if (!nccl().ok) throw Error(IGN_CUDA_ERROR, nccl().why);
+        ncclUniqueId u;
+        nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId");
+        std::memcpy(id, u.internal, IGN_NCCL_ID_BYTES);
+    });
+}
+
+int ign_attach_nccl(ign_context* ctx, const uint8_t* id, int nranks, int rank) {
+    return guarded(ctx, [&] {
+        if (!nccl().ok) throw Error(IGN_CUDA_ERROR, nccl().why);
+        if (nranks != ctx->nranks || rank != ctx->rank)
+            throw usage_error("ign_attach_nccl: rank/size differ from the slab config");
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, IGN_NCCL_ID_BYTES);
+        nccl_check(nccl().CommInitRank(&ctx->comm, nranks, u, rank), "ncclCommInitRank");
+    });
+}
+
+// ---------------------------------------------------------------- single-process groups
+int ign_group_create(ign_context** members, int n, ign_group** out) {
+    ign_error e{};
+    *out = nullptr;
+    auto* grp = new ign_group();
+    const int st = guarded_err(&e, members && n > 0 ? members[0]->device : -1, [&] {
+        if (n < 1) throw usage_error("ign_group_create: empty group");
+        for (int r = 0; r < n; ++r) {
+            ign_context* c = members[r];
+            if (!c || c->nranks != n || c->rank != r || c->device != members[0]->device ||
+                c->group || c->comm)
+                throw usage_error("ign_group_create: members must be slabs 0..n-1 of one config");
+        }
+        for (int r = 0; r < n; ++r) {
+            ign_context* c = members[r];
+            c->group = grp;
+            c->stream = members[0]->own_stream;  // lockstep on one stream
+            c->err = members[0]->own_err;        // one error word for the group
+            c->kp.err = c->err;
+            grp->m.push_back(c);
+        }
+    });
+    if (st != IGN_OK) {
+        delete grp;
+        return st;
+    }
+    *out = grp;
+    return IGN_OK;
+}
+
+void ign_group_destroy(ign_group* grp) {
+    if (!grp) return;
+    for (ign_context* c : grp->m) {
+        cudaSetDevice(c->device);
+        c->group = nullptr;
+        destroy_impl(c);
+    }
+    delete grp;
+}
+
+int ign_group_last_error(const ign_group* grp, ign_error* err) {
+    *err = grp->lasterr;
+    return IGN_OK;
+}
+
+static int group_guarded(ign_group* grp, const std::function<void(const Team&)>& f) {
+    return guarded_err(&grp->lasterr, grp->m[0]->device, [&] { f(Team{grp->m}); });
+}
+
+int ign_group_prepare_stage(ign_group* grp, int stage) {
+    return group_guarded(grp, [&](const Team& T) { t_prepare_sync(T, stage); });
+}
+
+int ign_group_rk3_steps(ign_group* grp, double dt, int64_t n) {
+    return group_guarded(grp, [&](const Team& T) { t_run_steps(T, dt, n, true); });
+}
+
+int ign_group_stable_dt(ign_group* grp, double* dt) {
+    return group_guarded(grp, [&](const Team& T) { *dt = t_stable_dt(T); });
+}
+
+int ign_group_conserved_totals(ign_group* grp, double* tot) {
+    return group_guarded(grp, [&](const Team& T) { t_conserved_totals(T, tot); });
+}
 
 }  // extern "C"

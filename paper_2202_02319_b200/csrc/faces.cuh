@@ -115,8 +115,9 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     const bool my_active = DIR == 0 ? my_f <= P.nx : (my_col < P.nx && my_f <= P.ny);
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
     auto err_index = [&](int f, int col) -> unsigned long long {
-        return DIR == 0 ? (unsigned long long)col * (P.nx + 1) + f
-                        : (unsigned long long)col * (P.ny + 1) + f;
+        // global (line, face) order of inviscid_direction (solver.hpp:450-481)
+        return DIR == 0 ? (unsigned long long)(col + P.j0) * (P.nx + 1) + f
+                        : (unsigned long long)col * (P.ny_glob + 1) + (f + P.j0);
     };
     // face metric (solver.hpp:484-489): mean of the two node metrics
     const long long il = DIR == 0 ? pidx(P, my_f - 1, my_col) : pidx(P, my_col, my_f - 1);

@@ -2,6 +2,7 @@
 // (the reference's flags) so setup arithmetic is bit-identical to the oracle.
 #include "host_core.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -18,10 +19,32 @@ void skew_jacobian(double xc, double yc, double beta, double L, double d[4]) {
     d[3] = 1.0 + beta * std::sin(k * xc);
 }
 
-// detail::index_deriv (metrics.hpp:45-67)
-double index_deriv(const HField& f, int i, int j, bool xdir, int pref) {
-    const int g = f.g;
-    const int n = xdir ? f.nx : f.ny;
+// Coordinates of the global padded rows [wlo, whi) of the mesh (all columns).
+struct CoordWindow {
+    int nx, g, wlo, whi;
+    std::vector<double> x, y;
+    double X(int i, int jg) const { return x[size_t(jg - wlo) * (nx + 2 * g) + (i + g)]; }
+    double Y(int i, int jg) const { return y[size_t(jg - wlo) * (nx + 2 * g) + (i + g)]; }
+};
+
+CoordWindow coord_window(const HMesh& m, int wlo, int whi) {
+    CoordWindow w{m.nx, m.g, wlo, whi, {}, {}};
+    const size_t n = size_t(m.nx + 2 * m.g) * (whi - wlo);
+    w.x.resize(n);
+    w.y.resize(n);
+    for (int jg = wlo; jg < whi; ++jg)
+        for (int i = -m.g; i < m.nx + m.g; ++i) {
+            const size_t k = size_t(jg - wlo) * (m.nx + 2 * m.g) + (i + m.g);
+            m.coords(i, jg, w.x[k], w.y[k]);
+        }
+    return w;
+}
+
+// detail::index_deriv (metrics.hpp:45-67) on a coordinate window; n and g are
+// the GLOBAL extents so rim fallbacks match the single-domain mesh.
+template <class F>
+double index_deriv(const F& f, int nx, int ny_glob, int g, int i, int j, bool xdir, int pref) {
+    const int n = xdir ? nx : ny_glob;
     const int c = xdir ? i : j;
     auto at = [&](int off) { return xdir ? f(i + off, j) : f(i, j + off); };
     int w = pref;
@@ -42,7 +65,25 @@ double index_deriv(const HField& f, int i, int j, bool xdir, int pref) {
 
 }  // namespace
 
-HMesh build_mesh(const ign_config& c) {
+void slab_rows(int ny_glob, int nranks, int rank, int& lo, int& count) {
+    const int base = ny_glob / nranks, rem = ny_glob % nranks;
+    lo = rank * base + (rank < rem ? rank : rem);
+    count = base + (rank < rem ? 1 : 0);
+}
+
+void HMesh::coords(int i, int jg, double& X, double& Y) const {
+    const double xc = xi(i), yc = eta_glob(jg);  // build_uniform (mesh.hpp:70-75)
+    if (!skew) {
+        X = xc;
+        Y = yc;
+        return;
+    }
+    const double L = lx;  // apply_skew (mesh.hpp:108-115)
+    X = xc * (1.0 + beta * std::sin(2.0 * M_PI * yc / L));
+    Y = yc * (1.0 + beta * std::sin(2.0 * M_PI * xc / L));
+}
+
+HMesh build_mesh(const ign_config& c, int nranks, int rank) {
     // build_uniform (mesh.hpp:48-77)
     if (c.lx <= 0.0 || c.ly <= 0.0)
         throw config_error("build_uniform: domain extents must be positive");
@@ -52,7 +93,10 @@ HMesh build_mesh(const ign_config& c) {
                            std::to_string(c.nx) + "x" + std::to_string(c.ny));
     HMesh m;
     m.nx = c.nx;
-    m.ny = c.ny;
+    m.ny_glob = c.ny;
+    slab_rows(c.ny, nranks, rank, m.j0, m.ny);
+    if (m.ny < c.g)
+        throw config_error("slab decomposition: each slab needs at least g rows");
     m.g = c.g;
     m.lx = c.lx;
     m.ly = c.ly;
@@ -60,76 +104,96 @@ HMesh build_mesh(const ign_config& c) {
     m.cy = c.center_y;
     m.periodic_x = c.periodic_x != 0;
     m.periodic_y = c.periodic_y != 0;
+    m.skew = c.apply_skew != 0;
+    m.beta = c.skew_beta;
+    if (m.skew) {
+        // apply_skew (mesh.hpp:92-105) validation, over this slab's interior rows
+        if (std::abs(m.lx - m.ly) > 1e-14 * m.lx || m.cx != 0.0 || m.cy != 0.0)
+            throw config_error("apply_skew: mesh must be square and origin-centered");
+        const double L = m.lx;
+        for (int j = m.j0; j < m.j0 + m.ny; ++j)
+            for (int i = 0; i < m.nx; ++i) {
+                double d[4];
+                skew_jacobian(m.xi(i), m.eta_glob(j), m.beta, L, d);
+                if (d[0] * d[3] - d[1] * d[2] <= 0.0)
+                    throw numerics_error("apply_skew: grid folding (J <= 0) at node (" +
+                                         std::to_string(i) + "," + std::to_string(j) +
+                                         ") for beta=" + std::to_string(m.beta));
+            }
+    }
     m.x = HField(m.nx, m.ny, m.g);
     m.y = HField(m.nx, m.ny, m.g);
     for (int j = -m.g; j < m.ny + m.g; ++j)
-        for (int i = -m.g; i < m.nx + m.g; ++i) {
-            m.x(i, j) = m.xi(i);
-            m.y(i, j) = m.eta(j);
-        }
-    if (!c.apply_skew) return m;
-    // apply_skew (mesh.hpp:92-117)
-    const double beta = c.skew_beta;
-    if (std::abs(m.lx - m.ly) > 1e-14 * m.lx || m.cx != 0.0 || m.cy != 0.0)
-        throw config_error("apply_skew: mesh must be square and origin-centered");
-    const double L = m.lx;
-    for (int j = 0; j < m.ny; ++j)
-        for (int i = 0; i < m.nx; ++i) {
-            double d[4];
-            skew_jacobian(m.xi(i), m.eta(j), beta, L, d);
-            if (d[0] * d[3] - d[1] * d[2] <= 0.0)
-                throw numerics_error("apply_skew: grid folding (J <= 0) at node (" +
-                                     std::to_string(i) + "," + std::to_string(j) +
-                                     ") for beta=" + std::to_string(beta));
-        }
-    const HField x0 = m.x, y0 = m.y;
-    for (int j = -m.g; j < m.ny + m.g; ++j)
-        for (int i = -m.g; i < m.nx + m.g; ++i) {
-            const double xc = x0(i, j);
-            const double yc = y0(i, j);
-            m.x(i, j) = xc * (1.0 + beta * std::sin(2.0 * M_PI * yc / L));
-            m.y(i, j) = yc * (1.0 + beta * std::sin(2.0 * M_PI * xc / L));
-        }
+        for (int i = -m.g; i < m.nx + m.g; ++i) m.coords(i, m.j0 + j, m.x(i, j), m.y(i, j));
     return m;
 }
 
 HMetrics compute_metrics(const HMesh& mesh, int mode, double beta) {
-    const int g = mesh.g;
     HMetrics mf;
+    const int g = mesh.g;
     mf.jac = HField(mesh.nx, mesh.ny, g);
     mf.m_xi_x = HField(mesh.nx, mesh.ny, g);
     mf.m_xi_y = HField(mesh.nx, mesh.ny, g);
     mf.m_eta_x = HField(mesh.nx, mesh.ny, g);
     mf.m_eta_y = HField(mesh.nx, mesh.ny, g);
+    double* out[5] = {mf.jac.d.data(), mf.m_xi_x.d.data(), mf.m_xi_y.d.data(),
+                      mf.m_eta_x.d.data(), mf.m_eta_y.d.data()};
+    metric_rows(mesh, mode, beta, mesh.j0 - g, mesh.j0 + mesh.ny + g, out);
+    return mf;
+}
+
+std::vector<double> jac_rows(const HMesh& mesh, int mode, double beta, int jlo, int jhi) {
+    const size_t n = size_t(mesh.nx + 2 * mesh.g) * (jhi - jlo);
+    std::vector<double> buf(5 * n);
+    double* out[5] = {buf.data(), buf.data() + n, buf.data() + 2 * n, buf.data() + 3 * n,
+                      buf.data() + 4 * n};
+    metric_rows(mesh, mode, beta, jlo, jhi, out);
+    buf.resize(n);
+    return buf;
+}
+
+void metric_rows(const HMesh& mesh, int mode, double beta, int jlo, int jhi, double* const* out) {
+    const int g = mesh.g;
+    const int sx = mesh.nx + 2 * g;
     const int pref = (mode == MM_ORDER6) ? 3 : (mode == MM_ORDER4) ? 2 : 1;
-    for (int j = -g; j < mesh.ny + g; ++j) {
+    // coordinates of the rows plus the 3-row stencil reach, clipped to the
+    // global padded box
+    const int wlo = std::max(jlo - g, -g);
+    const int whi = std::min(jhi + g, mesh.ny_glob + g);
+    const CoordWindow w =
+        mode == MM_ANALYTIC_SKEW ? CoordWindow{mesh.nx, g, 0, 0, {}, {}}
+                                 : coord_window(mesh, wlo, whi);
+    auto fx = [&](int i, int j) { return w.X(i, j); };
+    auto fy = [&](int i, int j) { return w.Y(i, j); };
+    for (int j = jlo; j < jhi; ++j) {  // global row
+        const size_t row = size_t(j - jlo) * sx;
         for (int i = -g; i < mesh.nx + g; ++i) {
             double x_xi, x_eta, y_xi, y_eta;
             if (mode == MM_ANALYTIC_SKEW) {
                 double d[4];
-                skew_jacobian(mesh.xi(i), mesh.eta(j), beta, mesh.lx, d);
+                skew_jacobian(mesh.xi(i), mesh.eta_glob(j), beta, mesh.lx, d);
                 x_xi = d[0] * mesh.dxi();
                 x_eta = d[1] * mesh.deta();
                 y_xi = d[2] * mesh.dxi();
                 y_eta = d[3] * mesh.deta();
             } else {
-                x_xi = index_deriv(mesh.x, i, j, true, pref);
-                x_eta = index_deriv(mesh.x, i, j, false, pref);
-                y_xi = index_deriv(mesh.y, i, j, true, pref);
-                y_eta = index_deriv(mesh.y, i, j, false, pref);
+                x_xi = index_deriv(fx, mesh.nx, mesh.ny_glob, g, i, j, true, pref);
+                x_eta = index_deriv(fx, mesh.nx, mesh.ny_glob, g, i, j, false, pref);
+                y_xi = index_deriv(fy, mesh.nx, mesh.ny_glob, g, i, j, true, pref);
+                y_eta = index_deriv(fy, mesh.nx, mesh.ny_glob, g, i, j, false, pref);
             }
             const double area = x_xi * y_eta - x_eta * y_xi;
-            if (!(area > 0.0) && i >= 0 && i < mesh.nx && j >= 0 && j < mesh.ny)
+            if (!(area > 0.0) && i >= 0 && i < mesh.nx && j >= 0 && j < mesh.ny_glob)
                 throw numerics_error("grid folding: J <= 0 at node (" + std::to_string(i) +
                                      "," + std::to_string(j) + ")");
-            mf.jac(i, j) = 1.0 / area;
-            mf.m_xi_x(i, j) = y_eta;
-            mf.m_xi_y(i, j) = -x_eta;
-            mf.m_eta_x(i, j) = -y_xi;
-            mf.m_eta_y(i, j) = x_xi;
+            const size_t k = row + (i + g);
+            out[0][k] = 1.0 / area;
+            out[1][k] = y_eta;
+            out[2][k] = -x_eta;
+            out[3][k] = -y_xi;
+            out[4][k] = x_xi;
         }
     }
-    return mf;
 }
 
 int inviscid_metric_mode(const ign_config& c) {

@@ -77,8 +77,24 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
     auto ij = [&](int a, int& i, int& j) {
         if (ypass) { i = t; j = a; } else { i = a; j = t; }
     };
+    // global (edge, t, k) order of the reference's loops (boundary.hpp:254-257)
+    const unsigned long long ekey =
+        ((unsigned long long)edge * (nx + 2 * g + P.ny_glob) + (ypass ? t - tlo : t + P.j0)) *
+        (g + 1);
     int gi, gj;
     switch (type) {
+    case BC_HALO:  // internal slab edge: ghost rows arrived from the neighbour
+        return;
+    case BC_HALO_WRAP: {  // periodic wrap across slabs: Ut_dst = Ut_src * J_src/J_dst
+        for (int k = 1; k <= g; ++k) {
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            const double ratio = P.wrap[side][(k - 1) * P.sx + (t + g)];
+            const long long d = pidx(P, gi, gj);
+#pragma unroll
+            for (int c = 0; c < NS + 3; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + d] * ratio;
+        }
+        return;
+    }
     case 0: {  // Periodic (boundary.hpp:203-209)
         for (int k = 1; k <= g; ++k) {
             int si, sj;
@@ -98,9 +114,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
             double rs;
             const int st = bc_prim_at<NS>(P, Ut, mi, mj, pt, rs);
             if (st) {
-                report(P.err, stage, PH_BC,
-                       ((unsigned long long)edge * (nx + 2 * g + ny) + (t - tlo)) * (g + 1) + k,
-                       st, step);
+                report(P.err, stage, PH_BC, ekey + k, st, step);
                 return;
             }
             pt.u = -pt.u;
@@ -121,9 +135,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
         double rs;
         const int st = bc_prim_at<NS>(P, Ut, ii, ji, inner, rs);
         if (st) {
-            report(P.err, stage, PH_BC,
-                   ((unsigned long long)edge * (nx + 2 * g + ny) + (t - tlo)) * (g + 1), st,
-                   step);
+            report(P.err, stage, PH_BC, ekey, st, step);
             return;
         }
         const double* prof = P.inflow[edge] + (long long)(t - tlo) * g * (3 + NS);
@@ -172,7 +184,8 @@ __global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
     double rs;
     const int st = primitives_from_conservative<NS>(U, P.mix, PT(P)[id], pt, &rs);
     if (st) {
-        report(P.err, stage, PH_PRIM, (unsigned long long)id, st, step);
+        report(P.err, stage, PH_PRIM, (unsigned long long)(id + (long long)P.j0 * P.sx), st,
+               step);
         return;
     }
     PRHO(P)[id] = pt.rho;
@@ -398,7 +411,7 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParam
             }
             if (P.laser.on)
                 r[NS + 2] += laser_power(ldg(P.xc + id), ldg(P.yc + id), t_stage, P.laser) * invJ;
-            const unsigned long long cell = (unsigned long long)j * P.nx + i;
+            const unsigned long long cell = (unsigned long long)(j + P.j0) * P.nx + i;
             bool bad = false;
 #pragma unroll
             for (int c = 0; c < NC; ++c) bad |= !isfinite(r[c]);
@@ -504,7 +517,7 @@ __global__ void __launch_bounds__(256) k_dt(const __grid_constant__ KParams P) {
 
 // ---------------------------------------------------------------- launcher table
 struct KernelSet {
-    int (*bc)(const KParams&, double* Ut, int stage, int step, cudaStream_t);
+    int (*bc)(const KParams&, double* Ut, int ypass, int stage, int step, cudaStream_t);
     int (*prim)(const KParams&, const double* Ut, int stage, int step, cudaStream_t);
     int (*faces)(const KParams&, int teno, int chr, const double* Ut, int stage, int step,
                  cudaStream_t);
@@ -516,11 +529,12 @@ struct KernelSet {
 };
 
 template <int NS> struct Launch {
-    static int bc(const KParams& P, double* Ut, int stage, int step, cudaStream_t s) {
-        const int nxp = P.ny, nyp = P.nx + 2 * P.g;
-        k_bc<NS><<<(2 * nxp + 127) / 128, 128, 0, s>>>(P, Ut, 0, stage, step);
-        k_bc<NS><<<(2 * nyp + 127) / 128, 128, 0, s>>>(P, Ut, 1, stage, step);
-        return 2;
+    // one ghost-fill pass: x edges over rows 0..ny-1 (ypass 0) or y edges over
+    // the full padded width (ypass 1) — boundary.hpp:254-257
+    static int bc(const KParams& P, double* Ut, int ypass, int stage, int step, cudaStream_t s) {
+        const int n = ypass ? P.nx + 2 * P.g : P.ny;
+        k_bc<NS><<<(2 * n + 127) / 128, 128, 0, s>>>(P, Ut, ypass, stage, step);
+        return 1;
     }
     static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
         const unsigned nb = (unsigned)((P.plane + 255) / 256);

@@ -12,7 +12,11 @@ namespace ign {
 
 // ---------------------------------------------------------------- errors
 // Device error word: the first failure in the reference's own order wins via
-// atomicMin on key = stage<<60 | phase<<52 | index<<4 | sub.
+// atomicMin on
+//   key = step<<44 | stage<<41 | phase<<38 | index<<3 | sub
+// (step within the current batch, 20 bits; index = GLOBAL row-major position,
+// 35 bits), so slabs of a decomposed domain agree on one first failure after
+// a MIN all-reduce of the word.
 enum Phase : unsigned {
     PH_BC = 1,     // StateError from fill_ghosts' prim_at (boundary.hpp:151-156)
     PH_PRIM = 2,   // StepFailure "stage state failure" (solver.hpp:162-165)
@@ -25,8 +29,6 @@ constexpr unsigned long long kNoError = ~0ull;
 
 struct ErrRec {
     unsigned long long key;
-    int32_t step;
-    int32_t _pad;
 };
 
 __device__ __forceinline__ bool failed(const ErrRec* e) {
@@ -35,18 +37,24 @@ __device__ __forceinline__ bool failed(const ErrRec* e) {
 
 __device__ __forceinline__ void report(ErrRec* e, unsigned stage, unsigned phase,
                                        unsigned long long idx, unsigned sub, int step) {
-    const unsigned long long key = ((unsigned long long)stage << 60) |
-                                   ((unsigned long long)phase << 52) | (idx << 4) | sub;
+    const unsigned long long key = ((unsigned long long)(step & 0xFFFFF) << 44) |
+                                   ((unsigned long long)stage << 41) |
+                                   ((unsigned long long)phase << 38) |
+                                   ((idx & ((1ull << 35) - 1)) << 3) | (sub & 7u);
     atomicMin(&e->key, key);
-    e->step = step;
 }
+
+// y-edge roles beyond the reference's BC types (boundary.hpp:16-22) for slabs
+enum : int32_t { BC_HALO_WRAP = 5, BC_HALO = 6 };
 
 // ---------------------------------------------------------------- params
 struct KParams {
     int32_t nx, ny, g, sx;
     long long plane;
+    int32_t j0, ny_glob;  // slab: global row of local row 0, global rows
     int32_t ns, viscous;
-    int32_t bc_type[4];  // left, right, bottom, top
+    int32_t bc_type[4];  // left, right, bottom, top (+ BC_HALO_WRAP / BC_HALO)
+    const double* wrap[2];  // [k][t] J_src/J_dst of periodic wrap ghost rows
     double T_wall[4];
     double sigma_out_right, p_target_right;
     double lx, ly, cx, cy;

@@ -218,3 +218,84 @@ class Simulation:
 
     def stream_handle(self) -> int:
         return int(self._api["stream_handle"](self._h) or 0)
+
+
+class SlabGroup:
+    """Single-process group of slab contexts (ign_group_*): the y-slabs of one
+    decomposed domain driven in lockstep on one GPU — the validation harness of
+    the multi-GPU path (halo rows by device copies instead of NCCL)."""
+
+    def __init__(self, cfg: abi.Config, nslabs: int, api: Optional[dict] = None):
+        from . import native
+        self._api = api or native.api()
+        self.members = []
+        for r in range(nslabs):
+            c = abi.Config()
+            C.memmove(C.byref(c), C.byref(cfg), C.sizeof(abi.Config))
+            c.slab_count, c.slab_rank = nslabs, r
+            self.members.append(Simulation(c, self._api))
+        arr = (C.c_void_p * nslabs)(*[m.handle.value for m in self.members])
+        g = C.c_void_p()
+        st = self._api["group_create"](arr, nslabs, C.byref(g))
+        if st != abi.IGN_OK:
+            raise_for(st, abi.Error())
+        self._g = g
+        for m in self.members:  # the group owns the contexts now
+            m._h = None
+        self._handles = [arr[k] for k in range(nslabs)]
+
+    def _check(self, st):
+        if st != abi.IGN_OK:
+            e = abi.Error()
+            self._api["group_last_error"](self._g, C.byref(e))
+            raise_for(st, e)
+
+    def member_call(self, k, name, *args):
+        return self._api[name](C.c_void_p(self._handles[k]), *args)
+
+    def set_state(self, k: int, Ut: np.ndarray, T: Optional[np.ndarray] = None):
+        Ut = np.ascontiguousarray(Ut, dtype=np.float64).reshape(-1)
+        Tp = None
+        if T is not None:
+            T = np.ascontiguousarray(T, dtype=np.float64).reshape(-1)
+            Tp = _dptr(T)
+        self._check(self.member_call(k, "set_state", _dptr(Ut), Tp))
+
+    def Ut(self, k: int) -> np.ndarray:
+        m = self.members[k]
+        out = np.empty(m.nc * m.plane)
+        self._check(self.member_call(k, "get_state", _dptr(out)))
+        return out.reshape((m.nc,) + m.shape)
+
+    def cache_T(self, k: int) -> np.ndarray:
+        m = self.members[k]
+        out = np.empty((6 + m.ns) * m.plane)
+        self._check(self.member_call(k, "get_cache", _dptr(out)))
+        return out.reshape((6 + m.ns,) + m.shape)[4]
+
+    def prepare_stage(self, stage: int = 1):
+        self._check(self._api["group_prepare_stage"](self._g, stage))
+
+    def rk3_steps(self, dt: float, n: int):
+        self._check(self._api["group_rk3_steps"](self._g, dt, n))
+
+    def stable_dt(self) -> float:
+        dt = C.c_double()
+        self._check(self._api["group_stable_dt"](self._g, C.byref(dt)))
+        return dt.value
+
+    def conserved_totals(self) -> np.ndarray:
+        out = np.empty(self.members[0].nc)
+        self._check(self._api["group_conserved_totals"](self._g, _dptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_g", None):
+            self._api["group_destroy"](self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

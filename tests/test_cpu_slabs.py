@@ -1,0 +1,96 @@
+"""CPU tests of the multi-GPU slab decomposition's host logic:
+partition, per-slab mesh/metric windows bit-identical to slices of the global
+arrays (so every slab computes exactly what the undecomposed domain computes),
+and the NCCL rendezvous over torch.distributed (gloo, world size 2)."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from paper_2202_02319_b200 import abi, configs, native
+from tests.parity import clone_cfg
+
+
+def slab_rows(ny, n, r):
+    base, rem = divmod(ny, n)
+    lo = r * base + min(r, rem)
+    return lo, base + (1 if r < rem else 0)
+
+
+def host(cfg, which):
+    api = native.api()
+    err = abi.Error()
+    # the library sizes the output from the (slab) config
+    n = cfg.slab_count if cfg.slab_count > 1 else 1
+    lo, cnt = slab_rows(cfg.ny, n, cfg.slab_rank if n > 1 else 0)
+    P = (cfg.nx + 2 * cfg.g) * (cnt + 2 * cfg.g)
+    out = np.empty(5 * P)
+    st = api["host_metrics"](C.byref(cfg), which, out.ctypes.data_as(C.POINTER(C.c_double)),
+                             C.byref(err))
+    assert st == 0, err.msg
+    return out.reshape(5, cnt + 2 * cfg.g, cfg.nx + 2 * cfg.g), lo, cnt
+
+
+@pytest.mark.parametrize("mk", [lambda: configs.tgv2d(24, ly_periods=2),
+                                lambda: configs.tgv2d(30, skew=0.15),
+                                lambda: configs.wall_channel(26),
+                                lambda: configs.tgv2d(20, scheme="weno3z")])
+@pytest.mark.parametrize("nslabs", [2, 3, 4])
+def test_slab_metrics_are_exact_slices(mk, nslabs):
+    cfg = mk().cfg
+    full = {w: host(cfg, w)[0] for w in (0, 1)}
+    for r in range(nslabs):
+        c = clone_cfg(cfg)
+        c.slab_count, c.slab_rank = nslabs, r
+        for w in (0, 1):
+            m, lo, cnt = host(c, w)
+            want = full[w][:, lo:lo + cnt + 2 * cfg.g, :]
+            assert np.array_equal(m.view(np.uint64), want.view(np.uint64)), (r, w)
+
+
+def test_slab_partition_covers_rows():
+    for ny in (7, 64, 1000, 4099):
+        for n in (1, 2, 3, 8):
+            rows = [slab_rows(ny, n, r) for r in range(n)]
+            assert rows[0][0] == 0 and sum(c for _, c in rows) == ny
+            assert all(rows[k][0] + rows[k][1] == rows[k + 1][0] for k in range(n - 1))
+
+
+def _rendezvous(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank 0 would call ign_nccl_unique_id; here a stand-in id exercises the
+    # broadcast the bench performs before ign_attach_nccl
+    uid = torch.zeros(abi.IGN_NCCL_ID_BYTES, dtype=torch.uint8)
+    if rank == 0:
+        uid[:] = torch.arange(abi.IGN_NCCL_ID_BYTES, dtype=torch.uint8)
+    dist.broadcast(uid, 0)
+    lo, cnt = slab_rows(4096 * world, world, rank)
+    t = torch.tensor([float(lo), float(cnt)])
+    dist.all_reduce(t)
+    q.put((rank, bytes(uid.numpy()), lo, cnt, float(t[0]), float(t[1])))
+    dist.destroy_process_group()
+
+
+def test_multirank_rendezvous_gloo():
+    """World-size-2 run of the bench's multi-GPU plumbing on CPU (gloo)."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_rendezvous, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0][1] == res[1][1] == bytes(range(abi.IGN_NCCL_ID_BYTES))
+    assert res[0][2:4] == (0, 4096) and res[1][2:4] == (4096, 4096)
+    assert res[0][4] == 4096.0 and res[0][5] == 8192.0
