@@ -115,11 +115,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_case(args):
+def make_case(args, nslabs: int = 1):
+    """nslabs > 1: weak scaling — the domain grows to n x (n*nslabs) rows so
+    every GPU keeps an n x n slab (TGV: periodic copies stacked along y)."""
     from paper_2202_02319_b200 import configs
     if args.case == "h2o2":
-        return configs.h2o2_counterflow(args.n), f"H2/O2 one-step counterflow flame {args.n}^2 (configs[2])"
-    return (configs.tgv2d(args.n),
+        c = configs.h2o2_counterflow(args.n, nxy=(args.n, args.n * nslabs))
+        return c, f"H2/O2 one-step counterflow flame {args.n}^2 per GPU (configs[2])"
+    return (configs.tgv2d(args.n, ly_periods=nslabs),
             f"TGV 2D {args.n}x{args.n} viscous, TENO6 characteristic, gamma-gas, fixed dt "
             f"(2D analogue of configs[1] TGV 256^3: same {args.n * args.n / 1e6:.1f}M cells; "
             "the reference is 2D-only)")
@@ -186,6 +189,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the NCCL slab path even with one rank (plumbing check)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,12 +211,27 @@ def main():
     torch.cuda.set_device(local)
     from paper_2202_02319_b200 import Simulation, native
 
-    case, workload = make_case(args)
+    slabs = world > 1 or args.force_slabs
+    case, workload = make_case(args, world)
     case.cfg.device = local
+    if slabs:  # one y-slab per rank, halo rows over NCCL
+        case.cfg.slab_count, case.cfg.slab_rank = world, rank
     sim = Simulation(case.cfg)
+    if slabs:
+        import ctypes
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            st = native.api()["nccl_unique_id"](uid)
+            if st != 0:
+                raise RuntimeError("ign_nccl_unique_id failed")
+        t = torch.tensor(list(uid.raw), dtype=torch.uint8, device=f"cuda:{local}")
+        if dist:
+            dist.broadcast(t, 0)
+        raw = bytes(t.cpu().tolist())
+        sim._check(native.api()["attach_nccl"](sim.handle, raw, world, rank))
     sim.set_initial_condition(case.ic)
     sim.prepare_stage(1)
-    cells = case.cfg.nx * case.cfg.ny
+    cells = case.cfg.nx * sim.ny  # this rank's slab
     nc = sim.nc
     stream = torch.cuda.ExternalStream(sim.stream_handle(), device=local)
 
@@ -309,7 +329,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic TGV initial condition)",
             "config": {"workload": workload, "global_batch": world * cells,
-                       "cells_per_gpu": cells, "parallelism": "replicas" if world > 1 else "single",
+                       "cells_per_gpu": cells,
+                       "parallelism": f"y-slabs x{world}, NCCL halo rows" if slabs else "single",
                        "l2": "state 4x538 MB per buffer >> 126 MB L2, no flush needed",
                        "dt": case.dt},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_state,

@@ -53,3 +53,26 @@ def test_slabs_match_single_domain(name, nslabs, cuda_device):
     compare("steps")
     assert bitwise_equal(grp.conserved_totals(), single.conserved_totals())
     grp.close()
+
+
+def test_nccl_single_rank_path(cuda_device):
+    """The NCCL transport (dlopen'ed libnccl, error-word/clip/dt all-reduces,
+    rank folds) with one rank reproduces the plain run bit for bit."""
+    import ctypes
+    from paper_2202_02319_b200 import native
+    case = configs.tgv2d(32)
+    a = Simulation(case.cfg)
+    a.set_initial_condition(case.ic)
+    cfg = configs.tgv2d(32).cfg
+    cfg.slab_count, cfg.slab_rank = 1, 0
+    b = Simulation(cfg)
+    uid = ctypes.create_string_buffer(128)
+    assert native.api()["nccl_unique_id"](uid) == 0
+    b._check(native.api()["attach_nccl"](b.handle, uid.raw, 1, 0))
+    b.set_state(a.Ut)
+    for s in (a, b):
+        s.prepare_stage(1)
+        s.rk3_steps(case.dt, 4)
+    assert bitwise_equal(a.Ut, b.Ut)
+    assert a.stable_dt() == b.stable_dt()
+    assert bitwise_equal(a.conserved_totals(), b.conserved_totals())
