@@ -156,7 +156,14 @@ typedef struct {
      * (ThreadTeam's block split, thread_team.hpp:63-69).  0 or 1 = whole mesh. */
     int32_t slab_count;
     int32_t slab_rank;
+    /* 3D extension (BASELINE configs[1]; no reference path — SURVEY §0):
+     * nz > 0 extrudes the (x, y) mesh uniformly over lz in z.  Component order
+     * then [rhoY_s, rho u, rho v, rho w, E]; primitive cache rho,u,v,w,p,T,c,Y;
+     * periodic boundaries in all directions. */
+    int32_t nz;
+    int32_t periodic_z;
     int32_t _pad;
+    double lz, center_z;
 } ign_config;
 
 /* errors.hpp:29-35 StepFailure payload + message */
@@ -186,6 +193,10 @@ void ign_destroy(ign_context* ctx);
 int ign_last_error(const ign_context* ctx, ign_error* err);
 int ign_dims(const ign_context* ctx, int32_t* nx, int32_t* ny, int32_t* g,
              int32_t* ns);
+/* 3D extension: cells in z (0 for the reference's 2D path).  In 3D the padded
+ * planes are (nx+2g)(ny+2g)(nz+2g), k slowest; set_initial_primitives takes
+ * rho,u,v,w,T,Y_s and get_cache returns rho,u,v,w,p,T,c,Y_s. */
+int ign_dims3(const ign_context* ctx, int32_t* nz);
 
 /* ---- setup / host mirrors --------------------------------------------- */
 /* mesh.x/mesh.y padded arrays (mesh.hpp:295-296) */

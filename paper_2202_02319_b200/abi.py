@@ -111,7 +111,8 @@ class Config(C.Structure):
                 ("viscous", C.c_int32), ("partitions", C.c_int32),
                 ("integ", Integrator),
                 ("device", C.c_int32), ("slab_count", C.c_int32),
-                ("slab_rank", C.c_int32), ("_pad", C.c_int32)]
+                ("slab_rank", C.c_int32), ("nz", C.c_int32), ("periodic_z", C.c_int32),
+                ("_pad", C.c_int32), ("lz", C.c_double), ("center_z", C.c_double)]
 
 
 class Error(C.Structure):
@@ -171,6 +172,7 @@ PRODUCT_ONLY = {
     "profile_read": (_I, [_P, _D, C.POINTER(C.c_int64)]),
     "stream_handle": (C.c_void_p, [_P]),
     "probe_fp64_peak": (_I, [_I, _D]),
+    "dims3": (_I, [_P, _I32P]),
     # multi-GPU slabs
     "nccl_unique_id": (_I, [C.c_char_p]),
     "attach_nccl": (_I, [_P, C.c_char_p, _I, _I]),

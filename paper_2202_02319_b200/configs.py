@@ -8,6 +8,7 @@ primitive arrays ``set_initial_primitives`` takes (rho, u, v, T, Y_s).
 """
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass, field
@@ -369,6 +370,73 @@ def wall_channel(n: int = 48, isothermal: bool = True, scheme: str = "teno6",
         return rho, u, v, T, Ys
 
     return Case(f"wall_{n}", cfg, ic, 0.2 * (L / n) / 450.0)
+
+
+def tgv3d(n: int = 256, *, viscous: bool = True, scheme: str = "teno6",
+          split: str = "char", mach: float = 0.1, mu: float = 6.25e-4,
+          nz=None) -> Case:
+    """BASELINE configs[1]: 3D Taylor-Green vortex on
+    [-pi, pi)^3, periodic, u = sin x cos y cos z, v = -cos x sin y cos z,
+    w = 0, p = p0 + (1/16)(cos 2x + cos 2y)(cos 2z + 2), rho0 = 1, Ma 0.1,
+    Re 1600, gamma-gas with the t_hi cap.  The reference is 2D-only: this runs
+    on the 3D extension (flux3.cuh), validated by the z-extrusion cross-check
+    (extrude_z).  ``nz`` overrides the z cell count with lz scaled so dz stays
+    2 pi / n (weak-scaling stacks)."""
+    L = 2.0 * math.pi
+    cfg = base_config(n, n, L, L)
+    nz = n if nz is None else nz
+    cfg.nz, cfg.periodic_z, cfg.lz, cfg.center_z = nz, 1, L * nz / n, 0.0
+    gamma = 1.4
+    gamma_gas(cfg.mix, gamma, 1.0, mu if viscous else 0.0)
+    set_scheme(cfg, scheme, split)
+    cfg.viscous = int(viscous)
+    p0 = 1.0 / (gamma * mach * mach)
+    c0 = math.sqrt(gamma * p0)
+    dx = L / n
+    # fixed step at CFL 0.5 on the inviscid 3D bound (|u|+|v|+|w| + sqrt3 c0 <= 3 + 1.74 c0)
+    dt = 0.5 * dx / (3.0 + math.sqrt(3.0) * c0)
+
+    def ic(X, Y, Z):
+        u = np.sin(X) * np.cos(Y) * np.cos(Z)
+        v = -np.cos(X) * np.sin(Y) * np.cos(Z)
+        w = np.zeros_like(X)
+        p = p0 + (1.0 / 16.0) * (np.cos(2.0 * X) + np.cos(2.0 * Y)) * (np.cos(2.0 * Z) + 2.0)
+        rho = np.ones_like(X)
+        return rho, u, v, w, p / rho, [np.ones_like(X)]
+
+    return Case(f"tgv3d_{n}" if nz == n else f"tgv3d_{n}x{n}x{nz}", cfg, ic, dt,
+                dict(p0=p0, c0=c0))
+
+
+def extrude_z(case: Case, nz: int = 7) -> Case:
+    """The z-extrusion cross-check of SURVEY §8c: a 2D periodic case on the 3D
+    path with nz >= 2g+1 planes, dz = 1.0 exactly (lz = nz), w = 0 and data
+    constant in z.  Its state must reproduce the 2D oracle's plane for plane."""
+    cfg = abi.Config()
+    ctypes.memmove(ctypes.byref(cfg), ctypes.byref(case.cfg), ctypes.sizeof(abi.Config))
+    cfg.nz, cfg.periodic_z, cfg.lz, cfg.center_z = nz, 1, float(nz), 0.0
+    ic2 = case.ic
+
+    def ic(X, Y, Z):
+        rho, u, v, T, Ys = ic2(X, Y)
+        return rho, u, v, np.zeros_like(X), T, Ys
+
+    return Case(case.name + f"_z{nz}", cfg, ic, case.dt, dict(case.notes, ic2=ic2))
+
+
+def state_2d_to_3d(Ut2: np.ndarray, ns: int, nz: int, g: int = 3) -> np.ndarray:
+    """[rhoY_s, rho u, rho v, E] planes -> [rhoY_s, rho u, rho v, rho w = 0, E]
+    replicated over nz + 2g z planes."""
+    nc2 = Ut2.shape[0]
+    out = np.zeros((nc2 + 1, nz + 2 * g) + Ut2.shape[1:])
+    out[: ns + 2] = Ut2[: ns + 2][:, None]
+    out[ns + 3] = Ut2[ns + 2][None]
+    return out
+
+
+def state_3d_to_2d(Ut3: np.ndarray, ns: int, k: int) -> np.ndarray:
+    """One z plane (padded index k) of a 3D state in the 2D component order."""
+    return np.concatenate([Ut3[: ns + 2, k], Ut3[ns + 3: ns + 4, k]])
 
 
 def padded_coords(cfg: abi.Config):

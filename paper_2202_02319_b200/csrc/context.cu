@@ -31,6 +31,7 @@
 
 #include "host_core.hpp"
 #include "ignis_b200.h"
+#include "flux3.cuh"
 #include "kernels.cuh"
 
 namespace ign {
@@ -42,6 +43,28 @@ KernelSet kernel_set_5();
 KernelSet kernel_set_6();
 KernelSet kernel_set_7();
 KernelSet kernel_set_8();
+
+KernelSet kernel_set3_1();
+KernelSet kernel_set3_2();
+KernelSet kernel_set3_3();
+KernelSet kernel_set3_4();
+KernelSet kernel_set3_5();
+KernelSet kernel_set3_6();
+KernelSet kernel_set3_7();
+KernelSet kernel_set3_8();
+
+KernelSet kernel_set3(int ns) {
+    switch (ns) {
+    case 1: return kernel_set3_1();
+    case 2: return kernel_set3_2();
+    case 3: return kernel_set3_3();
+    case 4: return kernel_set3_4();
+    case 5: return kernel_set3_5();
+    case 6: return kernel_set3_6();
+    case 7: return kernel_set3_7();
+    default: return kernel_set3_8();
+    }
+}
 
 KernelSet kernel_set(int ns) {
     switch (ns) {
@@ -76,6 +99,8 @@ struct ign_context {
     double* prim = nullptr;
     double* geom = nullptr;  // met(5), met_v(5), mesh x, y
     double *Fx = nullptr, *Gy = nullptr, *Fv = nullptr, *Gv = nullptr, *rhs = nullptr;
+    double *Hz = nullptr, *Hv = nullptr;  // 3D extension
+    int nz = 0;                           // 0: 2D (the reference), > 0: 3D extension
     double* inflow[4] = {nullptr, nullptr, nullptr, nullptr};
     double* wrap[2] = {nullptr, nullptr};
     ErrRec* err = nullptr;      // the word the kernels report into
@@ -660,9 +685,12 @@ void t_conserved_totals(const Team& T, double* tot) {
             cuda_check(cudaMemcpy(U.data(), c->S[c->cur] + comp * P, P * 8, cudaMemcpyDeviceToHost),
                        "totals");
             const int sx = c->nx + 2 * c->g, g = c->g;
+            const size_t sxy = size_t(sx) * (c->ny + 2 * g);
             double s = a[0];
-            for (int j = 0; j < c->ny; ++j)
-                for (int i = 0; i < c->nx; ++i) s += U[(size_t)(j + g) * sx + (i + g)];
+            for (int k = 0; k < (c->nz > 0 ? c->nz : 1); ++k)  // 3D: z-planes outermost
+                for (int j = 0; j < c->ny; ++j)
+                    for (int i = 0; i < c->nx; ++i)
+                        s += U[(c->nz > 0 ? (k + g) * sxy : 0) + (size_t)(j + g) * sx + (i + g)];
             a[0] = s;
         });
         tot[comp] = a1[0];
@@ -683,14 +711,18 @@ double t_product_fraction(const Team& T) {
     fold_ranks(T, acc, [&](ign_context* c, std::vector<double>& a) {
         const size_t P = c->plane;
         std::vector<double> Y(c->ns * P);
-        cuda_check(cudaMemcpy(Y.data(), c->prim + 6 * P, Y.size() * 8, cudaMemcpyDeviceToHost),
+        cuda_check(cudaMemcpy(Y.data(), c->prim + (c->nz > 0 ? 7 : 6) * P, Y.size() * 8,
+                              cudaMemcpyDeviceToHost),
                    "Y readback");
         const DMix& m = c->kp.mix;
         const int sx = c->nx + 2 * c->g, g = c->g;
+        const size_t sxy = size_t(sx) * (c->ny + 2 * g);
         double num = a[0], den = a[1];
+        for (int kz = 0; kz < (c->nz > 0 ? c->nz : 1); ++kz)
         for (int j = 0; j < c->ny; ++j)
             for (int i = 0; i < c->nx; ++i) {
-                const size_t id = (size_t)(j + g) * sx + (i + g);
+                const size_t id =
+                    (c->nz > 0 ? (kz + g) * sxy : 0) + (size_t)(j + g) * sx + (i + g);
                 double y[kMaxSpecies], x[kMaxSpecies];
                 for (int s = 0; s < c->ns; ++s) y[s] = Y[s * P + id];
                 double inv = 0.0;
@@ -768,6 +800,32 @@ void cons_from_prim(const DMix& m, double rho, double u, double v, double T, con
     }
 }
 
+template <int NS>
+void cons_from_prim3_t(const DMix& m, const Prim3<kMaxSpecies>& in, const double* Y, double* U) {
+    Prim3<NS> pt;
+    pt.rho = in.rho;
+    pt.u = in.u;
+    pt.v = in.v;
+    pt.w = in.w;
+    pt.T = in.T;
+    pt.p = 0.0;
+    for (int s = 0; s < NS; ++s) pt.Y[s] = Y[s];
+    conservative_from_primitives3<NS>(pt, m, U);
+}
+
+void cons_from_prim3(const DMix& m, const Prim3<kMaxSpecies>& pt, const double* Y, double* U) {
+    switch (m.ns) {
+    case 1: return cons_from_prim3_t<1>(m, pt, Y, U);
+    case 2: return cons_from_prim3_t<2>(m, pt, Y, U);
+    case 3: return cons_from_prim3_t<3>(m, pt, Y, U);
+    case 4: return cons_from_prim3_t<4>(m, pt, Y, U);
+    case 5: return cons_from_prim3_t<5>(m, pt, Y, U);
+    case 6: return cons_from_prim3_t<6>(m, pt, Y, U);
+    case 7: return cons_from_prim3_t<7>(m, pt, Y, U);
+    default: return cons_from_prim3_t<8>(m, pt, Y, U);
+    }
+}
+
 void upload_state(ign_context* ctx, const std::vector<double>& Ut) {
     cuda_check(cudaMemcpy(ctx->S[ctx->cur], Ut.data(), Ut.size() * sizeof(double),
                           cudaMemcpyHostToDevice),
@@ -783,6 +841,8 @@ void destroy_impl(ign_context* ctx) {
     cudaFree(ctx->Gy);
     cudaFree(ctx->Fv);
     cudaFree(ctx->Gv);
+    cudaFree(ctx->Hz);
+    cudaFree(ctx->Hv);
     cudaFree(ctx->rhs);
     for (double* p : ctx->inflow) cudaFree(p);
     for (double* p : ctx->wrap) cudaFree(p);
@@ -814,7 +874,40 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->met = compute_metrics(ctx->mesh, imode, cfg->skew_beta);
     ctx->metv = compute_metrics(ctx->mesh, MM_CENTRAL2, 0.0);
     ctx->integ = cfg->integ;
-    const int nx = cfg->nx, ny = ctx->mesh.ny, g = cfg->g, ns = cfg->mix.ns, nc = ns + 3;
+    const int nz = cfg->nz > 0 ? cfg->nz : 0;
+    ctx->nz = nz;
+    std::vector<double> mzz, vmzz;
+    if (nz > 0) {
+        // 3D extension: the (x, y) mesh extruded over lz (flux3.cuh)
+        if (nz < 2 * cfg->g + 1) throw config_error("3D: nz must be >= 2g+1");
+        if (!(cfg->lz > 0.0)) throw config_error("3D: lz must be positive");
+        if (ctx->nranks > 1) throw usage_error("3D: slab decomposition is 2D-only for now");
+        if (!cfg->periodic_x || !cfg->periodic_y || !cfg->periodic_z)
+            throw usage_error("3D: only periodic boundaries are supported");
+        if (cfg->laser.present && cfg->laser.energy != 0.0)
+            throw usage_error("3D: the laser source has no 3D form in the reference");
+        const double dz = cfg->lz / nz;
+        // cofactor metrics of (x(i,j), y(i,j), z(k)): xi/eta rows scale by z_zeta
+        // = dz, zeta row is the 2D area, J = 1/(area dz) — for dz = 1 every value
+        // is the 2D one bit for bit (the z-extrusion cross-check)
+        auto extrude = [&](HMetrics& m, std::vector<double>& zz) {
+            zz.resize(m.jac.d.size());
+            for (size_t q = 0; q < zz.size(); ++q) {
+                const double area =
+                    m.m_eta_y.d[q] * m.m_xi_x.d[q] - (-m.m_xi_y.d[q]) * (-m.m_eta_x.d[q]);
+                zz[q] = area;
+                m.jac.d[q] = 1.0 / (area * dz);
+                m.m_xi_x.d[q] *= dz;
+                m.m_xi_y.d[q] *= dz;
+                m.m_eta_x.d[q] *= dz;
+                m.m_eta_y.d[q] *= dz;
+            }
+        };
+        extrude(ctx->met, mzz);
+        extrude(ctx->metv, vmzz);
+    }
+    const int nx = cfg->nx, ny = ctx->mesh.ny, g = cfg->g, ns = cfg->mix.ns,
+              nc = ns + (nz > 0 ? 4 : 3);
     const int N = ctx->nranks, r = ctx->rank;
     const bool py = cfg->periodic_y != 0;
     if (N > 1) {
@@ -826,7 +919,8 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->g = g;
     ctx->ns = ns;
     ctx->nc = nc;
-    const size_t P = static_cast<size_t>(nx + 2 * g) * (ny + 2 * g);
+    const size_t P2 = static_cast<size_t>(nx + 2 * g) * (ny + 2 * g);  // one (x, y) plane
+    const size_t P = P2 * (nz > 0 ? nz + 2 * g : 1);
     ctx->plane = P;
     cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
     ctx->stream = ctx->own_stream;
@@ -834,32 +928,38 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
         s = dalloc(nc * P);
         cuda_check(cudaMemset(s, 0, nc * P * sizeof(double)), "memset");
     }
-    // primitive cache: rho,u,v,p = 0, T = c = 1 (solver.hpp:94-100), Y, X
-    const size_t nprim = 6 + 2 * static_cast<size_t>(ns);
+    // primitive cache: rho,u,v,(w),p = 0, T = c = 1 (solver.hpp:94-100), Y, X
+    const size_t head = nz > 0 ? 7 : 6;
+    const size_t nprim = head + 2 * static_cast<size_t>(ns);
     ctx->prim = dalloc(nprim * P);
     {
         std::vector<double> init(nprim * P, 0.0);
-        std::fill(init.begin() + 4 * P, init.begin() + 6 * P, 1.0);
+        std::fill(init.begin() + (head - 2) * P, init.begin() + head * P, 1.0);
         cuda_check(cudaMemcpy(ctx->prim, init.data(), init.size() * sizeof(double),
                               cudaMemcpyHostToDevice),
                    "cache init");
     }
-    ctx->geom = dalloc(12 * P);
+    ctx->geom = dalloc(12 * P2);
     {
-        const HField* f[12] = {&ctx->met.jac,  &ctx->met.m_xi_x,  &ctx->met.m_xi_y,
-                               &ctx->met.m_eta_x, &ctx->met.m_eta_y, &ctx->metv.jac,
-                               &ctx->metv.m_xi_x, &ctx->metv.m_xi_y, &ctx->metv.m_eta_x,
-                               &ctx->metv.m_eta_y, &ctx->mesh.x,   &ctx->mesh.y};
+        // 2D: mesh x, y in slots 10, 11 (laser); 3D: the zeta metrics there
+        const std::vector<double>* f[12] = {
+            &ctx->met.jac.d,    &ctx->met.m_xi_x.d,  &ctx->met.m_xi_y.d,  &ctx->met.m_eta_x.d,
+            &ctx->met.m_eta_y.d, &ctx->metv.jac.d,   &ctx->metv.m_xi_x.d, &ctx->metv.m_xi_y.d,
+            &ctx->metv.m_eta_x.d, &ctx->metv.m_eta_y.d, nz > 0 ? &mzz : &ctx->mesh.x.d,
+            nz > 0 ? &vmzz : &ctx->mesh.y.d};
         for (int k = 0; k < 12; ++k)
-            cuda_check(cudaMemcpy(ctx->geom + k * P, f[k]->d.data(), P * sizeof(double),
+            cuda_check(cudaMemcpy(ctx->geom + k * P2, f[k]->data(), P2 * sizeof(double),
                                   cudaMemcpyHostToDevice),
                        "geometry upload");
     }
-    ctx->Fx = dalloc(static_cast<size_t>(nc) * (nx + 1) * ny);
-    ctx->Gy = dalloc(static_cast<size_t>(nc) * nx * (ny + 1));
+    const size_t nzc = nz > 0 ? nz : 1;
+    ctx->Fx = dalloc(static_cast<size_t>(nc) * (nx + 1) * ny * nzc);
+    ctx->Gy = dalloc(static_cast<size_t>(nc) * nx * (ny + 1) * nzc);
+    if (nz > 0) ctx->Hz = dalloc(static_cast<size_t>(nc) * nx * ny * (nz + 1));
     if (cfg->viscous) {
         ctx->Fv = dalloc(nc * P);
         ctx->Gv = dalloc(nc * P);
+        if (nz > 0) ctx->Hv = dalloc(nc * P);
     }
     // inflow profile tables (boundary.hpp:227-241 ghost targets)
     const ign_edge* edges[4] = {&cfg->bc.left, &cfg->bc.right, &cfg->bc.bottom, &cfg->bc.top};
@@ -957,27 +1057,37 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     k.chem_dt_factor = cfg->integ.chem_dt_factor;
     k.prim = ctx->prim;
     k.jac = ctx->geom;
-    k.mxx = ctx->geom + P;
-    k.mxy = ctx->geom + 2 * P;
-    k.mex = ctx->geom + 3 * P;
-    k.mey = ctx->geom + 4 * P;
-    k.vjac = ctx->geom + 5 * P;
-    k.vmxx = ctx->geom + 6 * P;
-    k.vmxy = ctx->geom + 7 * P;
-    k.vmex = ctx->geom + 8 * P;
-    k.vmey = ctx->geom + 9 * P;
-    k.xc = ctx->geom + 10 * P;
-    k.yc = ctx->geom + 11 * P;
+    k.mxx = ctx->geom + P2;
+    k.mxy = ctx->geom + 2 * P2;
+    k.mex = ctx->geom + 3 * P2;
+    k.mey = ctx->geom + 4 * P2;
+    k.vjac = ctx->geom + 5 * P2;
+    k.vmxx = ctx->geom + 6 * P2;
+    k.vmxy = ctx->geom + 7 * P2;
+    k.vmex = ctx->geom + 8 * P2;
+    k.vmey = ctx->geom + 9 * P2;
+    if (nz > 0) {
+        k.mzz = ctx->geom + 10 * P2;
+        k.vmzz = ctx->geom + 11 * P2;
+    } else {
+        k.xc = ctx->geom + 10 * P2;
+        k.yc = ctx->geom + 11 * P2;
+    }
+    k.nz = nz;
+    k.nz_glob = nz;
+    k.sxy = static_cast<long long>(P2);
     k.Fx = ctx->Fx;
     k.Gy = ctx->Gy;
+    k.Hz = ctx->Hz;
     k.Fv = ctx->Fv;
     k.Gv = ctx->Gv;
+    k.Hv = ctx->Hv;
     k.err = ctx->err;
     k.red = ctx->red;
     k.mix = build_mix(cfg->mix);
     k.mech = build_mech(cfg->mech);
     k.laser = build_laser(cfg->laser);
-    ctx->ks = kernel_set(ns);
+    ctx->ks = nz > 0 ? kernel_set3(ns) : kernel_set(ns);
 }
 
 void copy_hfield(const HField& f, double* out) { std::memcpy(out, f.d.data(), f.d.size() * 8); }
@@ -1062,13 +1172,20 @@ int ign_get_mesh(const ign_context* ctx, double* x, double* y) {
     return IGN_OK;
 }
 
+int ign_dims3(const ign_context* ctx, int32_t* nz) {
+    *nz = ctx->nz;
+    return IGN_OK;
+}
+
 int ign_get_metrics(const ign_context* ctx, int which, double* out) {
-    metrics_out(which == 0 ? ctx->met : ctx->metv, out, ctx->plane);
+    const HMetrics& m = which == 0 ? ctx->met : ctx->metv;
+    metrics_out(m, out, m.jac.d.size());
     return IGN_OK;
 }
 
 int ign_set_initial_condition(ign_context* ctx, ign_ic_fn fn, void* user) {
     return guarded_err(&ctx->lasterr, ctx->device, [&] {
+        if (ctx->nz > 0) throw usage_error("3D: use ign_set_initial_primitives");
         const int g = ctx->g, nc = ctx->nc;
         const size_t P = ctx->plane;
         std::vector<double> Ut(nc * P);
@@ -1089,15 +1206,27 @@ int ign_set_initial_condition(ign_context* ctx, ign_ic_fn fn, void* user) {
 int ign_set_initial_primitives(ign_context* ctx, const double* prim) {
     return guarded_err(&ctx->lasterr, ctx->device, [&] {
         const int ns = ctx->ns, nc = ctx->nc;
-        const size_t P = ctx->plane;
+        const size_t P = ctx->plane, P2 = ctx->met.jac.d.size();
         std::vector<double> Ut(nc * P);
         for (size_t k = 0; k < P; ++k) {
-            double Y[kMaxSpecies];
-            for (int s = 0; s < ns; ++s) Y[s] = prim[(4 + s) * P + k];
-            double U[kMaxComp];
-            cons_from_prim(ctx->kp.mix, prim[k], prim[P + k], prim[2 * P + k], prim[3 * P + k], Y,
-                           U);
-            const double invJ = 1.0 / ctx->met.jac.d[k];
+            double U[kMaxComp + 1];
+            if (ctx->nz > 0) {  // rho, u, v, w, T, Y_s
+                Prim3<kMaxSpecies> pt{};
+                pt.rho = prim[k];
+                pt.u = prim[P + k];
+                pt.v = prim[2 * P + k];
+                pt.w = prim[3 * P + k];
+                pt.T = prim[4 * P + k];
+                double Y[kMaxSpecies];
+                for (int s = 0; s < ns; ++s) Y[s] = prim[(5 + s) * P + k];
+                cons_from_prim3(ctx->kp.mix, pt, Y, U);
+            } else {
+                double Y[kMaxSpecies];
+                for (int s = 0; s < ns; ++s) Y[s] = prim[(4 + s) * P + k];
+                cons_from_prim(ctx->kp.mix, prim[k], prim[P + k], prim[2 * P + k],
+                               prim[3 * P + k], Y, U);
+            }
+            const double invJ = 1.0 / ctx->met.jac.d[k % P2];
             for (int c = 0; c < nc; ++c) Ut[c * P + k] = U[c] * invJ;
         }
         upload_state(ctx, Ut);
@@ -1110,7 +1239,8 @@ int ign_set_state(ign_context* ctx, const double* Ut, const double* Tc) {
                               cudaMemcpyHostToDevice),
                    "set_state");
         if (Tc)
-            cuda_check(cudaMemcpy(ctx->prim + 4 * ctx->plane, Tc, ctx->plane * sizeof(double),
+            cuda_check(cudaMemcpy(ctx->prim + (ctx->nz > 0 ? 5 : 4) * ctx->plane, Tc,
+                                  ctx->plane * sizeof(double),
                                   cudaMemcpyHostToDevice),
                        "set_state T");
     });
@@ -1126,7 +1256,8 @@ int ign_get_state(ign_context* ctx, double* Ut) {
 
 int ign_get_cache(ign_context* ctx, double* prim) {
     return guarded_err(&ctx->lasterr, ctx->device, [&] {
-        cuda_check(cudaMemcpy(prim, ctx->prim, (6 + ctx->ns) * ctx->plane * sizeof(double),
+        cuda_check(cudaMemcpy(prim, ctx->prim,
+                              ((ctx->nz > 0 ? 7 : 6) + ctx->ns) * ctx->plane * sizeof(double),
                               cudaMemcpyDeviceToHost),
                    "get_cache");
     });

@@ -1,0 +1,392 @@
+// faces3d.cuh — inviscid face fluxes of the 3D extension (extruded meshes,
+// flux3.cuh).  Same CTA organisation as faces.cuh: NC = ns+4 warps own
+// 32*NC faces (x: along a row; y/z: 32 columns x NC face lines), the node
+// window lives in shared memory, warp w evaluates characteristic field w.
+#pragma once
+
+#include "flux3.cuh"
+#include "kernels_common.cuh"
+
+namespace ign {
+
+// 3D addressing helpers (state planes: (nx+2g)(ny+2g)(nz+2g), i fastest;
+// metric planes are 2D: the mesh is extruded in z)
+__device__ __forceinline__ long long pidx3(const KParams& P, int i, int j, int k) {
+    return (long long)(k + P.g) * P.sxy + (long long)(j + P.g) * P.sx + (i + P.g);
+}
+
+template <int NS, int DIR, bool TENO> struct FaceSmem3 {
+    static constexpr int NC = NS + 4;
+    static constexpr int H = TENO ? 3 : 2;
+    static constexpr int W = 2 * H;
+    static constexpr int NF = 32 * NC;
+    static constexpr int NT = DIR == 0 ? NF + W - 1 : 32 * (NC + W - 1);
+    static constexpr int NE = 17 + 2 * NS;
+    static constexpr int NV = 2 * W;
+    double U[NC][NT];
+    double F[NC][NT];
+    double u[NT], v[NT], w[NT], c[NT];
+    double E[NE][NF];
+    double L[NV][4][32];  // dp, dun, dut1, dut2
+    double amp[NC][NF];
+    int bad[NF];
+};
+
+enum : int {
+    F3N1 = 0, F3N2, F3N3, F3S, F3U, F3V, F3W, F3UN, F3UT1, F3UT2, F3K, F3H, F3C, F3C2, F3KAPPA,
+    F3YC2, F3YKAPPA, F3Y0
+};
+
+template <int DIR> __device__ __forceinline__ int tile_node3(int g, int lane, int k) {
+    return DIR == 0 ? g * 32 + lane + k : (g + k) * 32 + lane;
+}
+
+template <int NS, int DIR, bool TENO, bool CHAR>
+__global__ void __launch_bounds__(32 * (NS + 4))
+k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {
+    using Smem = FaceSmem3<NS, DIR, TENO>;
+    constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
+    constexpr int NV = Smem::NV;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    __shared__ int s_dead;
+    if (threadIdx.x == 0) s_dead = failed(P.err);
+    __syncthreads();
+    if (s_dead) return;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // DIR 0: faces along i of row (j, k); DIR 1: columns i, face rows along j,
+    // plane k; DIR 2: columns i, row j, face planes along k
+    const long long step_n = DIR == 0 ? 1 : DIR == 1 ? P.sx : P.sxy;
+    const int nd = DIR == 0 ? P.nx : DIR == 1 ? P.ny : P.nz;  // cells along DIR
+    const int f0 = DIR == 0 ? blockIdx.x * NF : (DIR == 1 ? blockIdx.y : blockIdx.z) * NC;
+    const int i0 = blockIdx.x * 32;
+    const int jb = DIR == 0 ? blockIdx.y : DIR == 1 ? 0 : blockIdx.y;  // fixed j (DIR 0, 2)
+    const int kb = DIR == 2 ? 0 : blockIdx.z;                          // fixed k (DIR 0, 1)
+    // metric planes: xi (DIR 0) / eta (DIR 1) use (m_x, m_y); zeta uses m_zz
+    const double* m1a = DIR == 0 ? P.mxx : DIR == 1 ? P.mex : P.mzz;
+    const double* m2a = DIR == 0 ? P.mxy : DIR == 1 ? P.mey : P.mzz;
+    auto node = [&](int a, int col) -> long long {  // a = index along DIR, col = i
+        if (DIR == 0) return pidx3(P, a, jb, kb);
+        if (DIR == 1) return pidx3(P, col, a, kb);
+        return pidx3(P, col, jb, a);
+    };
+
+    // ---------------- phase 1a: node window -> shared memory
+    for (int t = threadIdx.x; t < NT; t += blockDim.x) {
+        int a, col;
+        bool ok;
+        if (DIR == 0) {
+            a = f0 - H + t;
+            col = 0;
+            ok = a < P.nx + P.g;
+        } else {
+            a = f0 - H + t / 32;
+            col = i0 + t % 32;
+            ok = col < P.nx && a < nd + P.g;
+        }
+        if (!ok) continue;
+        const long long id = node(a, col);
+        const long long id2 = id % P.sxy;
+        const double J = ldg(P.jac + id2);
+        double Uk[NC], Fk[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
+        mapped_flux3<NS, DIR>(Uk, ldg(PP3(P) + id), ldg(m1a + id2), ldg(m2a + id2), Fk);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            S.U[c][t] = Uk[c];
+            S.F[c][t] = Fk[c];
+        }
+        S.u[t] = ldg(PU3(P) + id);
+        S.v[t] = ldg(PV3(P) + id);
+        S.w[t] = ldg(PW3(P) + id);
+        S.c[t] = ldg(PC3(P) + id);
+    }
+
+    const int my_f = DIR == 0 ? f0 + threadIdx.x : f0 + warp;
+    const int my_col = DIR == 0 ? 0 : i0 + lane;
+    const bool my_active = DIR == 0 ? my_f <= P.nx : (my_col < P.nx && my_f <= nd);
+    const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;  // z faces share the y code
+    auto err_index = [&](int f, int col) -> unsigned long long {
+        // face (f) of the line through (col/jb, kb): global line-major order
+        if (DIR == 0)
+            return ((unsigned long long)(kb + P.j0) * P.ny + jb) * (P.nx + 1) + f;
+        if (DIR == 1)
+            return ((unsigned long long)(kb + P.j0) * P.nx + col) * (P.ny + 1) + f;
+        return ((unsigned long long)jb * P.nx + col) * (P.nz_glob + 1) + (f + P.j0);
+    };
+    const long long il = node(my_f - 1, my_col), ir = il + step_n;
+    double m1f = 0.0, m2f = 0.0;
+    if (my_active) {
+        const long long l2 = il % P.sxy, r2 = ir % P.sxy;
+        m1f = 0.5 * (ldg(m1a + l2) + ldg(m1a + r2));
+        m2f = 0.5 * (ldg(m2a + l2) + ldg(m2a + r2));
+    }
+
+    if (CHAR) {
+        int bad = 0;
+        if (my_active) {
+            double Yl[NS], Yr[NS], Ya[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                Yl[s] = ldg(PY3(P, s) + il);
+                Yr[s] = ldg(PY3(P, s) + ir);
+            }
+            double Ta, ua, va, wa;
+            roe_average3<NS>(ldg(PRHO3(P) + il), Yl, ldg(PT3(P) + il), ldg(PU3(P) + il),
+                             ldg(PV3(P) + il), ldg(PW3(P) + il), ldg(PRHO3(P) + ir), Yr,
+                             ldg(PT3(P) + ir), ldg(PU3(P) + ir), ldg(PV3(P) + ir),
+                             ldg(PW3(P) + ir), P.mix, Ya, Ta, ua, va, wa);
+            Eigen3<NS> es;
+            const int est = eigen_at_state3<NS, DIR == 2 ? 2 : 0>(Ya, Ta, ua, va, wa, m1f, m2f,
+                                                                  P.mix, es);
+            if (est) {
+                report(P.err, stage, phase, err_index(my_f, my_col), 1 + est, step);
+                bad = 1;
+            }
+            const int t = threadIdx.x;
+            const double vals[F3Y0] = {es.n1, es.n2,  es.n3,  es.s, es.u,  es.v,
+                                       es.w,  es.un,  es.ut1, es.ut2, es.k, es.H,
+                                       es.c,  es.c2,  es.kappa, es.yc2, es.ykappa};
+#pragma unroll
+            for (int q = 0; q < F3Y0; ++q) S.E[q][t] = vals[q];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                S.E[F3Y0 + s][t] = es.Y[s];
+                S.E[F3Y0 + NS + s][t] = es.Theta[s];
+            }
+        }
+        S.bad[threadIdx.x] = my_active ? bad : 1;
+    }
+    __syncthreads();
+    if (!CHAR) {
+        // componentwise LLF wave speed (solver.hpp:537-548), 3D normal velocity
+        int bad = 1;
+        if (my_active) {
+            const double sf = DIR < 2 ? ghypot(m1f, m2f) : ghypot(m1f, 0.0);
+            double alpha = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node3<DIR>(warp, lane, k);
+                const double un = DIR < 2 ? (m1f * S.u[t] + m2f * S.v[t]) / sf
+                                          : (m1f * S.w[t]) / sf;
+                alpha = smax(alpha, sf * (fabs(un) + S.c[t]));
+            }
+            bad = 0;
+            if (!isfinite(alpha)) {
+                report(P.err, stage, phase, err_index(my_f, my_col), 1, step);
+                bad = 1;
+            }
+            S.E[0][threadIdx.x] = alpha;
+        }
+        S.bad[threadIdx.x] = bad;
+        __syncthreads();
+    }
+
+    double* out = DIR == 0 ? P.Fx : DIR == 1 ? P.Gy : P.Hz;
+    // face planes: x (nx+1) ny nz, y nx (ny+1) nz, z nx ny (nz+1)
+    const long long fplane = (long long)(P.nx + (DIR == 0)) * (P.ny + (DIR == 1)) *
+                             (P.nz + (DIR == 2));
+    const int fl = warp;
+    for (int g = 0; g < NC; ++g) {
+        const int face = g * 32 + lane;
+        const int f = DIR == 0 ? f0 + face : f0 + g;
+        const int col = DIR == 0 ? 0 : i0 + lane;
+        const bool live = !S.bad[face];
+        long long o;
+        if (DIR == 0) o = ((long long)kb * P.ny + jb) * (P.nx + 1) + f;
+        else if (DIR == 1) o = ((long long)kb * (P.ny + 1) + f) * P.nx + col;
+        else o = ((long long)f * P.ny + jb) * P.nx + col;
+        if (!CHAR) {
+            if (live) {
+                const double alpha = S.E[0][face];
+                double wp[W], wm[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int t = tile_node3<DIR>(g, lane, k);
+                    wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
+                    wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
+                }
+                out[fl * fplane + o] = face_pm<TENO>(wp, wm, P.rp);
+            }
+            continue;
+        }
+        // (a) field-independent parts of L q (flux.hpp:107-114 + z terms)
+        const double kap = S.E[F3KAPPA][face], eu = S.E[F3U][face], ev = S.E[F3V][face],
+                     ew = S.E[F3W][face];
+        const double n1 = S.E[F3N1][face], n2 = S.E[F3N2][face], n3 = S.E[F3N3][face];
+        const double un = S.E[F3UN][face], ut1 = S.E[F3UT1][face], ut2 = S.E[F3UT2][face];
+        for (int vec = warp; vec < NV; vec += NC) {
+            const int k = vec >> 1;
+            const int t = tile_node3<DIR>(g, lane, k);
+            double q[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) q[c] = (vec & 1) ? S.U[c][t] : S.F[c][t];
+            double drho = 0.0;
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp) drho += q[sp];
+            double dp = kap * q[NS + 3] - kap * eu * q[NS] - kap * ev * q[NS + 1] -
+                        kap * ew * q[NS + 2];
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp) dp += S.E[F3Y0 + NS + sp][face] * q[sp];
+            S.L[vec][0][lane] = dp;
+            if (DIR < 2) {
+                S.L[vec][1][lane] = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
+                S.L[vec][2][lane] = -n2 * q[NS] + n1 * q[NS + 1] - ut1 * drho;
+                S.L[vec][3][lane] = q[NS + 2] - ut2 * drho;
+            } else {
+                S.L[vec][1][lane] = n3 * q[NS + 2] - un * drho;
+                S.L[vec][2][lane] = q[NS] - ut1 * drho;
+                S.L[vec][3][lane] = q[NS + 1] - ut2 * drho;
+            }
+        }
+        __syncthreads();
+        // (b) row fl of L, wave speed, LLF split, reconstruction
+        double amp = 0.0;
+        if (live) {
+            const double es = S.E[F3S][face], ec = S.E[F3C][face];
+            const double c2 = S.E[F3C2][face], yc2 = S.E[F3YC2][face];
+            const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
+            const bool ac = fl == 0 || fl == NC - 1;
+            const bool sh1 = fl == NC - 3, sh2 = fl == NC - 2;
+            const int sp_i = (ac || sh1 || sh2) ? 0 : fl - 1;
+            const double sgn = fl == 0 ? -1.0 : 1.0;
+            const double Ys = S.E[F3Y0 + sp_i][face];
+            const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
+            double lf[W], lu[W];
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node3<DIR>(g, lane, k);
+#pragma unroll
+                for (int vu = 0; vu < 2; ++vu) {
+                    const int vec = 2 * k + vu;
+                    const double dp = S.L[vec][0][lane];
+                    const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
+                    const double fd = fdiv_try(num, den, yden, ok);
+                    const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
+                    const double wv = ac    ? fd
+                                      : sh1 ? S.L[vec][2][lane]
+                                      : sh2 ? S.L[vec][3][lane]
+                                            : qs - fd;
+                    if (vu) lu[k] = wv;
+                    else lf[k] = wv;
+                }
+            }
+            if (!(sh1 || sh2) && !ok) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int t = tile_node3<DIR>(g, lane, k);
+#pragma unroll
+                    for (int vu = 0; vu < 2; ++vu) {
+                        const int vec = 2 * k + vu;
+                        const double dp = S.L[vec][0][lane];
+                        const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
+                        const double fd = div_cold(num, den);
+                        const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
+                        const double wv = ac ? fd : qs - fd;
+                        if (vu) lu[k] = wv;
+                        else lf[k] = wv;
+                    }
+                }
+            }
+            double alpha = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node3<DIR>(g, lane, k);
+                const double unk = DIR < 2 ? n1 * S.u[t] + n2 * S.v[t] : n3 * S.w[t];
+                const double ck = S.c[t];
+                const double lam = es * (ac ? unk + sgn * ck : unk);
+                alpha = smax(alpha, fabs(lam));
+            }
+            if (!isfinite(alpha)) {
+                report(P.err, stage, phase, err_index(f, col), 1, step);
+            } else {
+                double wp[W], wm[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    wp[k] = 0.5 * (lf[k] + alpha * lu[k]);
+                    wm[k] = 0.5 * (lf[k] - alpha * lu[k]);
+                }
+                amp = face_pm<TENO>(wp, wm, P.rp);
+            }
+        }
+        S.amp[fl][face] = amp;
+        __syncthreads();
+    }
+    if (!CHAR) return;
+
+    // ---------------- phase 3: component fl of R * amp (flux.hpp:123-139 + z)
+    for (int g = 0; g < NC; ++g) {
+        const int face = g * 32 + lane;
+        if (S.bad[face]) continue;
+        const int f = DIR == 0 ? f0 + face : f0 + g;
+        const int col = DIR == 0 ? 0 : i0 + lane;
+        long long o;
+        if (DIR == 0) o = ((long long)kb * P.ny + jb) * (P.nx + 1) + f;
+        else if (DIR == 1) o = ((long long)kb * (P.ny + 1) + f) * P.nx + col;
+        else o = ((long long)f * P.ny + jb) * P.nx + col;
+        const double am = S.amp[0][face];
+        const double ap = S.amp[NC - 1][face];
+        const double at1 = S.amp[NC - 3][face];
+        const double at2 = S.amp[NC - 2][face];
+        const double c = S.E[F3C][face];
+        const double n1 = S.E[F3N1][face], n2 = S.E[F3N2][face], n3 = S.E[F3N3][face];
+        double r;
+        if (fl < NS) {
+            r = S.E[F3Y0 + fl][face] * (am + ap) + S.amp[1 + fl][face];
+        } else {
+            double asum = 0.0;
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp) asum += S.amp[1 + sp][face];
+            const double u = S.E[F3U][face], v = S.E[F3V][face], w = S.E[F3W][face];
+            if (fl == NS) {  // rho u
+                r = DIR < 2 ? (u - c * n1) * am + (u + c * n1) * ap + u * asum - n2 * at1
+                            : u * am + u * ap + u * asum + at1;
+            } else if (fl == NS + 1) {  // rho v
+                r = DIR < 2 ? (v - c * n2) * am + (v + c * n2) * ap + v * asum + n1 * at1
+                            : v * am + v * ap + v * asum + at2;
+            } else if (fl == NS + 2) {  // rho w
+                r = DIR < 2 ? w * am + w * ap + w * asum + at2
+                            : (w - c * n3) * am + (w + c * n3) * ap + w * asum;
+            } else {  // E
+                const double Hh = S.E[F3H][face], un = S.E[F3UN][face];
+                const double ut1 = S.E[F3UT1][face], ut2 = S.E[F3UT2][face];
+                const double kk = S.E[F3K][face], kappa = S.E[F3KAPPA][face];
+                const double ykappa = S.E[F3YKAPPA][face];
+                double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut1 * at1;
+                en = en + ut2 * at2;
+#pragma unroll
+                for (int sp = 0; sp < NS; ++sp) {
+                    const double th = S.E[F3Y0 + NS + sp][face];
+                    en += S.amp[1 + sp][face] *
+                          (2.0 * kk - (NS > 1 ? fdiv(th, kappa, ykappa) : th / kappa));
+                }
+                r = en;
+            }
+        }
+        out[fl * fplane + o] = r;
+    }
+}
+
+template <int NS, int DIR, bool TENO, bool CHAR>
+inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int step,
+                           cudaStream_t s) {
+    constexpr int NC = NS + 4;
+    const size_t smem = sizeof(FaceSmem3<NS, DIR, TENO>);
+    auto kern = k_faces3d<NS, DIR, TENO, CHAR>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const int NF = 32 * NC;
+    dim3 grid;
+    if (DIR == 0) grid = dim3((P.nx + 1 + NF - 1) / NF, P.ny, P.nz);
+    else if (DIR == 1) grid = dim3((P.nx + 31) / 32, (P.ny + 1 + NC - 1) / NC, P.nz);
+    else grid = dim3((P.nx + 31) / 32, P.ny, (P.nz + 1 + NC - 1) / NC);
+    kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step);
+}
+
+}  // namespace ign

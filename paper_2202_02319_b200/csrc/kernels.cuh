@@ -516,18 +516,6 @@ __global__ void __launch_bounds__(256) k_dt(const __grid_constant__ KParams P) {
 }
 
 // ---------------------------------------------------------------- launcher table
-struct KernelSet {
-    int (*bc)(const KParams&, double* Ut, int ypass, int stage, int step, cudaStream_t);
-    int (*prim)(const KParams&, const double* Ut, int stage, int step, cudaStream_t);
-    int (*faces)(const KParams&, int teno, int chr, const double* Ut, int stage, int step,
-                 cudaStream_t);
-    int (*visc)(const KParams&, int stage, int step, cudaStream_t);
-    int (*assemble)(const KParams&, int mode, const double* U0, const double* Ucur,
-                    double* Uout, double dt, double w, double t_stage, int stage, int step,
-                    int clip_slot, cudaStream_t);
-    int (*dt)(const KParams&, cudaStream_t);
-};
-
 template <int NS> struct Launch {
     // one ghost-fill pass: x edges over rows 0..ny-1 (ypass 0) or y edges over
     // the full padded width (ypass 1) — boundary.hpp:254-257

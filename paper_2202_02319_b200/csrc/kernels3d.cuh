@@ -1,0 +1,410 @@
+// kernels3d.cuh — stage kernels of the 3D extension (BASELINE configs[1],
+// TGV 256^3).  The reference is 2D-only; these kernels extend each 2D kernel
+// (kernels.cuh) by the z terms on EXTRUDED meshes (2D reference metrics x
+// uniform z, flux3.cuh), appended after the reference's 2D expressions so the
+// z-extrusion cross-check reproduces the 2D oracle bit for bit.  Boundary
+// conditions: periodic in x, y, z (the TGV); other BCs are 2D-only for now.
+#pragma once
+
+#include "faces3d.cuh"
+#include "flux3.cuh"
+#include "kernels_common.cuh"
+
+namespace ign {
+
+// ---------------------------------------------------------------- ghost fill
+// periodic copies (boundary.hpp:146-149, 203-209) pass by pass: x over the
+// interior (j, k), y over all i and interior k, z over all (i, j)
+template <int NS>
+__global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, double* Ut,
+                                             int pass) {
+    if (failed(P.err)) return;
+    const int g = P.g;
+    const int na = pass == 0 ? P.ny : P.nx + 2 * g;        // first transverse index
+    const int nb = pass == 2 ? P.ny + 2 * g : P.nz;       // second
+    const int a0 = pass == 0 ? 0 : -g, b0 = pass == 2 ? -g : 0;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= 2LL * na * nb) return;
+    const int side = (int)(tid / ((long long)na * nb));
+    const long long rem = tid % ((long long)na * nb);
+    const int a = a0 + (int)(rem % na), b = b0 + (int)(rem / na);
+    const int n = pass == 0 ? P.nx : pass == 1 ? P.ny : P.nz;
+    for (int k = 1; k <= g; ++k) {
+        const int sidx = side == 0 ? n - k : k - 1;
+        const int didx = side == 0 ? -k : n - 1 + k;
+        long long s, d;
+        if (pass == 0) {
+            s = pidx3(P, sidx, a, b);
+            d = pidx3(P, didx, a, b);
+        } else if (pass == 1) {
+            s = pidx3(P, a, sidx, b);
+            d = pidx3(P, a, didx, b);
+        } else {
+            s = pidx3(P, a, b, sidx);
+            d = pidx3(P, a, b, didx);
+        }
+        const double ratio = P.jac[s % P.sxy] / P.jac[d % P.sxy];
+#pragma unroll
+        for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+    }
+}
+
+// ---------------------------------------------------------------- primitives
+template <int NS, bool WX>
+__global__ void __launch_bounds__(256) k_prim3(const __grid_constant__ KParams P,
+                                               const double* __restrict__ Ut, int stage,
+                                               int step) {
+    if (failed(P.err)) return;
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= P.plane) return;
+    const double J = P.jac[id % P.sxy];
+    double U[NS + 4];
+#pragma unroll
+    for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
+    Prim3<NS> pt;
+    double rs;
+    const int st = primitives_from_conservative3<NS>(U, P.mix, PT3(P)[id], pt, &rs);
+    if (st) {
+        report(P.err, stage, PH_PRIM, (unsigned long long)(id + (long long)P.j0 * P.sxy), st,
+               step);
+        return;
+    }
+    PRHO3(P)[id] = pt.rho;
+    PU3(P)[id] = pt.u;
+    PV3(P)[id] = pt.v;
+    PW3(P)[id] = pt.w;
+    PP3(P)[id] = pt.p;
+    PT3(P)[id] = pt.T;
+    PC3(P)[id] = sound_speed_rs<NS>(pt.T, pt.Y, rs, P.mix);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) PY3(P, s)[id] = pt.Y[s];
+    if (WX) {
+        double X[NS];
+        mole_fractions<NS>(pt.Y, P.mix, X);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) PX3(P, s)[id] = X[s];
+    }
+}
+
+// ---------------------------------------------------------------- viscous
+// compute_viscous (solver.hpp:610-696) with the z gradient, z stresses and
+// the zeta flux appended after the reference's 2D terms
+template <int NS>
+__global__ void __launch_bounds__(128) k_visc3(const __grid_constant__ KParams P, int stage,
+                                               int step) {
+    constexpr int NC = NS + 4;
+    if (failed(P.err)) return;
+    const long long wx = P.nx + 2, wy = P.ny + 2;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= wx * wy * (P.nz + 2)) return;
+    const int i = (int)(t % wx) - 1, j = (int)((t / wx) % wy) - 1, k = (int)(t / (wx * wy)) - 1;
+    const long long id = pidx3(P, i, j, k), id2 = id % P.sxy;
+    auto ddxi = [&](const double* f) { return 0.5 * (ldg(f + id + 1) - ldg(f + id - 1)); };
+    auto ddeta = [&](const double* f) { return 0.5 * (ldg(f + id + P.sx) - ldg(f + id - P.sx)); };
+    auto ddzeta = [&](const double* f) {
+        return 0.5 * (ldg(f + id + P.sxy) - ldg(f + id - P.sxy));
+    };
+    const double vj = ldg(P.vjac + id2);
+    const double xi_x = ldg(P.vmxx + id2) * vj;
+    const double xi_y = ldg(P.vmxy + id2) * vj;
+    const double eta_x = ldg(P.vmex + id2) * vj;
+    const double eta_y = ldg(P.vmey + id2) * vj;
+    const double zeta_z = ldg(P.vmzz + id2) * vj;
+    auto gradx = [&](const double* f) { return xi_x * ddxi(f) + eta_x * ddeta(f); };
+    auto grady = [&](const double* f) { return xi_y * ddxi(f) + eta_y * ddeta(f); };
+    auto gradz = [&](const double* f) { return zeta_z * ddzeta(f); };
+    const double ux = gradx(PU3(P)), uy = grady(PU3(P)), uz = gradz(PU3(P));
+    const double vx = gradx(PV3(P)), vy = grady(PV3(P)), vz = gradz(PV3(P));
+    const double wx_ = gradx(PW3(P)), wy_ = grady(PW3(P)), wz = gradz(PW3(P));
+    const double Tx = gradx(PT3(P)), Ty = grady(PT3(P)), Tz = gradz(PT3(P));
+    const double T = ldg(PT3(P) + id), rho = ldg(PRHO3(P) + id);
+    double Y[NS], X[NS], gx[NS], gy[NS], gz[NS], hs[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        Y[s] = ldg(PY3(P, s) + id);
+        X[s] = ldg(PX3(P, s) + id);
+        gx[s] = gradx(PX3(P, s));
+        gy[s] = grady(PX3(P, s));
+        gz[s] = gradz(PX3(P, s));
+        hs[s] = h_species(T, P.mix.sp[s], P.mix.R);
+    }
+    double mu, lambda, D, cp;
+    transport<NS>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
+    const double div = (ux + vy) + wz;
+    const double txx = mu * (2.0 * ux - (2.0 / 3.0) * div);
+    const double tyy = mu * (2.0 * vy - (2.0 / 3.0) * div);
+    const double tzz = mu * (2.0 * wz - (2.0 / 3.0) * div);
+    const double txy = mu * (uy + vx);
+    const double txz = mu * (uz + wx_);
+    const double tyz = mu * (vz + wy_);
+    const double wbar = mean_molar_mass<NS>(Y, P.mix);
+    double ucx = 0.0, ucy = 0.0, ucz = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        ucx += (P.mix.sp[s].W / wbar) * D * gx[s];
+        ucy += (P.mix.sp[s].W / wbar) * D * gy[s];
+        ucz += (P.mix.sp[s].W / wbar) * D * gz[s];
+    }
+    double ex = lambda * Tx, ey = lambda * Ty, ez = lambda * Tz;
+    double Fd[NC], Gd[NC], Hd[NC];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const double jsx = rho * ((P.mix.sp[s].W / wbar) * D * gx[s] - Y[s] * ucx);
+        const double jsy = rho * ((P.mix.sp[s].W / wbar) * D * gy[s] - Y[s] * ucy);
+        const double jsz = rho * ((P.mix.sp[s].W / wbar) * D * gz[s] - Y[s] * ucz);
+        ex += jsx * hs[s];
+        ey += jsy * hs[s];
+        ez += jsz * hs[s];
+        Fd[s] = jsx;
+        Gd[s] = jsy;
+        Hd[s] = jsz;
+    }
+    const double u = ldg(PU3(P) + id), v = ldg(PV3(P) + id), w = ldg(PW3(P) + id);
+    Fd[NS] = txx;
+    Fd[NS + 1] = txy;
+    Fd[NS + 2] = txz;
+    Fd[NS + 3] = ((u * txx + v * txy) + w * txz) + ex;
+    Gd[NS] = txy;
+    Gd[NS + 1] = tyy;
+    Gd[NS + 2] = tyz;
+    Gd[NS + 3] = ((u * txy + v * tyy) + w * tyz) + ey;
+    Hd[NS] = txz;
+    Hd[NS + 1] = tyz;
+    Hd[NS + 2] = tzz;
+    Hd[NS + 3] = ((u * txz + v * tyz) + w * tzz) + ez;
+    const double a = ldg(P.vmxx + id2), b = ldg(P.vmxy + id2);
+    const double c2 = ldg(P.vmex + id2), d = ldg(P.vmey + id2), e = ldg(P.vmzz + id2);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        P.Fv[c * P.plane + id] = a * Fd[c] + b * Gd[c];
+        P.Gv[c * P.plane + id] = c2 * Fd[c] + d * Gd[c];
+        P.Hv[c * P.plane + id] = e * Hd[c];
+    }
+}
+
+// ---------------------------------------------------------------- assemble + update
+template <int NS, int MODE>
+__global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KParams P,
+                                                   const double* __restrict__ U0,
+                                                   const double* __restrict__ Ucur,
+                                                   double* __restrict__ Uout, double dt,
+                                                   double w, double t_stage, int stage,
+                                                   int step, int clip_slot) {
+    constexpr int NC = NS + 4;
+    __shared__ unsigned long long s_clip;
+    if (threadIdx.x == 0) s_clip = 0ull;
+    __syncthreads();
+    const bool dead = failed(P.err);
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double clip = 0.0;
+    if (!dead && id < P.plane) {
+        const int ip = (int)(id % P.sx), jp = (int)((id / P.sx) % (P.ny + 2 * P.g));
+        const int kp = (int)(id / P.sxy);
+        const int i = ip - P.g, j = jp - P.g, k = kp - P.g;
+        const bool interior = i >= 0 && i < P.nx && j >= 0 && j < P.ny && k >= 0 && k < P.nz;
+        if (!interior) {
+            if (MODE != 0) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = Ucur[c * P.plane + id];
+            }
+        } else {
+            const long long fxp = (long long)(P.nx + 1) * P.ny * P.nz;
+            const long long fyp = (long long)P.nx * (P.ny + 1) * P.nz;
+            const long long fzp = (long long)P.nx * P.ny * (P.nz + 1);
+            const long long fx = ((long long)k * P.ny + j) * (P.nx + 1) + i;
+            const long long fy = ((long long)k * (P.ny + 1) + j) * P.nx + i;
+            const long long fz = ((long long)k * P.ny + j) * P.nx + i;
+            double r[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const double dF = P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
+                const double dG = P.Gy[c * fyp + fy + P.nx] - P.Gy[c * fyp + fy];
+                const double dH = P.Hz[c * fzp + fz + (long long)P.nx * P.ny] - P.Hz[c * fzp + fz];
+                r[c] = -((dF + dG) + dH);
+            }
+            if (P.viscous) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double* Fv = P.Fv + c * P.plane;
+                    const double* Gv = P.Gv + c * P.plane;
+                    const double* Hv = P.Hv + c * P.plane;
+                    const double dVx = 0.5 * (Fv[id + 1] - Fv[id - 1]);
+                    const double dVy = 0.5 * (Gv[id + P.sx] - Gv[id - P.sx]);
+                    const double dVz = 0.5 * (Hv[id + P.sxy] - Hv[id - P.sxy]);
+                    r[c] += (dVx + dVy) + dVz;
+                }
+            }
+            const double J = ldg(P.jac + id % P.sxy);
+            const double invJ = 1.0 / J;
+            if (P.mech.present) {
+                double Y[NS], wdot[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) Y[s] = ldg(PY3(P, s) + id);
+                source_terms<NS>(ldg(PRHO3(P) + id), ldg(PT3(P) + id), Y, P.mix, P.mech, wdot);
+#pragma unroll
+                for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
+            }
+            const unsigned long long cell =
+                ((unsigned long long)(k + P.j0) * P.ny + j) * P.nx + i;
+            bool bad = false;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) bad |= !isfinite(r[c]);
+            if (bad) {
+                report(P.err, stage, PH_RHS, cell, 0, step);
+            } else if (MODE == 0) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = r[c];
+            } else {
+                double o[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double b = U0[c * P.plane + id];
+                    if (MODE == 1) o[c] = b + dt * r[c];
+                    else o[c] = b + w * ((Ucur[c * P.plane + id] - b) + dt * r[c]);
+                }
+                double rsum = 0.0;
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    if (o[s] < 0.0) {
+                        clip = smax(clip, -o[s] * J);
+                        o[s] = 0.0;
+                    }
+                    rsum += o[s];
+                }
+                bool fin = true;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) fin &= isfinite(o[c]);
+                if (!(rsum > 0.0)) report(P.err, stage, PH_POST, cell * 2, 0, step);
+                else if (!fin) report(P.err, stage, PH_POST, cell * 2 + 1, 0, step);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = o[c];
+            }
+        }
+    }
+    if (MODE != 0) {
+        if (clip > 0.0) atomicMax(&s_clip, (unsigned long long)__double_as_longlong(clip));
+        __syncthreads();
+        if (threadIdx.x == 0 && s_clip) atomicMax(&P.red[2 + clip_slot], s_clip);
+    }
+}
+
+// ---------------------------------------------------------------- stable dt
+template <int NS>
+__global__ void __launch_bounds__(256) k_dt3(const __grid_constant__ KParams P) {
+    __shared__ unsigned long long s_lam, s_chem;
+    if (threadIdx.x == 0) {
+        s_lam = 0ull;
+        s_chem = 0x7ff0000000000000ull;
+    }
+    __syncthreads();
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double lam_loc = 0.0, chem_loc = __longlong_as_double(0x7ff0000000000000ll);
+    if (t < (long long)P.nx * P.ny * P.nz) {
+        const int i = (int)(t % P.nx), j = (int)((t / P.nx) % P.ny), k = (int)(t / ((long long)P.nx * P.ny));
+        const long long id = pidx3(P, i, j, k), id2 = id % P.sxy;
+        const double J = ldg(P.jac + id2);
+        const double mxx = ldg(P.mxx + id2), mxy = ldg(P.mxy + id2);
+        const double mex = ldg(P.mex + id2), mey = ldg(P.mey + id2), mzz = ldg(P.mzz + id2);
+        const double sx = ghypot(mxx, mxy), sy = ghypot(mex, mey), sz = fabs(mzz);
+        const double u = ldg(PU3(P) + id), v = ldg(PV3(P) + id), w = ldg(PW3(P) + id);
+        const double c = ldg(PC3(P) + id);
+        const double ux = mxx * u + mxy * v, uy = mex * u + mey * v, uz = mzz * w;
+        double lam = ((fabs(ux) + c * sx + fabs(uy) + c * sy) + fabs(uz) + c * sz) * J;
+        double Y[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) Y[s] = ldg(PY3(P, s) + id);
+        const double rho = ldg(PRHO3(P) + id), T = ldg(PT3(P) + id);
+        if (P.viscous) {
+            double X[NS];
+            mole_fractions<NS>(Y, P.mix, X);
+            double mu, lambda, D, cp;
+            transport<NS>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
+            const double nu = smax(2.0 * mu / rho, smax(lambda / (rho * cp), D));
+            lam += 2.0 * nu * ((sx * sx + sy * sy) + sz * sz) * J * J;
+        }
+        lam_loc = smax(0.0, lam);
+        if (P.mech.present && P.chem_dt_limit) {
+            double wdot[NS];
+            source_terms<NS>(rho, T, Y, P.mix, P.mech, wdot);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const double wv = fabs(wdot[s]);
+                if (wv > 0.0) chem_loc = smin(chem_loc, P.chem_dt_factor * (rho * smax(Y[s], 1e-3)) / wv);
+            }
+        }
+    }
+    if (lam_loc > 0.0) atomicMax(&s_lam, (unsigned long long)__double_as_longlong(lam_loc));
+    if (chem_loc < __longlong_as_double(0x7ff0000000000000ll))
+        atomicMin(&s_chem, (unsigned long long)__double_as_longlong(chem_loc));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_lam) atomicMax(&P.red[0], s_lam);
+        if (s_chem != 0x7ff0000000000000ull) atomicMin(&P.red[1], s_chem);
+    }
+}
+
+template <int NS> struct Launch3 {
+    static int bc(const KParams& P, double* Ut, int ypass, int stage, int step, cudaStream_t s) {
+        (void)stage;
+        (void)step;
+        const int g = P.g;
+        if (ypass == 0) {
+            const long long n = 2LL * P.ny * P.nz;
+            k_bc3<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, Ut, 0);
+            return 1;
+        }
+        const long long n1 = 2LL * (P.nx + 2 * g) * P.nz;
+        k_bc3<NS><<<(unsigned)((n1 + 127) / 128), 128, 0, s>>>(P, Ut, 1);
+        const long long n2 = 2LL * (P.nx + 2 * g) * (P.ny + 2 * g);
+        k_bc3<NS><<<(unsigned)((n2 + 127) / 128), 128, 0, s>>>(P, Ut, 2);
+        return 2;
+    }
+    static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
+        const unsigned nb = (unsigned)((P.plane + 255) / 256);
+        if (P.viscous) k_prim3<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step);
+        else k_prim3<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step);
+        return 1;
+    }
+    template <bool TENO, bool CHAR>
+    static void faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
+        launch_faces3d<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
+        launch_faces3d<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
+        launch_faces3d<NS, 2, TENO, CHAR>(P, Ut, stage, step, s);
+    }
+    static int faces(const KParams& P, int teno, int chr, const double* Ut, int stage, int step,
+                     cudaStream_t s) {
+        if (teno && chr) faces_t<true, true>(P, Ut, stage, step, s);
+        else if (teno) faces_t<true, false>(P, Ut, stage, step, s);
+        else if (chr) faces_t<false, true>(P, Ut, stage, step, s);
+        else faces_t<false, false>(P, Ut, stage, step, s);
+        return 3;
+    }
+    static int visc(const KParams& P, int stage, int step, cudaStream_t s) {
+        const long long n = (long long)(P.nx + 2) * (P.ny + 2) * (P.nz + 2);
+        k_visc3<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, stage, step);
+        return 1;
+    }
+    static int assemble(const KParams& P, int mode, const double* U0, const double* Ucur,
+                        double* Uout, double dt, double w, double t_stage, int stage, int step,
+                        int clip_slot, cudaStream_t s) {
+        const unsigned nb = (unsigned)((P.plane + 255) / 256);
+        if (mode == 0)
+            k_assemble3<NS, 0><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
+                                                  clip_slot);
+        else if (mode == 1)
+            k_assemble3<NS, 1><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
+                                                  clip_slot);
+        else
+            k_assemble3<NS, 2><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
+                                                  clip_slot);
+        return 1;
+    }
+    static int dt(const KParams& P, cudaStream_t s) {
+        const long long n = (long long)P.nx * P.ny * P.nz;
+        k_dt3<NS><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P);
+        return 1;
+    }
+    static KernelSet make() { return KernelSet{&bc, &prim, &faces, &visc, &assemble, &dt}; }
+};
+
+}  // namespace ign

@@ -67,6 +67,12 @@ struct KParams {
     const double *vjac, *vmxx, *vmxy, *vmex, *vmey;  // met_v (Central2)
     const double *xc, *yc;                           // mesh.x, mesh.y
     double *Fx, *Gy, *Fv, *Gv;
+    // 3D extension (extruded mesh; nz = 0 for 2D): z cells, state plane
+    // stride, zeta metric (2D planes), z face fluxes, viscous z fluxes
+    int32_t nz, nz_glob;
+    long long sxy;
+    const double *mzz, *vmzz;
+    double *Hz, *Hv;
     const double* inflow[4];  // per edge [t][k][u,v,T,Y_s] profile tables
     ErrRec* err;
     unsigned long long* red;  // [0] lam_max bits, [1] dt_chem bits, [2..7] clip bits
@@ -90,5 +96,34 @@ __device__ __forceinline__ long long pidx(const KParams& P, int i, int j) {
 #define PX(P, s) ((P).prim + (6 + (P).ns + (s)) * (P).plane)
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+}  // namespace ign
+
+namespace ign {
+
+// primitive cache planes of the 3D extension: rho,u,v,w,p,T,c then Y_s, X_s
+#define PRHO3(P) ((P).prim)
+#define PU3(P) ((P).prim + (P).plane)
+#define PV3(P) ((P).prim + 2 * (P).plane)
+#define PW3(P) ((P).prim + 3 * (P).plane)
+#define PP3(P) ((P).prim + 4 * (P).plane)
+#define PT3(P) ((P).prim + 5 * (P).plane)
+#define PC3(P) ((P).prim + 6 * (P).plane)
+#define PY3(P, s) ((P).prim + (7 + (s)) * (P).plane)
+#define PX3(P, s) ((P).prim + (7 + (P).ns + (s)) * (P).plane)
+
+// Launcher table of one (species count, dimension) instantiation; every entry
+// returns the number of kernels it launched.
+struct KernelSet {
+    int (*bc)(const KParams&, double* Ut, int ypass, int stage, int step, cudaStream_t);
+    int (*prim)(const KParams&, const double* Ut, int stage, int step, cudaStream_t);
+    int (*faces)(const KParams&, int teno, int chr, const double* Ut, int stage, int step,
+                 cudaStream_t);
+    int (*visc)(const KParams&, int stage, int step, cudaStream_t);
+    int (*assemble)(const KParams&, int mode, const double* U0, const double* Ucur,
+                    double* Uout, double dt, double w, double t_stage, int stage, int step,
+                    int clip_slot, cudaStream_t);
+    int (*dt)(const KParams&, cudaStream_t);
+};
 
 }  // namespace ign

@@ -41,12 +41,17 @@ class Simulation:
             # creation errors carry no context; re-run the host validation for text
             raise_for(st, self._create_error(st))
         self._h = h
-        nx, ny, g, ns = (C.c_int32() for _ in range(4))
+        nx, ny, g, ns, nz = (C.c_int32() for _ in range(5))
         api["dims"](h, C.byref(nx), C.byref(ny), C.byref(g), C.byref(ns))
+        if "dims3" in api:
+            api["dims3"](h, C.byref(nz))
         self.nx, self.ny, self.g, self.ns = nx.value, ny.value, g.value, ns.value
-        self.nc = self.ns + 3
+        self.nz = nz.value  # 0: 2D (the reference), > 0: 3D extension
+        self.nc = self.ns + (4 if self.nz else 3)
         self.shape = (self.ny + 2 * self.g, self.nx + 2 * self.g)
-        self.plane = self.shape[0] * self.shape[1]
+        if self.nz:
+            self.shape = (self.nz + 2 * self.g,) + self.shape
+        self.plane = int(np.prod(self.shape))
 
     def _create_error(self, st):
         e = abi.Error()
@@ -83,25 +88,42 @@ class Simulation:
 
     # ------------------------------------------------------------ setup
     def mesh_xy(self):
-        x = np.empty(self.plane)
-        y = np.empty(self.plane)
+        shp = self.shape[-2:]
+        n = shp[0] * shp[1]
+        x = np.empty(n)
+        y = np.empty(n)
         self._check(self._api["get_mesh"](self._h, _dptr(x), _dptr(y)))
-        return x.reshape(self.shape), y.reshape(self.shape)
+        return x.reshape(shp), y.reshape(shp)
+
+    def mesh_z(self):
+        """z node coordinates of the 3D extension (uniform, padded)."""
+        c = self.cfg
+        k = np.arange(-self.g, self.nz + self.g)
+        return c.center_z - 0.5 * c.lz + (k + 0.5) * (c.lz / self.nz)
 
     def metrics(self, which: int = 0) -> np.ndarray:
-        out = np.empty(5 * self.plane)
+        shp = self.shape[-2:]
+        out = np.empty(5 * shp[0] * shp[1])
         self._check(self._api["get_metrics"](self._h, which, _dptr(out)))
-        return out.reshape((5,) + self.shape)
+        return out.reshape((5,) + shp)
 
     def set_initial_condition(self, ic: Callable):
         """solver.hpp:115-128 with a vectorised primitive function of the
-        physical node coordinates: ic(X, Y) -> (rho, u, v, T, [Y_s])."""
+        physical node coordinates: ic(X, Y) -> (rho, u, v, T, [Y_s]); 3D
+        extension: ic(X, Y, Z) -> (rho, u, v, w, T, [Y_s])."""
         X, Y = self.mesh_xy()
-        rho, u, v, T, Ys = ic(X, Y)
-        prim = np.empty((4 + self.ns,) + self.shape)
-        prim[0], prim[1], prim[2], prim[3] = rho, u, v, T
-        for s in range(self.ns):
-            prim[4 + s] = Ys[s]
+        if self.nz:
+            Z = self.mesh_z()[:, None, None] * np.ones((1,) + X.shape)
+            X3 = np.broadcast_to(X, Z.shape)
+            Y3 = np.broadcast_to(Y, Z.shape)
+            rho, u, v, w, T, Ys = ic(X3, Y3, Z)
+            fields = [rho, u, v, w, T] + list(Ys)
+        else:
+            rho, u, v, T, Ys = ic(X, Y)
+            fields = [rho, u, v, T] + list(Ys)
+        prim = np.empty((len(fields),) + self.shape)
+        for k, f in enumerate(fields):
+            prim[k] = f
         prim = np.ascontiguousarray(prim)
         self._check(self._api["set_initial_primitives"](self._h, _dptr(prim)))
 
@@ -122,11 +144,12 @@ class Simulation:
         return out.reshape((self.nc,) + self.shape)
 
     def cache(self) -> dict:
-        out = np.empty((6 + self.ns) * self.plane)
+        names = ("rho", "u", "v", "w", "p", "T", "c") if self.nz else ("rho", "u", "v", "p", "T", "c")
+        out = np.empty((len(names) + self.ns) * self.plane)
         self._check(self._api["get_cache"](self._h, _dptr(out)))
-        out = out.reshape((6 + self.ns,) + self.shape)
-        d = {k: out[i] for i, k in enumerate(("rho", "u", "v", "p", "T", "c"))}
-        d["Y"] = out[6:]
+        out = out.reshape((len(names) + self.ns,) + self.shape)
+        d = {k: out[i] for i, k in enumerate(names)}
+        d["Y"] = out[len(names):]
         return d
 
     @property
@@ -269,9 +292,10 @@ class SlabGroup:
 
     def cache_T(self, k: int) -> np.ndarray:
         m = self.members[k]
-        out = np.empty((6 + m.ns) * m.plane)
+        head = 7 if m.nz else 6
+        out = np.empty((head + m.ns) * m.plane)
         self._check(self.member_call(k, "get_cache", _dptr(out)))
-        return out.reshape((6 + m.ns,) + m.shape)[4]
+        return out.reshape((head + m.ns,) + m.shape)[head - 2]
 
     def prepare_stage(self, stage: int = 1):
         self._check(self._api["group_prepare_stage"](self._g, stage))

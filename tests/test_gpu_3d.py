@@ -1,0 +1,214 @@
+"""3D extension (BASELINE configs[1], TGV 256^3) against the 2D oracle.
+
+The reference is 2D-only, so the 3D path is anchored on the
+z-extrusion cross-check of SURVEY §8c:
+
+  * (x, y) extrusion: a 2D case on nz = 7 planes with dz = 1.0, w = 0 and
+    z-constant data.  Every z plane must reproduce the 2D oracle: bitwise (up
+    to the sign of zero) for the gamma-gas cases, within the 2D multi-species
+    tolerances otherwise — and bitwise equal to the 2D B200 path in all cases.
+  * (x, z) extrusion: a 2D case laid in the x-z plane (v = 0, y-constant,
+    dy = 1) exercises the zeta-face kernel; equal to the 2D oracle within a
+    tolerance (the 2D oracle's y metrics carry ulp noise the uniform z
+    metrics do not).
+  * 3D TGV: periodic conservation of mass, momenta and energy.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2202_02319_b200 import Simulation, abi, configs
+from tests.parity import clone_cfg, field_errors
+
+pytestmark = pytest.mark.gpu
+
+RHS_TOL = 1e-13
+STEP_TOL = 1e-10
+XZ_TOL = 1e-11
+
+# name -> (2D builder, exact vs oracle, nsteps)
+EXTRUDE = {
+    "tgv_char_teno6_visc": (lambda: configs.tgv2d(24), True, 8),
+    "tgv_comp_teno6_inviscid": (lambda: configs.tgv2d(24, split="comp", viscous=False), False, 8),
+    "tgv_char_weno3z_visc": (lambda: configs.tgv2d(20, scheme="weno3z"), True, 8),
+    "tgv_comp_weno3z_visc": (lambda: configs.tgv2d(20, scheme="weno3z", split="comp"), False, 8),
+    "tgv_skew_char_teno6": (lambda: configs.tgv2d(24, skew=0.2), True, 6),
+    "ch4_react_char": (lambda: configs.reacting_ch4(20, laser=False), False, 8),
+    "ch4_react_comp_weno3z": (lambda: configs.reacting_ch4(20, scheme="weno3z", split="comp",
+                                                          laser=False), False, 8),
+}
+
+NZ = 7
+
+
+def same_values(a, b):
+    """Bitwise equality except +0 == -0 (z terms add exact zeros)."""
+    return a.shape == b.shape and bool(np.all((a == b) | (np.isnan(a) & np.isnan(b))))
+
+
+def planes(U3, ns, g=3):
+    """The nz interior z planes of a 3D component array, in 2D component order."""
+    return [configs.state_3d_to_2d(U3, ns, k) for k in range(g, U3.shape[1] - g)]
+
+
+@pytest.fixture(params=sorted(EXTRUDE))
+def triple(request, oracle_api, cuda_device):
+    mk, exact, n = EXTRUDE[request.param]
+    case = mk()
+    refs = Simulation(clone_cfg(case.cfg), oracle_api)
+    refs.set_initial_condition(case.ic)
+    prod2 = Simulation(clone_cfg(case.cfg))
+    prod2.set_state(refs.Ut)
+    case3 = configs.extrude_z(case, NZ)
+    prod3 = Simulation(clone_cfg(case3.cfg))
+    assert prod3.nz == NZ and prod3.nc == prod2.nc + 1
+    prod3.set_state(configs.state_2d_to_3d(refs.Ut, refs.ns, NZ))
+    yield case, refs, prod2, prod3, exact, n
+    for s in (refs, prod2, prod3):
+        s.close()
+
+
+def test_extrusion_initial_condition(oracle_api, cuda_device):
+    """set_initial_primitives' 3D conversion reduces to the 2D one (w = 0)."""
+    for mk in (lambda: configs.tgv2d(16), lambda: configs.reacting_ch4(16, laser=False)):
+        case = mk()
+        refs = Simulation(clone_cfg(case.cfg), oracle_api)
+        refs.set_initial_condition(case.ic)
+        case3 = configs.extrude_z(case, NZ)
+        p3 = Simulation(clone_cfg(case3.cfg))
+        p3.set_initial_condition(case3.ic)
+        U3 = p3.Ut
+        for pl in planes(U3, refs.ns):
+            assert same_values(pl[..., 3:-3, 3:-3], refs.Ut[..., 3:-3, 3:-3])
+        assert not np.any(U3[refs.ns + 2])
+
+
+def test_extrusion_prepare_stage(triple):
+    case, refs, prod2, prod3, exact, n = triple
+    for s in (refs, prod3):
+        s.prepare_stage(1)
+    a, b = prod3.cache(), refs.cache()
+    g = 3
+    for k in ("rho", "u", "v", "p", "T", "c"):
+        for kz in range(g, g + NZ):
+            assert same_values(a[k][kz], b[k]), k
+    assert not np.any(a["w"])
+    for pl in planes(prod3.Ut, refs.ns):
+        assert same_values(pl, refs.Ut)  # (x, y) ghosts filled identically
+
+
+def test_extrusion_rhs(triple):
+    case, refs, prod2, prod3, exact, n = triple
+    for s in (refs, prod2, prod3):
+        s.prepare_stage(1)
+    t = 0.37 * case.dt
+    r3 = prod3.compute_rhs(t, 1)
+    r2 = prod2.compute_rhs(t, 1)
+    rr = refs.compute_rhs(t, 1)
+    g = 3
+    assert not np.any(r3[refs.ns + 2, g:-g, g:-g, g:-g])  # d(rho w)/dt == 0
+    for pl in planes(r3, refs.ns):
+        pi, p2 = pl[..., g:-g, g:-g], r2[..., g:-g, g:-g]
+        assert same_values(pi, p2)
+        if exact:
+            assert same_values(pi, rr[..., g:-g, g:-g])
+        else:
+            assert field_errors(pl, rr, refs.ns).max() <= RHS_TOL
+
+
+def test_extrusion_steps(triple):
+    case, refs, prod2, prod3, exact, n = triple
+    for s in (refs, prod2, prod3):
+        s.prepare_stage(1)
+        s.rk3_steps(case.dt, n)
+    assert prod3.iter == refs.iter == n and prod3.time == refs.time
+    U3, U2, Ur = prod3.Ut, prod2.Ut, refs.Ut
+    assert not np.any(U3[refs.ns + 2])
+    for pl in planes(U3, refs.ns):
+        assert same_values(pl, U2)
+        if exact:
+            assert same_values(pl, Ur)
+        else:
+            assert field_errors(pl, Ur, refs.ns).max() <= STEP_TOL
+    # ±0 aside, the temperature cache (the Newton guess) carries over too
+    T3 = prod3.cache()["T"]
+    for kz in range(3, 3 + NZ):
+        assert same_values(T3[kz], prod2.cache()["T"])
+
+
+def test_extrusion_stable_dt_bounded(triple):
+    """The 3D spectral radius adds the z term: dt3 <= dt2 (solver.hpp:370-383)."""
+    case, refs, prod2, prod3, exact, n = triple
+    for s in (refs, prod3):
+        s.prepare_stage(1)
+    d3, d2 = prod3.stable_dt(), refs.stable_dt()
+    assert 0.0 < d3 <= d2
+
+
+# ----------------------------------------------------------------- x-z plane
+def _xz_pair(oracle_api, case2):
+    """A 2D case laid in the (x, z) plane of a 3D box: ny = 7 cells of dy = 1."""
+    c2 = case2.cfg
+    cfg3 = clone_cfg(c2)
+    cfg3.ny, cfg3.ly, cfg3.center_y = NZ, float(NZ), 0.0
+    cfg3.nz, cfg3.lz, cfg3.center_z, cfg3.periodic_z = c2.ny, c2.ly, c2.center_y, 1
+    ic2 = case2.ic
+
+    def ic3(X, Y, Z):
+        rho, u, v, T, Ys = ic2(X, Z)
+        return rho, u, np.zeros_like(X), v, T, Ys
+
+    refs = Simulation(clone_cfg(c2), oracle_api)
+    refs.set_initial_condition(ic2)
+    p3 = Simulation(cfg3)
+    p3.set_initial_condition(ic3)
+    return refs, p3
+
+
+def _xz_to_2d(U3, ns, j):
+    """3D [.., rho u, rho v, rho w, E](z, y, x) at y index j -> 2D (y := z)."""
+    return np.concatenate([U3[: ns + 1, :, j], U3[ns + 2: ns + 4, :, j]])
+
+
+@pytest.mark.parametrize("mk", [
+    lambda: configs.tgv2d(24),
+    lambda: configs.tgv2d(20, scheme="weno3z", split="comp"),
+    lambda: configs.reacting_ch4(16, laser=False),
+], ids=["tgv_char_teno6", "tgv_comp_weno3z", "ch4_char"])
+def test_xz_plane_matches_oracle(mk, oracle_api, cuda_device):
+    case = mk()
+    refs, p3 = _xz_pair(oracle_api, case)
+    ns, g = refs.ns, 3
+    for s in (refs, p3):
+        s.prepare_stage(1)
+    t = 0.25 * case.dt
+    r3, rr = p3.compute_rhs(t, 1), refs.compute_rhs(t, 1)
+    assert not np.any(r3[ns + 1, g:-g, g:-g, g:-g])  # d(rho v)/dt == 0
+    for j in range(g, g + NZ):
+        assert field_errors(_xz_to_2d(r3, ns, j), rr, ns).max() <= XZ_TOL
+    for s in (refs, p3):
+        s.rk3_steps(case.dt, 5)
+    U3, Ur = p3.Ut, refs.Ut
+    for j in range(g, g + NZ):
+        assert field_errors(_xz_to_2d(U3, ns, j), Ur, ns).max() <= XZ_TOL
+
+
+# ----------------------------------------------------------------- 3D TGV
+def test_tgv3d_conservation_and_symmetry(cuda_device):
+    """Config B at 32^3: periodic totals conserved; the TGV's x <-> y mirror
+    symmetry (u(x,y,z) = -v(y,x,z)) is preserved by the scheme to rounding."""
+    case = configs.tgv3d(32)
+    sim = Simulation(case.cfg)
+    sim.set_initial_condition(case.ic)
+    sim.prepare_stage(1)
+    tot0 = sim.conserved_totals()
+    sim.rk3_steps(case.dt, 10)
+    tot1 = sim.conserved_totals()
+    assert sim.iter == 10
+    # mass scale rho0 V also bounds the momenta (|u| <= 1)
+    scale = np.array([tot0[0]] * 4 + [abs(tot0[4])])
+    assert np.all(np.abs(tot1 - tot0) <= 1e-12 * scale), (tot0, tot1)
+    U = sim.Ut[..., 3:-3, 3:-3, 3:-3]
+    ru, rv = U[1], U[2]
+    assert np.abs(ru + np.swapaxes(rv, 1, 2)).max() <= 1e-12
