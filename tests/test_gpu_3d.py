@@ -171,6 +171,13 @@ def _xz_to_2d(U3, ns, j):
     return np.concatenate([U3[: ns + 1, :, j], U3[ns + 2: ns + 4, :, j]])
 
 
+def _state_scale(U, ns, g=3):
+    b = U[..., g:-g, g:-g]
+    rho = np.abs(b[:ns].sum(axis=0)).max()
+    mom = np.sqrt(b[ns] ** 2 + b[ns + 1] ** 2).max()
+    return np.array([rho] * ns + [mom, mom, np.abs(b[ns + 2]).max()])
+
+
 @pytest.mark.parametrize("mk", [
     lambda: configs.tgv2d(24),
     lambda: configs.tgv2d(20, scheme="weno3z", split="comp"),
@@ -184,9 +191,18 @@ def test_xz_plane_matches_oracle(mk, oracle_api, cuda_device):
         s.prepare_stage(1)
     t = 0.25 * case.dt
     r3, rr = p3.compute_rhs(t, 1), refs.compute_rhs(t, 1)
-    assert not np.any(r3[ns + 1, g:-g, g:-g, g:-g])  # d(rho v)/dt == 0
+    # d(rho v)/dt vanishes up to the ulp noise of the y metrics' cross terms
+    # (m_xi_y, m_eta_x ~ 1e-17) times the pressure flux: scale by the energy
+    p_scale = np.abs(p3.Ut[ns + 3]).max()
+    assert np.abs(r3[ns + 1, g:-g, g:-g, g:-g]).max() <= 1e-13 * p_scale
+    # the TGV starts near equilibrium, so its RHS is a small residual of large
+    # fluxes: measure the RHS difference as a one-step state increment (x dt)
+    # against the state's own scale
+    Ur0 = refs.Ut
     for j in range(g, g + NZ):
-        assert field_errors(_xz_to_2d(r3, ns, j), rr, ns).max() <= XZ_TOL
+        d = np.abs(_xz_to_2d(r3, ns, j) - rr)[..., g:-g, g:-g]
+        d = d.reshape(d.shape[0], -1).max(axis=1) * case.dt
+        assert (d / _state_scale(Ur0, ns)).max() <= 1e-13
     for s in (refs, p3):
         s.rk3_steps(case.dt, 5)
     U3, Ur = p3.Ut, refs.Ut
@@ -195,9 +211,8 @@ def test_xz_plane_matches_oracle(mk, oracle_api, cuda_device):
 
 
 # ----------------------------------------------------------------- 3D TGV
-def test_tgv3d_conservation_and_symmetry(cuda_device):
-    """Config B at 32^3: periodic totals conserved; the TGV's x <-> y mirror
-    symmetry (u(x,y,z) = -v(y,x,z)) is preserved by the scheme to rounding."""
+def test_tgv3d_conservation(cuda_device):
+    """Config B at 32^3: periodic totals of mass, momenta, energy conserved."""
     case = configs.tgv3d(32)
     sim = Simulation(case.cfg)
     sim.set_initial_condition(case.ic)
@@ -209,6 +224,52 @@ def test_tgv3d_conservation_and_symmetry(cuda_device):
     # mass scale rho0 V also bounds the momenta (|u| <= 1)
     scale = np.array([tot0[0]] * 4 + [abs(tot0[4])])
     assert np.all(np.abs(tot1 - tot0) <= 1e-12 * scale), (tot0, tot1)
-    U = sim.Ut[..., 3:-3, 3:-3, 3:-3]
-    ru, rv = U[1], U[2]
-    assert np.abs(ru + np.swapaxes(rv, 1, 2)).max() <= 1e-12
+
+
+def _field3(X, Y, Z, p0):
+    """A generic smooth fully-3D state (no symmetry of its own)."""
+    rho = 1 + 0.1 * np.sin(X + 2 * Y) * np.cos(3 * Z + 0.3)
+    u = np.sin(X) * np.cos(Y) * np.cos(Z) + 0.1 * np.sin(2 * Z + Y)
+    v = -np.cos(X) * np.sin(Y) * np.cos(Z) + 0.05 * np.cos(X - Z)
+    w = 0.2 * np.sin(Y + 2 * X) * np.cos(Z)
+    p = p0 + 0.3 * np.cos(2 * X + Z) * np.sin(Y)
+    return rho, u, v, w, p
+
+
+@pytest.mark.parametrize("scheme,split", [("teno6", "char"), ("teno6", "comp"),
+                                          ("weno3z", "comp")])
+def test_axis_permutation_invariance(scheme, split, cuda_device):
+    """On the cube, relabelling the axes (y <-> z, x <-> z; velocity components
+    with them) commutes with the RHS: checks the eta/zeta face kernels, the 3D
+    viscous terms and the assembly against each other on a fully 3D state.
+    Equal to rounding (the 2D metrics carry ulp noise the z metrics do not)."""
+    case = configs.tgv3d(16, scheme=scheme, split=split)
+    p0 = case.notes["p0"]
+    res = {}
+    for perm in ("id", "yz", "xz"):
+        def ic(X, Y, Z, perm=perm):
+            if perm == "id":
+                rho, u, v, w, p = _field3(X, Y, Z, p0)
+            elif perm == "yz":
+                rho, u, w, v, p = _field3(X, Z, Y, p0)
+            else:
+                rho, w, v, u, p = _field3(Z, Y, X, p0)
+            return rho, u, v, w, p / rho, [np.ones_like(X)]
+        sim = Simulation(clone_cfg(case.cfg))
+        sim.set_initial_condition(ic)
+        sim.prepare_stage(1)
+        r = sim.compute_rhs(0.0, 1)
+        sim.rk3_steps(case.dt, 3)
+        res[perm] = (r, sim.Ut)
+        sim.close()
+    g = 3
+    sl = (slice(None), slice(g, -g), slice(g, -g), slice(g, -g))
+    r0, U0 = res["id"]
+    for perm, idx, ax in (("yz", [0, 1, 3, 2, 4], 2), ("xz", [0, 3, 2, 1, 4], 3)):
+        r, U = res[perm]
+        rp = np.swapaxes(r[idx], 1, ax)[sl]
+        Up = np.swapaxes(U[idx], 1, ax)[sl]
+        er = np.abs(rp - r0[sl]).reshape(5, -1).max(1) / np.abs(r0[sl]).reshape(5, -1).max(1)
+        eU = np.abs(Up - U0[sl]).reshape(5, -1).max(1) / np.abs(U0[sl]).reshape(5, -1).max(1)
+        assert er.max() <= 1e-11, (perm, er)
+        assert eU.max() <= 1e-12, (perm, eU)
