@@ -193,10 +193,12 @@ void ign_destroy(ign_context* ctx);
 int ign_last_error(const ign_context* ctx, ign_error* err);
 int ign_dims(const ign_context* ctx, int32_t* nx, int32_t* ny, int32_t* g,
              int32_t* ns);
-/* 3D extension: cells in z (0 for the reference's 2D path).  In 3D the padded
- * planes are (nx+2g)(ny+2g)(nz+2g), k slowest; set_initial_primitives takes
- * rho,u,v,w,T,Y_s and get_cache returns rho,u,v,w,p,T,c,Y_s. */
-int ign_dims3(const ign_context* ctx, int32_t* nz);
+/* 3D extension: this context's cells in z (0 for the reference's 2D path),
+ * its first global z cell k0 and the global count (z-slabs: nz < nz_glob).
+ * In 3D the padded planes are (nx+2g)(ny+2g)(nz+2g), k slowest;
+ * set_initial_primitives takes rho,u,v,w,T,Y_s and get_cache returns
+ * rho,u,v,w,p,T,c,Y_s.  Any pointer may be NULL. */
+int ign_dims3(const ign_context* ctx, int32_t* nz, int32_t* k0, int32_t* nz_glob);
 
 /* ---- setup / host mirrors --------------------------------------------- */
 /* mesh.x/mesh.y padded arrays (mesh.hpp:295-296) */

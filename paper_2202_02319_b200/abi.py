@@ -172,7 +172,7 @@ PRODUCT_ONLY = {
     "profile_read": (_I, [_P, _D, C.POINTER(C.c_int64)]),
     "stream_handle": (C.c_void_p, [_P]),
     "probe_fp64_peak": (_I, [_I, _D]),
-    "dims3": (_I, [_P, _I32P]),
+    "dims3": (_I, [_P, _I32P, _I32P, _I32P]),
     # multi-GPU slabs
     "nccl_unique_id": (_I, [C.c_char_p]),
     "attach_nccl": (_I, [_P, C.c_char_p, _I, _I]),

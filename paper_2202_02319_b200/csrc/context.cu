@@ -101,6 +101,7 @@ struct ign_context {
     double *Fx = nullptr, *Gy = nullptr, *Fv = nullptr, *Gv = nullptr, *rhs = nullptr;
     double *Hz = nullptr, *Hv = nullptr;  // 3D extension
     int nz = 0;                           // 0: 2D (the reference), > 0: 3D extension
+    int k0 = 0, nz_glob = 0;              // 3D z-slab: first global z cell, global count
     double* inflow[4] = {nullptr, nullptr, nullptr, nullptr};
     double* wrap[2] = {nullptr, nullptr};
     ErrRec* err = nullptr;      // the word the kernels report into
@@ -321,6 +322,14 @@ Error to_error(const ign_context* ctx, const DevFail& f) {
     case PH_BC: return state_error(pstatus_msg(f.sub));
     case PH_PRIM: {
         const int sx = ctx->nx + 2 * ctx->g;
+        if (ctx->nz > 0) {  // 3D: global padded (i, j, k) of the node
+            const unsigned long long sy = ctx->ny + 2 * ctx->g;
+            const int i = (int)(f.idx % sx) - ctx->g, j = (int)((f.idx / sx) % sy) - ctx->g;
+            const int k = (int)(f.idx / (sx * sy)) - ctx->g;
+            return step_failure(std::string("stage state failure: ") + pstatus_msg(f.sub) +
+                                    " (k=" + std::to_string(k) + ")",
+                                rep_stage, i, j);
+        }
         const int i = (int)(f.idx % sx) - ctx->g, j = (int)(f.idx / sx) - ctx->g;
         return step_failure(std::string("stage state failure: ") + pstatus_msg(f.sub),
                             rep_stage, i, j);
@@ -331,12 +340,15 @@ Error to_error(const ign_context* ctx, const DevFail& f) {
         if (f.sub == 3) return numerics_error("eigen: non-positive c^2");
         return numerics_error("inviscid face: non-finite wavespeed");
     case PH_RHS: {
-        const int i = (int)(f.idx % ctx->nx), j = (int)(f.idx / ctx->nx);
+        const unsigned long long cell = f.idx;
+        const int i = (int)(cell % ctx->nx);
+        const int j = (int)(ctx->nz > 0 ? (cell / ctx->nx) % ctx->ny : cell / ctx->nx);
         return step_failure("non-finite RHS", rep_stage, i, j);
     }
     default: {
         const unsigned long long cell = f.idx / 2;
-        const int i = (int)(cell % ctx->nx), j = (int)(cell / ctx->nx);
+        const int i = (int)(cell % ctx->nx);
+        const int j = (int)(ctx->nz > 0 ? (cell / ctx->nx) % ctx->ny : cell / ctx->nx);
         return step_failure(f.idx % 2 ? "non-finite state" : "non-positive density", rep_stage,
                             i, j);
     }
@@ -361,15 +373,21 @@ void t_errsync(const Team& T) {
 // Halo rows of state buffer `buf`: our g bottom/top interior rows to the
 // neighbours, their rows into our ghost rows (all components; rows are
 // contiguous in the padded planes, so every transfer is one contiguous chunk).
+// 2D: y-slabs exchange g padded rows; 3D: z-slabs exchange g padded planes
+static size_t halo_stride(const ign_context* c) {
+    return c->nz > 0 ? size_t(c->kp.sxy) : size_t(c->kp.sx);
+}
+static size_t halo_count(const ign_context* c) { return c->nz > 0 ? c->nz : c->ny; }
+
 void t_exchange(const Team& T, int buf) {
     if (T.local()) {
         for (ign_context* c : T.m) {
-            const size_t chunk = size_t(c->g) * c->kp.sx;
+            const size_t st = halo_stride(c), chunk = size_t(c->g) * st;
             for (int comp = 0; comp < c->nc; ++comp) {
                 if (c->lo_peer >= 0) {
                     const ign_context* s = T.m[c->lo_peer];
                     cuda_check(cudaMemcpyAsync(c->S[buf] + comp * c->plane,
-                                               s->S[buf] + comp * s->plane + size_t(s->ny) * s->kp.sx,
+                                               s->S[buf] + comp * s->plane + halo_count(s) * st,
                                                chunk * sizeof(double), cudaMemcpyDeviceToDevice,
                                                T.stream()),
                                "halo copy");
@@ -377,7 +395,7 @@ void t_exchange(const Team& T, int buf) {
                 if (c->hi_peer >= 0) {
                     const ign_context* s = T.m[c->hi_peer];
                     cuda_check(cudaMemcpyAsync(c->S[buf] + comp * c->plane +
-                                                   size_t(c->ny + c->g) * c->kp.sx,
+                                                   (halo_count(c) + c->g) * st,
                                                s->S[buf] + comp * s->plane + chunk,
                                                chunk * sizeof(double), cudaMemcpyDeviceToDevice,
                                                T.stream()),
@@ -392,14 +410,14 @@ void t_exchange(const Team& T, int buf) {
     if (!c->comm)
         throw usage_error("slab context without a transport: call ign_attach_nccl or use a group");
     NcclApi& n = nccl();
-    const size_t chunk = size_t(c->g) * c->kp.sx;
+    const size_t st = halo_stride(c), chunk = size_t(c->g) * st, nl = halo_count(c);
     nccl_check(n.GroupStart(), "ncclGroupStart");
     for (int comp = 0; comp < c->nc; ++comp) {
         double* base = c->S[buf] + comp * c->plane;
         // per peer pair the order is [top, bottom] sends against [lo, hi]
         // receives, so a two-slab periodic ring matches correctly
         if (c->hi_peer >= 0)
-            nccl_check(n.Send(base + size_t(c->ny) * c->kp.sx, chunk, ncclFloat64, c->hi_peer,
+            nccl_check(n.Send(base + nl * st, chunk, ncclFloat64, c->hi_peer,
                               c->comm, c->stream), "ncclSend");
         if (c->lo_peer >= 0)
             nccl_check(n.Send(base + chunk, chunk, ncclFloat64, c->lo_peer, c->comm, c->stream),
@@ -408,7 +426,7 @@ void t_exchange(const Team& T, int buf) {
             nccl_check(n.Recv(base, chunk, ncclFloat64, c->lo_peer, c->comm, c->stream),
                        "ncclRecv");
         if (c->hi_peer >= 0)
-            nccl_check(n.Recv(base + size_t(c->ny + c->g) * c->kp.sx, chunk, ncclFloat64,
+            nccl_check(n.Recv(base + (nl + c->g) * st, chunk, ncclFloat64,
                               c->hi_peer, c->comm, c->stream), "ncclRecv");
     }
     nccl_check(n.GroupEnd(), "ncclGroupEnd");
@@ -868,25 +886,30 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->rank = ctx->nranks > 1 ? cfg->slab_rank : 0;
     if (ctx->rank < 0 || ctx->rank >= ctx->nranks) throw usage_error("slab_rank out of range");
     // Simulation::init (solver.hpp:82-101), on this slab's rows
-    ctx->mesh = build_mesh(*cfg, ctx->nranks, ctx->rank);
+    // 2D: y-slabs of the mesh; 3D: z-slabs over the whole (x, y) mesh
+    const bool three_d = cfg->nz > 0;
+    ctx->mesh = three_d ? build_mesh(*cfg, 1, 0) : build_mesh(*cfg, ctx->nranks, ctx->rank);
     validate_config(*cfg, ctx->mesh);
     const int imode = inviscid_metric_mode(*cfg);
     ctx->met = compute_metrics(ctx->mesh, imode, cfg->skew_beta);
     ctx->metv = compute_metrics(ctx->mesh, MM_CENTRAL2, 0.0);
     ctx->integ = cfg->integ;
-    const int nz = cfg->nz > 0 ? cfg->nz : 0;
-    ctx->nz = nz;
+    int nz = 0;
     std::vector<double> mzz, vmzz;
-    if (nz > 0) {
+    if (three_d) {
         // 3D extension: the (x, y) mesh extruded over lz (flux3.cuh)
-        if (nz < 2 * cfg->g + 1) throw config_error("3D: nz must be >= 2g+1");
         if (!(cfg->lz > 0.0)) throw config_error("3D: lz must be positive");
-        if (ctx->nranks > 1) throw usage_error("3D: slab decomposition is 2D-only for now");
         if (!cfg->periodic_x || !cfg->periodic_y || !cfg->periodic_z)
             throw usage_error("3D: only periodic boundaries are supported");
         if (cfg->laser.present && cfg->laser.energy != 0.0)
             throw usage_error("3D: the laser source has no 3D form in the reference");
-        const double dz = cfg->lz / nz;
+        int k0 = 0;
+        slab_rows(cfg->nz, ctx->nranks, ctx->rank, k0, nz);
+        if (nz < cfg->g) throw config_error("3D: every z-slab needs >= g planes");
+        if (ctx->nranks == 1 && nz < 2 * cfg->g + 1) throw config_error("3D: nz must be >= 2g+1");
+        ctx->k0 = k0;
+        ctx->nz_glob = cfg->nz;
+        const double dz = cfg->lz / cfg->nz;
         // cofactor metrics of (x(i,j), y(i,j), z(k)): xi/eta rows scale by z_zeta
         // = dz, zeta row is the 2D area, J = 1/(area dz) — for dz = 1 every value
         // is the 2D one bit for bit (the z-extrusion cross-check)
@@ -908,8 +931,9 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     }
     const int nx = cfg->nx, ny = ctx->mesh.ny, g = cfg->g, ns = cfg->mix.ns,
               nc = ns + (nz > 0 ? 4 : 3);
+    ctx->nz = nz;
     const int N = ctx->nranks, r = ctx->rank;
-    const bool py = cfg->periodic_y != 0;
+    const bool py = (three_d ? cfg->periodic_z : cfg->periodic_y) != 0;
     if (N > 1) {
         ctx->lo_peer = r > 0 ? r - 1 : (py ? N - 1 : -1);
         ctx->hi_peer = r < N - 1 ? r + 1 : (py ? 0 : -1);
@@ -964,8 +988,8 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     // inflow profile tables (boundary.hpp:227-241 ghost targets)
     const ign_edge* edges[4] = {&cfg->bc.left, &cfg->bc.right, &cfg->bc.bottom, &cfg->bc.top};
     int bc_type[4] = {edges[0]->type, edges[1]->type, edges[2]->type, edges[3]->type};
-    if (ctx->lo_peer >= 0) bc_type[2] = (r == 0) ? BC_HALO_WRAP : BC_HALO;
-    if (ctx->hi_peer >= 0) bc_type[3] = (r == N - 1) ? BC_HALO_WRAP : BC_HALO;
+    if (!three_d && ctx->lo_peer >= 0) bc_type[2] = (r == 0) ? BC_HALO_WRAP : BC_HALO;
+    if (!three_d && ctx->hi_peer >= 0) bc_type[3] = (r == N - 1) ? BC_HALO_WRAP : BC_HALO;
     for (int e = 0; e < 4; ++e) {
         if (bc_type[e] != 3) continue;
         const bool xedge = e < 2;
@@ -1074,7 +1098,11 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
         k.yc = ctx->geom + 11 * P2;
     }
     k.nz = nz;
-    k.nz_glob = nz;
+    k.nz_glob = three_d ? ctx->nz_glob : 0;
+    if (three_d) {
+        k.j0 = ctx->k0;  // 3D: global z offset of the slab (error keys)
+        k.zhalo = ctx->lo_peer >= 0 || ctx->hi_peer >= 0;
+    }
     k.sxy = static_cast<long long>(P2);
     k.Fx = ctx->Fx;
     k.Gy = ctx->Gy;
@@ -1172,8 +1200,10 @@ int ign_get_mesh(const ign_context* ctx, double* x, double* y) {
     return IGN_OK;
 }
 
-int ign_dims3(const ign_context* ctx, int32_t* nz) {
-    *nz = ctx->nz;
+int ign_dims3(const ign_context* ctx, int32_t* nz, int32_t* k0, int32_t* nz_glob) {
+    if (nz) *nz = ctx->nz;
+    if (k0) *k0 = ctx->k0;
+    if (nz_glob) *nz_glob = ctx->nz_glob;
     return IGN_OK;
 }
 

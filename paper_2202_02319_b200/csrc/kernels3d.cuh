@@ -344,20 +344,24 @@ __global__ void __launch_bounds__(256) k_dt3(const __grid_constant__ KParams P) 
 }
 
 template <int NS> struct Launch3 {
+    // ypass 0 (before the halo exchange): x then y periodic copies, so the
+    // exchanged z planes carry their x/y ghosts; ypass 1: z copies (single
+    // domain) — with z-slabs the z ghost planes came from the peers instead
     static int bc(const KParams& P, double* Ut, int ypass, int stage, int step, cudaStream_t s) {
         (void)stage;
         (void)step;
         const int g = P.g;
         if (ypass == 0) {
-            const long long n = 2LL * P.ny * P.nz;
-            k_bc3<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, Ut, 0);
-            return 1;
+            const long long n0 = 2LL * P.ny * P.nz;
+            k_bc3<NS><<<(unsigned)((n0 + 127) / 128), 128, 0, s>>>(P, Ut, 0);
+            const long long n1 = 2LL * (P.nx + 2 * g) * P.nz;
+            k_bc3<NS><<<(unsigned)((n1 + 127) / 128), 128, 0, s>>>(P, Ut, 1);
+            return 2;
         }
-        const long long n1 = 2LL * (P.nx + 2 * g) * P.nz;
-        k_bc3<NS><<<(unsigned)((n1 + 127) / 128), 128, 0, s>>>(P, Ut, 1);
+        if (P.zhalo) return 0;
         const long long n2 = 2LL * (P.nx + 2 * g) * (P.ny + 2 * g);
         k_bc3<NS><<<(unsigned)((n2 + 127) / 128), 128, 0, s>>>(P, Ut, 2);
-        return 2;
+        return 1;
     }
     static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
         const unsigned nb = (unsigned)((P.plane + 255) / 256);

@@ -70,6 +70,7 @@ struct KParams {
     // 3D extension (extruded mesh; nz = 0 for 2D): z cells, state plane
     // stride, zeta metric (2D planes), z face fluxes, viscous z fluxes
     int32_t nz, nz_glob;
+    int32_t zhalo, _pad3;  // 3D z-slabs: z ghost planes come from the peers
     long long sxy;
     const double *mzz, *vmzz;
     double *Hz, *Hv;

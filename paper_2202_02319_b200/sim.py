@@ -41,10 +41,11 @@ class Simulation:
             # creation errors carry no context; re-run the host validation for text
             raise_for(st, self._create_error(st))
         self._h = h
-        nx, ny, g, ns, nz = (C.c_int32() for _ in range(5))
+        nx, ny, g, ns, nz, k0, nzg = (C.c_int32() for _ in range(7))
         api["dims"](h, C.byref(nx), C.byref(ny), C.byref(g), C.byref(ns))
         if "dims3" in api:
-            api["dims3"](h, C.byref(nz))
+            api["dims3"](h, C.byref(nz), C.byref(k0), C.byref(nzg))
+        self.k0, self.nz_glob = k0.value, nzg.value
         self.nx, self.ny, self.g, self.ns = nx.value, ny.value, g.value, ns.value
         self.nz = nz.value  # 0: 2D (the reference), > 0: 3D extension
         self.nc = self.ns + (4 if self.nz else 3)
@@ -98,8 +99,8 @@ class Simulation:
     def mesh_z(self):
         """z node coordinates of the 3D extension (uniform, padded)."""
         c = self.cfg
-        k = np.arange(-self.g, self.nz + self.g)
-        return c.center_z - 0.5 * c.lz + (k + 0.5) * (c.lz / self.nz)
+        k = self.k0 + np.arange(-self.g, self.nz + self.g)  # global z index (z-slabs)
+        return c.center_z - 0.5 * c.lz + (k + 0.5) * (c.lz / self.nz_glob)
 
     def metrics(self, which: int = 0) -> np.ndarray:
         shp = self.shape[-2:]
