@@ -2,16 +2,19 @@
 """Benchmark of the B200 RHS + SSP-RK3 path (BASELINE.json metric:
 "FP64 cell-updates/s per RK step").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--n 4096]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--case tgv3d|tgv|h2o2] [--n N]
 
 A "step" is one full SSP-RK3 step (three RHS evaluations + updates + the
 advance-loop prepare_stage(1), solver.hpp:304-345) over the whole grid.
 
-Workload (config.workload): 2D compressible viscous Taylor-Green vortex at
-4096^2 interior cells = 16.8 M cells, the same cell count as BASELINE
-configs[1] (TGV 256^3); the reference is 2D-only so its 3D case has no oracle
-(SURVEY §0).  γ-gas, TENO6 characteristic, Re 1600, Ma 0.1, fixed dt.
-The state (4 x 538 MB) is far larger than the 126 MB L2, so no flush is needed.
+Workload (config.workload): BASELINE configs[1], the 3D compressible viscous
+Taylor-Green vortex at 256^3 = 16.8 M cells (gamma-gas, TENO6 characteristic,
+Re 1600, Ma 0.1, fixed dt), on the 3D extension (flux3.cuh; validated by the
+z-extrusion cross-check against the 2D oracle, tests/test_gpu_3d.py).
+--case tgv runs the 2D analogue (4096^2, the same cell count), --case h2o2
+configs[2].  The state (5 x 144 MB per buffer) is larger than the 126 MB L2
+and every stage streams several such buffers, so no flush is needed.
 
 value   = cells x K / device time of K steps, inputs resident in HBM (CUDA
           events on the library's stream, max over ranks);
@@ -23,9 +26,9 @@ roofline = the dominant kernel class (inviscid faces) against the measured
 cpu_baseline = the CPU oracle (unmodified reference, all host cores) on a
           bounded sample of the same workload.
 
-Multi-GPU (torchrun): one rank per GPU, weak scaling.  Until the slab halo
-exchange lands each rank advances an independent replica of the per-GPU
-problem (parallelism "replicas"); no collective is on the data path.
+Multi-GPU (torchrun): one rank per GPU, weak scaling — every rank keeps a
+256^3 slab of a domain stacked along z (3D) or y (2D); g ghost planes/rows per
+side move over NCCL send/recv each stage; dt / error word / clip all-reduce.
 """
 from __future__ import annotations
 
@@ -48,6 +51,16 @@ UNIT = "cell-updates/s"
 # algorithmic FP64 ops (add+mul+div, reference's own code) per
 # cell and stage for the inviscid part of the 2D γ-gas TENO6 characteristic
 # case, and per cell-step for the whole step (TENO6 char + viscous).
+# 3D TGV (no reference path): SURVEY §8d's derived ~25 800 ops per cell-step
+# (3 face directions, nc 5); the inviscid share scaled from the 2D count by
+# the ratio of FP64 instructions the 3D and 2D face kernels execute per cell
+# and stage (ncu, profiles/r1_fp64_inst_ratio.txt).
+OPS = {  # case -> (inviscid ops per cell-stage, whole-step ops per cell)
+    "tgv": (4274, 14333),
+    "tgv3d": (None, 25800),
+    "h2o2": (None, 29738),
+}
+INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
 INVISCID_OPS_PER_CELL_STAGE = 4274
 STEP_OPS_PER_CELL = 14333
 BYTES_PER_CELL_STEP = lambda nc: 8 * (8 * nc + 6)  # noqa: E731  SURVEY §8d B_alg
@@ -119,6 +132,11 @@ def make_case(args, nslabs: int = 1):
     """nslabs > 1: weak scaling — the domain grows to n x (n*nslabs) rows so
     every GPU keeps an n x n slab (TGV: periodic copies stacked along y)."""
     from paper_2202_02319_b200 import configs
+    if args.case == "tgv3d":
+        n = args.n
+        return (configs.tgv3d(n, nz=n * nslabs),
+                f"TGV 3D {n}^3 per GPU (BASELINE configs[1]), viscous Re 1600, Ma 0.1, TENO6 "
+                "characteristic, gamma-gas, fixed dt; 3D extension (the reference is 2D-only)")
     if args.case == "h2o2":
         c = configs.h2o2_counterflow(args.n, nxy=(args.n, args.n * nslabs))
         return c, f"H2/O2 one-step counterflow flame {args.n}^2 per GPU (configs[2])"
@@ -129,7 +147,8 @@ def make_case(args, nslabs: int = 1):
 
 
 def cpu_reference_rate(n: int, target_s: float, threads: int, case: str = "tgv"):
-    """Times the CPU oracle (the unmodified reference) on an n^2 sample."""
+    """Times the CPU oracle (the unmodified reference) on an n^2 sample; for
+    the 3D TGV (no reference path) its 2D analogue, same physics and scheme."""
     from oracle import ref
     from paper_2202_02319_b200 import configs
     c = configs.tgv2d(n) if case == "tgv" else configs.h2o2_counterflow(n)
@@ -153,8 +172,8 @@ def run_reference_arm(args, rank, world):
     threads = os.cpu_count() or 1
     from oracle import ref
     from paper_2202_02319_b200 import configs
-    n = min(args.n, 1024)
-    c = configs.tgv2d(n) if args.case == "tgv" else configs.h2o2_counterflow(n)
+    n = 512 if args.case == "tgv3d" else min(args.n, 1024)
+    c = configs.h2o2_counterflow(n) if args.case == "h2o2" else configs.tgv2d(n)
     sim = ref.simulation(c.cfg, partitions=threads)
     sim.set_initial_condition(c.ic)
     sim.prepare_stage(1)
@@ -166,6 +185,9 @@ def run_reference_arm(args, rank, world):
     _, workload = make_case(args)
     sample = (f"{n}x{n} sub-problem of the same workload per step (same physics and scheme), "
               f"reference advance() loop body, {threads} threads")
+    if args.case == "tgv3d":
+        sample = (f"2D analogue {n}x{n} (the reference has no 3D path; same TGV physics, "
+                  f"TENO6 characteristic, viscous), advance() loop body, {threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
@@ -184,8 +206,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=4096)
-    ap.add_argument("--case", default="tgv", choices=["tgv", "h2o2"])
+    ap.add_argument("--n", type=int, default=None,
+                    help="cells per side (default 256 for tgv3d, 4096 tgv, 512 h2o2)")
+    ap.add_argument("--case", default="tgv3d", choices=["tgv3d", "tgv", "h2o2"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -193,6 +216,8 @@ def main():
                     help="run the NCCL slab path even with one rank (plumbing check)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.n is None:
+        args.n = {"tgv3d": 256, "tgv": 4096, "h2o2": 512}[args.case]
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     dist = None
@@ -231,7 +256,7 @@ def main():
         sim._check(native.api()["attach_nccl"](sim.handle, raw, world, rank))
     sim.set_initial_condition(case.ic)
     sim.prepare_stage(1)
-    cells = case.cfg.nx * sim.ny  # this rank's slab
+    cells = case.cfg.nx * sim.ny * max(sim.nz, 1)  # this rank's slab
     nc = sim.nc
     stream = torch.cuda.ExternalStream(sim.stream_handle(), device=local)
 
@@ -290,10 +315,16 @@ def main():
     total_prof = sum(v[0] for v in prof.values())
     dom = max(prof, key=lambda k: prof[k][0])
     f_ms, f_n = prof["faces"]
-    face_ops = cells * INVISCID_OPS_PER_CELL_STAGE  # per launch = one stage, x + y
+    inv_ops, step_ops = OPS[args.case]
+    if inv_ops is None:
+        inv_ops = INVISCID_OPS_PER_CELL_STAGE * (INVISCID_3D_OVER_2D if args.case == "tgv3d" else 1.0)
+    face_ops = cells * inv_ops  # per timed faces region = one stage, all directions
     achieved = face_ops / (f_ms / f_n / 1e3) / 1e12 if f_n else None
     roofline = {
-        "bound": "fp64", "kernel": "k_faces<x>+k_faces<y> (inviscid TENO6 characteristic)",
+        "bound": "fp64",
+        "kernel": ("k_faces3d<x,y,z>" if args.case == "tgv3d" else "k_faces3<x>+k_faces3<y>")
+                  + " (inviscid face fluxes, one stage)",
+        "ops_per_cell_stage": inv_ops,
         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
         "frac": achieved / peak.value if achieved and peak.value else None,
         "traffic": None,
@@ -301,8 +332,9 @@ def main():
         "share_of_step": f_ms / total_prof if total_prof else None,
         "peak_source": "live DFMA-chain microbenchmark (ign_probe_fp64_peak), 2 flop/FMA",
         "whole_step": {
-            "fp64_tflops": value / world * STEP_OPS_PER_CELL / 1e12,
-            "fp64_frac": value / world * STEP_OPS_PER_CELL / 1e12 / peak.value if peak.value else None,
+            "ops_per_cell_step": step_ops,
+            "fp64_tflops": value / world * step_ops / 1e12,
+            "fp64_frac": value / world * step_ops / 1e12 / peak.value if peak.value else None,
             "hbm_gbs": value / world * BYTES_PER_CELL_STEP(nc) / 1e9,
             "hbm_frac": value / world * BYTES_PER_CELL_STEP(nc) / 1e9 / 6451.8,
         },
@@ -316,8 +348,9 @@ def main():
             threads = os.cpu_count() or 1
             rate, k, el = cpu_reference_rate(512, args.cpu_seconds, threads, args.case)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"512x512 sub-problem of the same workload, {k} RK3 steps in "
-                             f"{el:.1f} s, unmodified reference via oracle/_ref, {threads} threads"}
+                   "sample": (f"512x512 {'2D analogue (no 3D reference path)' if args.case == 'tgv3d' else 'sub-problem'}"
+                              f" of the same workload, {k} RK3 steps in {el:.1f} s, unmodified "
+                              f"reference via oracle/_ref, {threads} threads")}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -331,7 +364,8 @@ def main():
             "config": {"workload": workload, "global_batch": world * cells,
                        "cells_per_gpu": cells,
                        "parallelism": f"y-slabs x{world}, NCCL halo rows" if slabs else "single",
-                       "l2": "state 4x538 MB per buffer >> 126 MB L2, no flush needed",
+                       "l2": f"state {nc} x {sim.plane * 8 / 1e6:.0f} MB per buffer >> 126 MB L2, "
+                             "no flush needed",
                        "dt": case.dt},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
                     "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
