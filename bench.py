@@ -62,6 +62,7 @@ OPS = {  # case -> (inviscid ops per cell-stage, whole-step ops per cell)
 }
 INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
 INVISCID_OPS_PER_CELL_STAGE = 4274
+TRAFFIC = {("tgv3d", 256): (1.790325 + 1.825101 + 2.307236 + 0.652938 + 0.657513 + 0.664158) * 1e9}
 STEP_OPS_PER_CELL = 14333
 BYTES_PER_CELL_STEP = lambda nc: 8 * (8 * nc + 6)  # noqa: E731  SURVEY §8d B_alg
 
@@ -327,7 +328,12 @@ def main():
         "ops_per_cell_stage": inv_ops,
         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
         "frac": achieved / peak.value if achieved and peak.value else None,
-        "traffic": None,
+        # dram read+write of the three k_faces3d launches of one stage, one
+        # ncu --set full capture at 256^3 (profiles/r1_ncu_faces3d_256.txt);
+        # algorithmic: 13 fields read + 5 face planes written per direction
+        "traffic": TRAFFIC.get((args.case, args.n)),
+        "traffic_unit": "bytes per faces region (one stage)",
+        "traffic_algorithmic": (3 * (13 + 5) * cells * 8) if args.case == "tgv3d" else None,
         "ops_per_launch": face_ops, "avg_launch_ms": f_ms / f_n if f_n else None,
         "share_of_step": f_ms / total_prof if total_prof else None,
         "peak_source": "live DFMA-chain microbenchmark (ign_probe_fp64_peak), 2 flop/FMA",
