@@ -259,7 +259,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             const double sgn = fl == 0 ? -1.0 : 1.0;
             const double Ys = S.E[EY0 + sp_i][face];
             const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
-            bool ok = true;
+            unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
                 const int t = tile_node<DIR>(g, lane, k);
@@ -268,14 +268,14 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                     const int vec = 2 * k + vu;
                     const double dp = S.L[vec][0][lane];
                     const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                    const double fd = fdiv_try(num, den, yden, ok);
+                    const double fd = fdiv_pos_try(num, den, yden, bad);
                     const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
                     const double w = ac ? fd : sh ? S.L[vec][2][lane] : qs - fd;
                     if (vu) lu[k] = w;
                     else lf[k] = w;
                 }
             }
-            if (!sh && !ok) {  // exact redo (rare): plain IEEE quotients
+            if (!sh && bad) {  // exact redo (rare): plain IEEE quotients
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
                     const int t = tile_node<DIR>(g, lane, k);

@@ -255,7 +255,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             const double Ys = S.E[F3Y0 + sp_i][face];
             const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
             double lf[W], lu[W];
-            bool ok = true;
+            unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
                 const int t = tile_node3<DIR>(g, lane, k);
@@ -264,7 +264,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                     const int vec = 2 * k + vu;
                     const double dp = S.L[vec][0][lane];
                     const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                    const double fd = fdiv_try(num, den, yden, ok);
+                    const double fd = fdiv_pos_try(num, den, yden, bad);
                     const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
                     const double wv = ac    ? fd
                                       : sh1 ? S.L[vec][2][lane]
@@ -274,7 +274,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                     else lf[k] = wv;
                 }
             }
-            if (!(sh1 || sh2) && !ok) {
+            if (!(sh1 || sh2) && bad) {
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
                     const int t = tile_node3<DIR>(g, lane, k);
