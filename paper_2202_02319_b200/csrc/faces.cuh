@@ -21,6 +21,9 @@
 // Every value is produced by the reference's own operation sequence.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <type_traits>
 
 #include "flux.cuh"
@@ -370,6 +373,14 @@ inline void launch_faces3(const KParams& P, const double* Ut, int stage, int ste
     static bool configured = false;  // per instantiation
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        if (std::getenv("IGN_DEBUG_OCC")) {
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NC * 32, smem);
+            std::fprintf(stderr, "k_faces3<NS=%d,DIR=%d>: smem %zu B, %d CTAs/SM\n", NS, DIR,
+                         smem, nb);
+        }
         configured = true;
     }
     const int NF = 32 * NC;

@@ -4,6 +4,9 @@
 // window lives in shared memory, warp w evaluates characteristic field w.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "flux3.cuh"
 #include "kernels_common.cuh"
 
@@ -21,11 +24,15 @@ template <int NS, int DIR, bool TENO> struct FaceSmem3 {
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;
     static constexpr int NT = DIR == 0 ? NF + W - 1 : 32 * (NC + W - 1);
-    static constexpr int NE = 17 + 2 * NS;
+    // eigen table rows: 12 common + Y, Theta + the direction's own (n1, n2, ut1
+    // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w)
+    static constexpr int NE = 12 + 2 * NS + (DIR < 2 ? 3 : 1);
     static constexpr int NV = 2 * W;
+    static constexpr int NVEL = DIR < 2 ? 2 : 1;  // wave speed: (u, v) or w
     double U[NC][NT];
     double F[NC][NT];
-    double u[NT], v[NT], w[NT], c[NT];
+    double vel[NVEL][NT];
+    double c[NT];
     double E[NE][NF];
     double L[NV][4][32];  // dp, dun, dut1, dut2
     double amp[NC][NF];
@@ -33,8 +40,28 @@ template <int NS, int DIR, bool TENO> struct FaceSmem3 {
 };
 
 enum : int {
-    F3N1 = 0, F3N2, F3N3, F3S, F3U, F3V, F3W, F3UN, F3UT1, F3UT2, F3K, F3H, F3C, F3C2, F3KAPPA,
-    F3YC2, F3YKAPPA, F3Y0
+    F3S = 0, F3U, F3V, F3W, F3UN, F3K, F3H, F3C, F3C2, F3KAPPA, F3YC2, F3YKAPPA, F3Y0
+};
+
+// direction-specific eigen rows (FaceSmem3::E): ut2 is w (xi/eta) or v
+// (zeta), ut1 is u for zeta faces, the off-axis normal components are 0
+template <int NS, int DIR> struct ERow {
+    static constexpr int X0 = F3Y0 + 2 * NS;
+    template <class Sm> __device__ static double n1(const Sm& S, int f) {
+        return DIR < 2 ? S.E[X0][f] : 0.0;
+    }
+    template <class Sm> __device__ static double n2(const Sm& S, int f) {
+        return DIR < 2 ? S.E[X0 + 1][f] : 0.0;
+    }
+    template <class Sm> __device__ static double n3(const Sm& S, int f) {
+        return DIR == 2 ? S.E[X0][f] : 0.0;
+    }
+    template <class Sm> __device__ static double ut1(const Sm& S, int f) {
+        return DIR < 2 ? S.E[X0 + 2][f] : S.E[F3U][f];
+    }
+    template <class Sm> __device__ static double ut2(const Sm& S, int f) {
+        return DIR < 2 ? S.E[F3W][f] : S.E[F3V][f];
+    }
 };
 
 template <int DIR> __device__ __forceinline__ int tile_node3(int g, int lane, int k) {
@@ -49,10 +76,11 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     constexpr int NV = Smem::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    // an earlier failure (error word set) ends the kernel after phase 1: the
+    // load's latency hides behind the window staging instead of stalling the
+    // CTA start (garbage phase-1 reports carry larger keys than the first one)
     __shared__ int s_dead;
-    if (threadIdx.x == 0) s_dead = failed(P.err);
-    __syncthreads();
-    if (s_dead) return;
+    const bool dead0 = threadIdx.x == 0 && failed(P.err);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // DIR 0: faces along i of row (j, k); DIR 1: columns i, face rows along j,
@@ -98,9 +126,12 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             S.U[c][t] = Uk[c];
             S.F[c][t] = Fk[c];
         }
-        S.u[t] = ldg(PU3(P) + id);
-        S.v[t] = ldg(PV3(P) + id);
-        S.w[t] = ldg(PW3(P) + id);
+        if (DIR < 2) {
+            S.vel[0][t] = ldg(PU3(P) + id);
+            S.vel[DIR < 2 ? 1 : 0][t] = ldg(PV3(P) + id);
+        } else {
+            S.vel[0][t] = ldg(PW3(P) + id);
+        }
         S.c[t] = ldg(PC3(P) + id);
     }
 
@@ -146,9 +177,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 bad = 1;
             }
             const int t = threadIdx.x;
-            const double vals[F3Y0] = {es.n1, es.n2,  es.n3,  es.s, es.u,  es.v,
-                                       es.w,  es.un,  es.ut1, es.ut2, es.k, es.H,
-                                       es.c,  es.c2,  es.kappa, es.yc2, es.ykappa};
+            const double vals[F3Y0] = {es.s, es.u,  es.v,     es.w,   es.un,     es.k,
+                                       es.H, es.c,  es.c2,    es.kappa, es.yc2, es.ykappa};
 #pragma unroll
             for (int q = 0; q < F3Y0; ++q) S.E[q][t] = vals[q];
 #pragma unroll
@@ -156,10 +186,20 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 S.E[F3Y0 + s][t] = es.Y[s];
                 S.E[F3Y0 + NS + s][t] = es.Theta[s];
             }
+            constexpr int X0 = ERow<NS, DIR>::X0;
+            if (DIR < 2) {
+                S.E[X0][t] = es.n1;
+                S.E[X0 + (DIR < 2 ? 1 : 0)][t] = es.n2;
+                S.E[X0 + (DIR < 2 ? 2 : 0)][t] = es.ut1;
+            } else {
+                S.E[X0][t] = es.n3;
+            }
         }
         S.bad[threadIdx.x] = my_active ? bad : 1;
     }
+    if (threadIdx.x == 0) s_dead = dead0;
     __syncthreads();
+    if (s_dead) return;
     if (!CHAR) {
         // componentwise LLF wave speed (solver.hpp:537-548), 3D normal velocity
         int bad = 1;
@@ -169,8 +209,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
 #pragma unroll
             for (int k = 0; k < W; ++k) {
                 const int t = tile_node3<DIR>(warp, lane, k);
-                const double un = DIR < 2 ? (m1f * S.u[t] + m2f * S.v[t]) / sf
-                                          : (m1f * S.w[t]) / sf;
+                const double un = DIR < 2 ? (m1f * S.vel[0][t] + m2f * S.vel[DIR < 2][t]) / sf
+                                          : (m1f * S.vel[0][t]) / sf;
                 alpha = smax(alpha, sf * (fabs(un) + S.c[t]));
             }
             bad = 0;
@@ -215,8 +255,9 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         // (a) field-independent parts of L q (flux.hpp:107-114 + z terms)
         const double kap = S.E[F3KAPPA][face], eu = S.E[F3U][face], ev = S.E[F3V][face],
                      ew = S.E[F3W][face];
-        const double n1 = S.E[F3N1][face], n2 = S.E[F3N2][face], n3 = S.E[F3N3][face];
-        const double un = S.E[F3UN][face], ut1 = S.E[F3UT1][face], ut2 = S.E[F3UT2][face];
+        using ER = ERow<NS, DIR>;
+        const double n1 = ER::n1(S, face), n2 = ER::n2(S, face), n3 = ER::n3(S, face);
+        const double un = S.E[F3UN][face], ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
         for (int vec = warp; vec < NV; vec += NC) {
             const int k = vec >> 1;
             const int t = tile_node3<DIR>(g, lane, k);
@@ -295,7 +336,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
 #pragma unroll
             for (int k = 0; k < W; ++k) {
                 const int t = tile_node3<DIR>(g, lane, k);
-                const double unk = DIR < 2 ? n1 * S.u[t] + n2 * S.v[t] : n3 * S.w[t];
+                const double unk =
+                    DIR < 2 ? n1 * S.vel[0][t] + n2 * S.vel[DIR < 2][t] : n3 * S.vel[0][t];
                 const double ck = S.c[t];
                 const double lam = es * (ac ? unk + sgn * ck : unk);
                 alpha = smax(alpha, fabs(lam));
@@ -336,7 +378,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         const double at1 = S.amp[NC - 3][face];
         const double at2 = S.amp[NC - 2][face];
         const double c = S.E[F3C][face];
-        const double n1 = S.E[F3N1][face], n2 = S.E[F3N2][face], n3 = S.E[F3N3][face];
+        using ER = ERow<NS, DIR>;
+        const double n1 = ER::n1(S, face), n2 = ER::n2(S, face), n3 = ER::n3(S, face);
         double r;
         if (fl < NS) {
             r = S.E[F3Y0 + fl][face] * (am + ap) + S.amp[1 + fl][face];
@@ -356,7 +399,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                             : (w - c * n3) * am + (w + c * n3) * ap + w * asum;
             } else {  // E
                 const double Hh = S.E[F3H][face], un = S.E[F3UN][face];
-                const double ut1 = S.E[F3UT1][face], ut2 = S.E[F3UT2][face];
+                const double ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
                 const double kk = S.E[F3K][face], kappa = S.E[F3KAPPA][face];
                 const double ykappa = S.E[F3YKAPPA][face];
                 double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut1 * at1;
@@ -383,6 +426,14 @@ inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int st
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        if (std::getenv("IGN_DEBUG_OCC")) {
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NC * 32, smem);
+            std::fprintf(stderr, "k_faces3d<NS=%d,DIR=%d>: smem %zu B, %d CTAs/SM\n", NS, DIR,
+                         smem, nb);
+        }
         configured = true;
     }
     const int NF = 32 * NC;
