@@ -61,7 +61,7 @@ template <int DIR> __device__ __forceinline__ int tile_node(int g, int lane, int
 
 template <int NS, int DIR, bool TENO, bool CHAR>
 #ifndef IGN_FACES_MINB
-#define IGN_FACES_MINB 1
+#define IGN_FACES_MINB 4
 #endif
 __global__ void __launch_bounds__(32 * (NS + 3), (NS == 1 ? IGN_FACES_MINB : 1))
 k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {

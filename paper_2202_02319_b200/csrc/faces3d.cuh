@@ -23,7 +23,8 @@ template <int NS, int DIR, bool TENO> struct FaceSmem3 {
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;
-    static constexpr int NT = DIR == 0 ? NF + W - 1 : 32 * (NC + W - 1);
+    // x: up to two row segments of the flattened face order (see k_faces3d)
+    static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
     // eigen table rows: 12 common + Y, Theta + the direction's own (n1, n2, ut1
     // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w)
     static constexpr int NE = 12 + 2 * NS + (DIR < 2 ? 3 : 1);
@@ -64,8 +65,15 @@ template <int NS, int DIR> struct ERow {
     }
 };
 
-template <int DIR> __device__ __forceinline__ int tile_node3(int g, int lane, int k) {
-    return DIR == 0 ? g * 32 + lane + k : (g + k) * 32 + lane;
+// window slot of stencil node k of face (g, lane); x faces past the first row
+// segment (q >= L0) sit W-1 slots further (their segment's own halo)
+template <int DIR, int W>
+__device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
+    if (DIR == 0) {
+        const int q = g * 32 + lane;
+        return q + k + (q >= L0 ? W - 1 : 0);
+    }
+    return (g + k) * 32 + lane;
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR>
@@ -83,21 +91,48 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     const bool dead0 = threadIdx.x == 0 && failed(P.err);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // DIR 0: faces along i of row (j, k); DIR 1: columns i, face rows along j,
-    // plane k; DIR 2: columns i, row j, face planes along k
+    // DIR 0: NF consecutive faces of the flattened (row, f) order, row = k ny + j,
+    // f = 0..nx — at most two row segments when nx+1 >= NF (no idle lanes at row
+    // ends), else one row segment per CTA; DIR 1: 32 columns i x NC face rows
+    // along j in plane k; DIR 2: 32 columns i of row j x NC face planes along k
     const long long step_n = DIR == 0 ? 1 : DIR == 1 ? P.sx : P.sxy;
     const int nd = DIR == 0 ? P.nx : DIR == 1 ? P.ny : P.nz;  // cells along DIR
-    const int f0 = DIR == 0 ? blockIdx.x * NF : (DIR == 1 ? blockIdx.y : blockIdx.z) * NC;
+    const int nrows = P.ny * P.nz;
+    int f0, r0 = 0, L0 = NF;
+    if (DIR == 0) {
+        if (P.nx + 1 >= NF) {
+            const long long F0 = (long long)blockIdx.x * NF;
+            r0 = (int)(F0 / (P.nx + 1));
+            f0 = (int)(F0 % (P.nx + 1));
+            L0 = min(NF, P.nx + 1 - f0);
+        } else {
+            r0 = blockIdx.z * P.ny + blockIdx.y;
+            f0 = blockIdx.x * NF;
+        }
+    } else {
+        f0 = (DIR == 1 ? blockIdx.y : blockIdx.z) * NC;
+    }
     const int i0 = blockIdx.x * 32;
-    const int jb = DIR == 0 ? blockIdx.y : DIR == 1 ? 0 : blockIdx.y;  // fixed j (DIR 0, 2)
-    const int kb = DIR == 2 ? 0 : blockIdx.z;                          // fixed k (DIR 0, 1)
+    const int jb = DIR == 2 ? blockIdx.y : 0;  // fixed j (DIR 2)
+    const int kb = DIR == 1 ? blockIdx.z : 0;  // fixed k (DIR 1)
     // metric planes: xi (DIR 0) / eta (DIR 1) use (m_x, m_y); zeta uses m_zz
     const double* m1a = DIR == 0 ? P.mxx : DIR == 1 ? P.mex : P.mzz;
     const double* m2a = DIR == 0 ? P.mxy : DIR == 1 ? P.mey : P.mzz;
-    auto node = [&](int a, int col) -> long long {  // a = index along DIR, col = i
-        if (DIR == 0) return pidx3(P, a, jb, kb);
+    // a = index along DIR; col = i (DIR 1, 2) or the flattened row (DIR 0)
+    auto node = [&](int a, int col) -> long long {
+        if (DIR == 0) return pidx3(P, a, col % P.ny, col / P.ny);
         if (DIR == 1) return pidx3(P, col, a, kb);
         return pidx3(P, col, jb, a);
+    };
+    // x face q of this CTA -> (row, f)
+    auto xface = [&](int q, int& row, int& f) {
+        if (q < L0) {
+            row = r0;
+            f = f0 + q;
+        } else {
+            row = r0 + 1;
+            f = q - L0;
+        }
     };
 
     // ---------------- phase 1a: node window -> shared memory
@@ -105,9 +140,15 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         int a, col;
         bool ok;
         if (DIR == 0) {
-            a = f0 - H + t;
-            col = 0;
-            ok = a < P.nx + P.g;
+            const int n0 = L0 + W - 1;  // window slots of the first segment
+            if (t < n0) {
+                a = f0 - H + t;
+                col = r0;
+            } else {
+                a = -H + (t - n0);
+                col = r0 + 1;
+            }
+            ok = a < P.nx + P.g && col < nrows && (t < n0 || t - n0 < NF - L0 + W - 1);
         } else {
             a = f0 - H + t / 32;
             col = i0 + t % 32;
@@ -135,17 +176,30 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         S.c[t] = ldg(PC3(P) + id);
     }
 
-    const int my_f = DIR == 0 ? f0 + threadIdx.x : f0 + warp;
-    const int my_col = DIR == 0 ? 0 : i0 + lane;
-    const bool my_active = DIR == 0 ? my_f <= P.nx : (my_col < P.nx && my_f <= nd);
+    int my_f, my_col;
+    if (DIR == 0) {
+        xface(threadIdx.x, my_col, my_f);
+    } else {
+        my_f = f0 + warp;
+        my_col = i0 + lane;
+    }
+    const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < nrows)
+                                    : (my_col < P.nx && my_f <= nd);
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;  // z faces share the y code
     auto err_index = [&](int f, int col) -> unsigned long long {
-        // face (f) of the line through (col/jb, kb): global line-major order
-        if (DIR == 0)
-            return ((unsigned long long)(kb + P.j0) * P.ny + jb) * (P.nx + 1) + f;
+        // face f of the line through col (DIR 0: flattened row k ny + j): global
+        // line-major order
+        if (DIR == 0) return ((unsigned long long)col + (unsigned long long)P.j0 * P.ny) *
+                                 (P.nx + 1) + f;
         if (DIR == 1)
             return ((unsigned long long)(kb + P.j0) * P.nx + col) * (P.ny + 1) + f;
         return ((unsigned long long)jb * P.nx + col) * (P.nz_glob + 1) + (f + P.j0);
+    };
+    // face plane offset (x: (nx+1) ny nz, y: nx (ny+1) nz, z: nx ny (nz+1))
+    auto out_index = [&](int f, int col) -> long long {
+        if (DIR == 0) return (long long)col * (P.nx + 1) + f;
+        if (DIR == 1) return ((long long)kb * (P.ny + 1) + f) * P.nx + col;
+        return ((long long)f * P.ny + jb) * P.nx + col;
     };
     const long long il = node(my_f - 1, my_col), ir = il + step_n;
     double m1f = 0.0, m2f = 0.0;
@@ -208,7 +262,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR>(warp, lane, k);
+                const int t = tile_node3<DIR, W>(warp, lane, k, L0);
                 const double un = DIR < 2 ? (m1f * S.vel[0][t] + m2f * S.vel[DIR < 2][t]) / sf
                                           : (m1f * S.vel[0][t]) / sf;
                 alpha = smax(alpha, sf * (fabs(un) + S.c[t]));
@@ -231,20 +285,22 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     const int fl = warp;
     for (int g = 0; g < NC; ++g) {
         const int face = g * 32 + lane;
-        const int f = DIR == 0 ? f0 + face : f0 + g;
-        const int col = DIR == 0 ? 0 : i0 + lane;
+        int f, col;
+        if (DIR == 0) {
+            xface(face, col, f);
+        } else {
+            f = f0 + g;
+            col = i0 + lane;
+        }
         const bool live = !S.bad[face];
-        long long o;
-        if (DIR == 0) o = ((long long)kb * P.ny + jb) * (P.nx + 1) + f;
-        else if (DIR == 1) o = ((long long)kb * (P.ny + 1) + f) * P.nx + col;
-        else o = ((long long)f * P.ny + jb) * P.nx + col;
+        const long long o = out_index(f, col);
         if (!CHAR) {
             if (live) {
                 const double alpha = S.E[0][face];
                 double wp[W], wm[W];
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int t = tile_node3<DIR>(g, lane, k);
+                    const int t = tile_node3<DIR, W>(g, lane, k, L0);
                     wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
                     wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
                 }
@@ -260,7 +316,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         const double un = S.E[F3UN][face], ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
         for (int vec = warp; vec < NV; vec += NC) {
             const int k = vec >> 1;
-            const int t = tile_node3<DIR>(g, lane, k);
+            const int t = tile_node3<DIR, W>(g, lane, k, L0);
             double q[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) q[c] = (vec & 1) ? S.U[c][t] : S.F[c][t];
@@ -299,7 +355,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR>(g, lane, k);
+                const int t = tile_node3<DIR, W>(g, lane, k, L0);
 #pragma unroll
                 for (int vu = 0; vu < 2; ++vu) {
                     const int vec = 2 * k + vu;
@@ -318,7 +374,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             if (!(sh1 || sh2) && bad) {
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int t = tile_node3<DIR>(g, lane, k);
+                    const int t = tile_node3<DIR, W>(g, lane, k, L0);
 #pragma unroll
                     for (int vu = 0; vu < 2; ++vu) {
                         const int vec = 2 * k + vu;
@@ -335,7 +391,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR>(g, lane, k);
+                const int t = tile_node3<DIR, W>(g, lane, k, L0);
                 const double unk =
                     DIR < 2 ? n1 * S.vel[0][t] + n2 * S.vel[DIR < 2][t] : n3 * S.vel[0][t];
                 const double ck = S.c[t];
@@ -367,12 +423,14 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     for (int g = 0; g < NC; ++g) {
         const int face = g * 32 + lane;
         if (S.bad[face]) continue;
-        const int f = DIR == 0 ? f0 + face : f0 + g;
-        const int col = DIR == 0 ? 0 : i0 + lane;
-        long long o;
-        if (DIR == 0) o = ((long long)kb * P.ny + jb) * (P.nx + 1) + f;
-        else if (DIR == 1) o = ((long long)kb * (P.ny + 1) + f) * P.nx + col;
-        else o = ((long long)f * P.ny + jb) * P.nx + col;
+        int f, col;
+        if (DIR == 0) {
+            xface(face, col, f);
+        } else {
+            f = f0 + g;
+            col = i0 + lane;
+        }
+        const long long o = out_index(f, col);
         const double am = S.amp[0][face];
         const double ap = S.amp[NC - 1][face];
         const double at1 = S.amp[NC - 3][face];
@@ -438,7 +496,12 @@ inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int st
     }
     const int NF = 32 * NC;
     dim3 grid;
-    if (DIR == 0) grid = dim3((P.nx + 1 + NF - 1) / NF, P.ny, P.nz);
+    if (DIR == 0) {
+        if (P.nx + 1 >= NF)  // flattened rows: (nx+1) ny nz faces in runs of NF
+            grid = dim3((unsigned)(((long long)(P.nx + 1) * P.ny * P.nz + NF - 1) / NF), 1, 1);
+        else
+            grid = dim3((P.nx + 1 + NF - 1) / NF, P.ny, P.nz);
+    }
     else if (DIR == 1) grid = dim3((P.nx + 31) / 32, (P.ny + 1 + NC - 1) / NC, P.nz);
     else grid = dim3((P.nx + 31) / 32, P.ny, (P.nz + 1 + NC - 1) / NC);
     kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step);

@@ -34,6 +34,8 @@ EXTRUDE = {
     "tgv_char_weno3z_visc": (lambda: configs.tgv2d(20, scheme="weno3z"), True, 8),
     "tgv_comp_weno3z_visc": (lambda: configs.tgv2d(20, scheme="weno3z", split="comp"), False, 8),
     "tgv_skew_char_teno6": (lambda: configs.tgv2d(24, skew=0.2), True, 6),
+    # nx + 1 >= 32 NC: the x-face kernel's flattened-row mode (segments straddle rows)
+    "tgv_wide_flat_x_teno6": (lambda: configs.tgv2d(168), True, 3),
     "ch4_react_char": (lambda: configs.reacting_ch4(20, laser=False), False, 8),
     "ch4_react_comp_weno3z": (lambda: configs.reacting_ch4(20, scheme="weno3z", split="comp",
                                                           laser=False), False, 8),
