@@ -296,6 +296,11 @@ DMix build_mix(const ign_mixture& mx) {
             p.cp_deg = q.c4 != 0.0 ? 4 : q.c3 != 0.0 ? 3 : q.c2 != 0.0 ? 2 : q.c1 != 0.0 ? 1 : 0;
             p.inv_terms = (q.cm2 != 0.0 || q.cm1 != 0.0) ? 1 : 0;
         }
+        d.simple = (a.npieces == 1 && d.pc[0].cp_deg == 0 && d.pc[0].inv_terms == 0 &&
+                    !std::signbit(d.pc[0].c0))
+                       ? 1
+                       : 0;
+        d._pad = 0;
     }
     // W-only factors of Wilke's rule (thermo.hpp:249-251), same glibc calls
     for (int i = 0; i < mx.ns; ++i)
