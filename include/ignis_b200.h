@@ -289,6 +289,35 @@ int ign_group_prepare_stage(ign_group* grp, int stage);
 int ign_group_rk3_steps(ign_group* grp, double dt, int64_t nsteps);
 int ign_group_stable_dt(ign_group* grp, double* dt);
 int ign_group_conserved_totals(ign_group* grp, double* tot);
+int ign_group_advance(ign_group* grp);
+int ign_group_write_snapshot(ign_group* grp, const char* path, int version, int with_t);
+int ign_group_read_snapshot(ign_group* grp, const char* path);
+
+/* ---- outputs (the reference's field output and diagnostics) ------------ */
+/* Simulation::add_probe (solver.hpp:130-135): inclusive interior box in
+ * global cell indices; ConfigError when out of range (2D only). */
+int ign_add_probe(ign_context* ctx, int32_t i0, int32_t j0, int32_t i1, int32_t j1);
+/* probe_interval / trace_interval (solver.hpp:71-73): advance() samples the
+ * probes and the product-fraction trace every k-th iteration (0 = off). */
+int ign_set_sampling(ign_context* ctx, int32_t probe_interval, int32_t trace_interval);
+/* ProbeSeries (solver.hpp:42-46): n samples; times[n], rows[n][5+ns] =
+ * box means of rho, u, v, p, T, Y_s.  NULL arrays: query n only. */
+int ign_probe_samples(const ign_context* ctx, int32_t probe, int64_t* n, double* times,
+                      double* rows);
+/* TraceSeries product_fraction (solver.hpp:48-51, 379-384) */
+int ign_trace_samples(const ign_context* ctx, int64_t* n, double* times, double* values);
+/* Simulation::config_hash (solver.hpp:68), carried by snapshots */
+int ign_set_config_hash(ign_context* ctx, uint64_t hash);
+int ign_get_config_hash(const ign_context* ctx, uint64_t* hash);
+/* write_snapshot (snapshot.hpp:52-76): IGNS v1, byte-identical to the
+ * reference's file for the same state (3D contexts write v2). */
+int ign_write_snapshot(ign_context* ctx, const char* path);
+/* IGNS v2 (this library): v1 + nz after ns + u32 flags after the hash; flags
+ * bit 0 appends the T cache (the Newton guess) for a bit-exact restart. */
+int ign_write_snapshot_v2(ign_context* ctx, const char* path, int with_t);
+/* read_snapshot + apply_snapshot (snapshot.hpp:78-145): v1 or v2; FormatError
+ * on bad magic / version / truncation / shape or species mismatch. */
+int ign_read_snapshot(ign_context* ctx, const char* path);
 
 #ifdef __cplusplus
 }

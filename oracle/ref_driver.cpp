@@ -441,6 +441,51 @@ int ignref_read_snapshot(ref_ctx* ctx, const char* path) {
     });
 }
 
+// probes and the product-fraction trace (solver.hpp:68-74, 130-135, 351-385)
+int ignref_add_probe(ref_ctx* ctx, int32_t i0, int32_t j0, int32_t i1, int32_t j1) {
+    return guarded(&ctx->err, [&] { ctx->sim.add_probe(ProbeSpec{i0, j0, i1, j1}); });
+}
+
+int ignref_set_sampling(ref_ctx* ctx, int32_t probe_interval, int32_t trace_interval) {
+    ctx->sim.probe_interval = probe_interval;
+    ctx->sim.trace_interval = trace_interval;
+    return IGN_OK;
+}
+
+int ignref_probe_samples(const ref_ctx* ctx, int32_t probe, int64_t* n, double* times,
+                         double* rows) {
+    if (probe < 0 || probe >= (int)ctx->sim.probes.size()) return IGN_USAGE_ERROR;
+    const auto& pr = ctx->sim.probes[probe];
+    if (n) *n = (int64_t)pr.times.size();
+    for (std::size_t k = 0; k < pr.times.size(); ++k) {
+        if (times) times[k] = pr.times[k];
+        if (rows)
+            for (std::size_t q = 0; q < pr.rows[k].size(); ++q)
+                rows[k * pr.rows[k].size() + q] = pr.rows[k][q];
+    }
+    return IGN_OK;
+}
+
+int ignref_trace_samples(const ref_ctx* ctx, int64_t* n, double* times, double* values) {
+    const auto& tr = ctx->sim.product_fraction;
+    if (n) *n = (int64_t)tr.times.size();
+    for (std::size_t k = 0; k < tr.times.size(); ++k) {
+        if (times) times[k] = tr.times[k];
+        if (values) values[k] = tr.values[k];
+    }
+    return IGN_OK;
+}
+
+int ignref_set_config_hash(ref_ctx* ctx, uint64_t hash) {
+    ctx->sim.config_hash = hash;
+    return IGN_OK;
+}
+
+int ignref_get_config_hash(const ref_ctx* ctx, uint64_t* hash) {
+    *hash = ctx->sim.config_hash;
+    return IGN_OK;
+}
+
 int64_t ignref_kernel_launches(const ref_ctx*) { return 0; }
 
 } // extern "C"

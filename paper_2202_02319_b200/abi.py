@@ -164,6 +164,15 @@ SIGNATURES = {
     "host_metrics": (_I, [C.POINTER(Config), _I, _D, C.POINTER(Error)]),
     "host_mesh": (_I, [C.POINTER(Config), _D, _D, C.POINTER(Error)]),
     "kernel_launches": (C.c_int64, [_P]),
+    # outputs: probes, trace, snapshots
+    "add_probe": (_I, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "set_sampling": (_I, [_P, C.c_int32, C.c_int32]),
+    "probe_samples": (_I, [_P, C.c_int32, C.POINTER(C.c_int64), _D, _D]),
+    "trace_samples": (_I, [_P, C.POINTER(C.c_int64), _D, _D]),
+    "set_config_hash": (_I, [_P, C.c_uint64]),
+    "get_config_hash": (_I, [_P, C.POINTER(C.c_uint64)]),
+    "write_snapshot": (_I, [_P, C.c_char_p]),
+    "read_snapshot": (_I, [_P, C.c_char_p]),
 }
 
 # measurement entry points only the B200 library has (no oracle analogue)
@@ -183,6 +192,10 @@ PRODUCT_ONLY = {
     "group_rk3_steps": (_I, [_P, C.c_double, C.c_int64]),
     "group_stable_dt": (_I, [_P, _D]),
     "group_conserved_totals": (_I, [_P, _D]),
+    "group_advance": (_I, [_P]),
+    "group_write_snapshot": (_I, [_P, C.c_char_p, _I, _I]),
+    "group_read_snapshot": (_I, [_P, C.c_char_p]),
+    "write_snapshot_v2": (_I, [_P, C.c_char_p, _I]),
 }
 IGN_NCCL_ID_BYTES = 128
 PROF_CLASSES = ("bc", "prim", "faces", "visc", "assemble", "dt", "r6", "r7")

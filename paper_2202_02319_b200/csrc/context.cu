@@ -31,6 +31,7 @@
 
 #include "host_core.hpp"
 #include "ignis_b200.h"
+#include "io.hpp"
 #include "flux3.cuh"
 #include "kernels.cuh"
 
@@ -102,6 +103,15 @@ struct ign_context {
     double *Hz = nullptr, *Hv = nullptr;  // 3D extension
     int nz = 0;                           // 0: 2D (the reference), > 0: 3D extension
     int k0 = 0, nz_glob = 0;              // 3D z-slab: first global z cell, global count
+    // outputs (solver.hpp:68-74): config hash, probes, product-fraction trace
+    uint64_t config_hash = 0;
+    int probe_interval = 0, trace_interval = 0;
+    struct Probe {
+        int i0, j0, i1, j1;  // inclusive interior box, GLOBAL indices
+        std::vector<double> times, rows;
+    };
+    std::vector<Probe> probes;
+    std::vector<double> trace_t, trace_v;
     double* inflow[4] = {nullptr, nullptr, nullptr, nullptr};
     double* wrap[2] = {nullptr, nullptr};
     ErrRec* err = nullptr;      // the word the kernels report into
@@ -1125,14 +1135,192 @@ void metrics_out(const HMetrics& m, double* out, size_t P) {
     for (int k = 0; k < 5; ++k) copy_hfield(*f[k], out + k * P);
 }
 
-// advance (solver.hpp:336-349) over a team
+// ---------------------------------------------------------------- outputs
+// sample_outputs (solver.hpp:353-385): box-averaged primitives per probe (on
+// the device, serial sums in the reference's j-major order, continued slab to
+// slab), and the product-fraction trace.  Results live on the lead context.
+void t_sample(const Team& T) {
+    ign_context* L = T.lead();
+    const bool want_probe = L->probe_interval > 0 && (L->iter % L->probe_interval == 0);
+    const bool want_trace = L->trace_interval > 0 && (L->iter % L->trace_interval == 0);
+    if (want_probe) {
+        const int nq = 5 + L->ns;
+        double* d = dalloc(2 * static_cast<size_t>(nq));
+        try {
+            for (auto& pr : L->probes) {
+                std::vector<double> row(nq, 0.0);
+                fold_ranks(T, row, [&](ign_context* c, std::vector<double>& a) {
+                    const int jlo = std::max(pr.j0, c->mesh.j0);
+                    const int jhi = std::min(pr.j1, c->mesh.j0 + c->ny - 1);
+                    if (jlo > jhi) return;
+                    cuda_check(cudaMemcpyAsync(d, a.data(), nq * 8, cudaMemcpyHostToDevice,
+                                               c->stream), "probe");
+                    launch_probe(c->prim, (long long)c->plane, c->kp.sx, c->g, c->ns, pr.i0,
+                                 jlo - c->mesh.j0, pr.i1, jhi - c->mesh.j0, d, d + nq, c->stream);
+                    c->launches += 1;
+                    cuda_check(cudaMemcpyAsync(a.data(), d + nq, nq * 8, cudaMemcpyDeviceToHost,
+                                               c->stream), "probe");
+                    cuda_check(cudaStreamSynchronize(c->stream), "probe");
+                });
+                const int n = (pr.i1 - pr.i0 + 1) * (pr.j1 - pr.j0 + 1);
+                for (auto& x : row) x /= n;
+                pr.times.push_back(L->time);
+                pr.rows.insert(pr.rows.end(), row.begin(), row.end());
+            }
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        cudaFree(d);
+    }
+    if (want_trace) {
+        L->trace_t.push_back(L->time);
+        L->trace_v.push_back(t_product_fraction(T));
+    }
+}
+
+// Global padded layers (2D rows / 3D planes) of the current state, gathered
+// on the lead (rank 0): each slab contributes its interior layers, the first
+// and last also the global edge ghosts — exactly the undecomposed planes.
+// `field` selects the source: the state components (nc planes) or the T cache.
+void t_gather(const Team& T, bool tcache, std::vector<double>& out) {
+    ign_context* L = T.lead();
+    const int N = T.local() ? (int)T.m.size() : L->nranks, g = L->g;
+    const bool three_d = L->nz > 0;
+    const size_t st = halo_stride(L);
+    const int NG = three_d ? L->nz_glob : L->mesh.ny_glob;
+    const int nf = tcache ? 1 : L->nc;
+    const size_t gplane = static_cast<size_t>(NG + 2 * g) * st;
+    if (!T.local() && L->rank != 0 && L->comm) {
+        // non-lead rank: send its layers to rank 0
+        NcclApi& n = nccl();
+        const int nl = (int)halo_count(L);
+        const int p0 = g, p1 = (L->rank == N - 1) ? nl + 2 * g : nl + g;
+        nccl_check(n.GroupStart(), "ncclGroupStart");
+        for (int c = 0; c < nf; ++c) {
+            const double* src = (tcache ? L->prim + (three_d ? 5 : 4) * L->plane
+                                        : L->S[L->cur] + c * L->plane) + p0 * st;
+            nccl_check(n.Send(src, (p1 - p0) * st, ncclFloat64, 0, L->comm, L->stream),
+                       "ncclSend(gather)");
+        }
+        nccl_check(n.GroupEnd(), "ncclGroupEnd");
+        cuda_check(cudaStreamSynchronize(L->stream), "gather");
+        return;
+    }
+    out.assign(static_cast<size_t>(nf) * gplane, 0.0);
+    double* stage = nullptr;
+    for (int r = 0; r < N; ++r) {
+        int lo, nl;
+        slab_rows(NG, N, r, lo, nl);
+        const int p0 = r == 0 ? 0 : g, p1 = r == N - 1 ? nl + 2 * g : nl + g;
+        const size_t cnt = (p1 - p0) * st;
+        for (int c = 0; c < nf; ++c) {
+            double* dst = out.data() + c * gplane + (lo + p0) * st;
+            const ign_context* m = T.local() ? T.m[r] : L;
+            if (T.local() || r == 0) {
+                const double* src = (tcache ? m->prim + (three_d ? 5 : 4) * m->plane
+                                            : m->S[m->cur] + c * m->plane) + p0 * st;
+                cuda_check(cudaMemcpy(dst, src, cnt * 8, cudaMemcpyDeviceToHost), "gather");
+            } else {
+                if (!stage) stage = dalloc(static_cast<size_t>(NG / N + 2 + 2 * g) * st);
+                NcclApi& n = nccl();
+                nccl_check(n.Recv(stage, cnt, ncclFloat64, r, L->comm, L->stream),
+                           "ncclRecv(gather)");
+                cuda_check(cudaMemcpyAsync(dst, stage, cnt * 8, cudaMemcpyDeviceToHost, L->stream),
+                           "gather");
+                cuda_check(cudaStreamSynchronize(L->stream), "gather");
+            }
+        }
+    }
+    if (stage) cudaFree(stage);
+}
+
+// write_snapshot (snapshot.hpp:52-76): version 1 = the reference's format
+// (2D); version 2 adds nz (3D) and, with `with_t`, the T cache
+void t_write_snapshot(const Team& T, const std::string& path, int version, bool with_t) {
+    ign_context* L = T.lead();
+    const bool three_d = L->nz > 0;
+    if (three_d && version < 2) throw usage_error("snapshot: 3D state needs IGNS version 2");
+    if (version != 1 && version != 2) throw usage_error("snapshot: version must be 1 or 2");
+    Snapshot s;
+    t_gather(T, false, s.state);
+    if (with_t) t_gather(T, true, s.tcache);
+    if (!T.local() && L->rank != 0 && L->comm) return;  // rank 0 writes
+    s.version = (uint32_t)version;
+    s.nx = L->nx;
+    s.ny = three_d ? L->ny : L->mesh.ny_glob;
+    s.g = L->g;
+    s.ns = L->ns;
+    s.nz = three_d ? L->nz_glob : 0;
+    for (int k = 0; k < L->ns; ++k)
+        s.species.emplace_back(L->cfg.mix.species[k].name,
+                               strnlen(L->cfg.mix.species[k].name, IGN_NAME_LEN));
+    s.time = L->time;
+    s.iteration = L->iter;
+    s.config_hash = L->config_hash;
+    s.flags = with_t ? 1u : 0u;
+    // J over the global padded rows (2D: the reference's met.jac; 3D: the
+    // extruded J of every z plane)
+    const int g = L->g, NG = s.ny;
+    if (three_d || L->nranks == 1)
+        s.jac = L->met.jac.d;  // the whole (x, y) plane already
+    else                       // 2D slabs: the global rows, global stencils
+        s.jac = jac_rows(L->mesh, inviscid_metric_mode(L->cfg), L->cfg.skew_beta, -g, NG + g);
+    snapshot_write(s, path);
+}
+
+// read_snapshot + apply_snapshot (snapshot.hpp:78-145): every slab reads the
+// file and takes its own layers; time, iteration and hash are restored, the
+// T cache too when the file carries it (v2)
+void t_read_snapshot(const Team& T, const std::string& path) {
+    ign_context* L = T.lead();
+    const Snapshot s = snapshot_read(path);
+    const bool three_d = L->nz > 0;
+    const int NG = three_d ? L->nz_glob : L->mesh.ny_glob;
+    const int sny = three_d ? L->ny : L->mesh.ny_glob;
+    if (s.nx != L->nx || s.ny != sny || s.g != L->g || s.nz != (three_d ? L->nz_glob : 0))
+        throw Error(IGN_FORMAT_ERROR,
+                    "snapshot: shape mismatch, file " + std::to_string(s.nx) + "x" +
+                        std::to_string(s.ny) + " (g=" + std::to_string(s.g) +
+                        ") vs simulation " + std::to_string(L->nx) + "x" + std::to_string(sny) +
+                        " (g=" + std::to_string(L->g) + ")");
+    if (s.ns != L->ns) throw Error(IGN_FORMAT_ERROR, "snapshot: species count mismatch");
+    for (int k = 0; k < s.ns; ++k)
+        if (s.species[k] != std::string(L->cfg.mix.species[k].name,
+                                        strnlen(L->cfg.mix.species[k].name, IGN_NAME_LEN)))
+            throw Error(IGN_FORMAT_ERROR,
+                        "snapshot: species name mismatch at slot " + std::to_string(k));
+    const size_t st = halo_stride(L);
+    const size_t gplane = static_cast<size_t>(NG + 2 * L->g) * st;
+    for (ign_context* c : T.m) {
+        const int lo = three_d ? c->k0 : c->mesh.j0;  // global interior start
+        const size_t cnt = (halo_count(c) + 2 * c->g) * st;
+        for (int comp = 0; comp < c->nc; ++comp)
+            cuda_check(cudaMemcpy(c->S[c->cur] + comp * c->plane,
+                                  s.state.data() + comp * gplane + lo * st, cnt * 8,
+                                  cudaMemcpyHostToDevice),
+                       "snapshot upload");
+        if (s.flags & 1u)
+            cuda_check(cudaMemcpy(c->prim + (three_d ? 5 : 4) * c->plane,
+                                  s.tcache.data() + lo * st, cnt * 8, cudaMemcpyHostToDevice),
+                       "snapshot upload");
+        c->time = s.time;
+        c->iter = s.iteration;
+        c->config_hash = s.config_hash;
+    }
+}
+
+// advance (solver.hpp:336-349) over a team, sampling probes and the trace
 void t_advance(const Team& T, ign_step_hook hook, void* user) {
     ign_context* L = T.lead();
     t_prepare_sync(T, 1);
+    t_sample(T);
     const ign_integrator& in = L->integ;
     const double t_eps = 1e-12 * std::max(1.0, std::abs(in.t_end));
+    const bool sampling = (L->probe_interval > 0 && !L->probes.empty()) || L->trace_interval > 0;
     if (in.fixed_dt > 0.0 && !hook) {
-        // pinned step, no hook: the step count is known up front
+        // pinned step, no hook: the step count is known up front; runs are cut
+        // at the sampling iterations
         int64_t n = 0;
         double t = L->time;
         int64_t it = L->iter;
@@ -1141,7 +1329,19 @@ void t_advance(const Team& T, ign_step_hook hook, void* user) {
             ++it;
             ++n;
         }
-        t_run_steps(T, in.fixed_dt, n, true);
+        while (n > 0) {
+            int64_t k = n;
+            if (sampling) {
+                for (int iv : {L->probe_interval, L->trace_interval}) {
+                    if (iv <= 0) continue;
+                    const int64_t to_next = iv - (L->iter % iv);
+                    k = std::min(k, to_next);
+                }
+            }
+            t_run_steps(T, in.fixed_dt, k, true);
+            n -= k;
+            if (sampling) t_sample(T);
+        }
         return;
     }
     while (L->iter < in.max_iter && L->time < in.t_end - t_eps) {
@@ -1149,6 +1349,7 @@ void t_advance(const Team& T, ign_step_hook hook, void* user) {
         if (in.fixed_dt <= 0.0) dt = smin(dt, in.t_end - L->time);
         t_run_steps(T, dt, 1, false);
         t_prepare_sync(T, 1);
+        t_sample(T);
         if (hook) hook(L, user);
     }
 }
@@ -1371,6 +1572,65 @@ int ign_advance(ign_context* ctx, ign_step_hook hook, void* user) {
     return guarded(ctx, [&] { t_advance(solo(ctx), hook, user); });
 }
 
+// ---- outputs: probes, trace, snapshots (solver.hpp:68-74, 130-135, 351-385;
+// snapshot.hpp)
+int ign_add_probe(ign_context* ctx, int32_t i0, int32_t j0, int32_t i1, int32_t j1) {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
+        if (ctx->nz > 0) throw usage_error("probes: the 3D extension has no probe boxes");
+        const int nyg = ctx->mesh.ny_glob;
+        if (i0 < 0 || j0 < 0 || i1 >= ctx->nx || j1 >= nyg || i0 > i1 || j0 > j1)
+            throw config_error("probe box out of range");
+        ctx->probes.push_back(ign_context::Probe{i0, j0, i1, j1, {}, {}});
+    });
+}
+
+int ign_set_sampling(ign_context* ctx, int32_t probe_interval, int32_t trace_interval) {
+    ctx->probe_interval = probe_interval;
+    ctx->trace_interval = trace_interval;
+    return IGN_OK;
+}
+
+int ign_probe_samples(const ign_context* ctx, int32_t probe, int64_t* n, double* times,
+                      double* rows) {
+    if (probe < 0 || probe >= (int)ctx->probes.size()) return IGN_USAGE_ERROR;
+    const auto& pr = ctx->probes[probe];
+    if (n) *n = (int64_t)pr.times.size();
+    if (times) std::memcpy(times, pr.times.data(), pr.times.size() * 8);
+    if (rows) std::memcpy(rows, pr.rows.data(), pr.rows.size() * 8);
+    return IGN_OK;
+}
+
+int ign_trace_samples(const ign_context* ctx, int64_t* n, double* times, double* values) {
+    if (n) *n = (int64_t)ctx->trace_t.size();
+    if (times) std::memcpy(times, ctx->trace_t.data(), ctx->trace_t.size() * 8);
+    if (values) std::memcpy(values, ctx->trace_v.data(), ctx->trace_v.size() * 8);
+    return IGN_OK;
+}
+
+int ign_set_config_hash(ign_context* ctx, uint64_t hash) {
+    ctx->config_hash = hash;
+    return IGN_OK;
+}
+
+int ign_get_config_hash(const ign_context* ctx, uint64_t* hash) {
+    *hash = ctx->config_hash;
+    return IGN_OK;
+}
+
+int ign_write_snapshot(ign_context* ctx, const char* path) {
+    return guarded(ctx, [&] {
+        t_write_snapshot(solo(ctx), path ? path : "", ctx->nz > 0 ? 2 : 1, false);
+    });
+}
+
+int ign_write_snapshot_v2(ign_context* ctx, const char* path, int with_t) {
+    return guarded(ctx, [&] { t_write_snapshot(solo(ctx), path ? path : "", 2, with_t != 0); });
+}
+
+int ign_read_snapshot(ign_context* ctx, const char* path) {
+    return guarded(ctx, [&] { t_read_snapshot(solo(ctx), path ? path : ""); });
+}
+
 int ign_conserved_totals(ign_context* ctx, double* tot) {
     return guarded(ctx, [&] { t_conserved_totals(solo(ctx), tot); });
 }
@@ -1515,6 +1775,20 @@ int ign_group_stable_dt(ign_group* grp, double* dt) {
 
 int ign_group_conserved_totals(ign_group* grp, double* tot) {
     return group_guarded(grp, [&](const Team& T) { t_conserved_totals(T, tot); });
+}
+
+int ign_group_advance(ign_group* grp) {
+    return group_guarded(grp, [&](const Team& T) { t_advance(T, nullptr, nullptr); });
+}
+
+int ign_group_write_snapshot(ign_group* grp, const char* path, int version, int with_t) {
+    return group_guarded(grp, [&](const Team& T) {
+        t_write_snapshot(T, path ? path : "", version, with_t != 0);
+    });
+}
+
+int ign_group_read_snapshot(ign_group* grp, const char* path) {
+    return group_guarded(grp, [&](const Team& T) { t_read_snapshot(T, path ? path : ""); });
 }
 
 }  // extern "C"

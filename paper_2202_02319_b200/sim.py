@@ -229,6 +229,54 @@ class Simulation:
     def kernel_launches(self) -> int:
         return int(self._api["kernel_launches"](self._h))
 
+    # ------------------------------------------------------------ outputs
+    def add_probe(self, i0: int, j0: int, i1: int, j1: int):
+        """Simulation::add_probe (solver.hpp:130-135), ProbeSpec{i0, j0, i1, j1}."""
+        self._check(self._api["add_probe"](self._h, i0, j0, i1, j1))
+
+    def set_sampling(self, probe_interval: int = 0, trace_interval: int = 0):
+        """probe_interval / trace_interval (solver.hpp:71-73)."""
+        self._check(self._api["set_sampling"](self._h, probe_interval, trace_interval))
+
+    def probe(self, k: int):
+        """ProbeSeries k: (times[n], rows[n, 5+ns]) — rho, u, v, p, T, Y_s box means."""
+        n = C.c_int64()
+        self._check(self._api["probe_samples"](self._h, k, C.byref(n), None, None))
+        t = np.empty(n.value)
+        r = np.empty((n.value, 5 + self.ns))
+        self._check(self._api["probe_samples"](self._h, k, C.byref(n), _dptr(t), _dptr(r)))
+        return t, r
+
+    def trace(self):
+        """product_fraction TraceSeries: (times[n], values[n])."""
+        n = C.c_int64()
+        self._check(self._api["trace_samples"](self._h, C.byref(n), None, None))
+        t, v = np.empty(n.value), np.empty(n.value)
+        self._check(self._api["trace_samples"](self._h, C.byref(n), _dptr(t), _dptr(v)))
+        return t, v
+
+    @property
+    def config_hash(self) -> int:
+        h = C.c_uint64()
+        self._check(self._api["get_config_hash"](self._h, C.byref(h)))
+        return h.value
+
+    @config_hash.setter
+    def config_hash(self, h: int):
+        self._check(self._api["set_config_hash"](self._h, h))
+
+    def write_snapshot(self, path: str):
+        """write_snapshot (snapshot.hpp:52-76), IGNS v1."""
+        self._check(self._api["write_snapshot"](self._h, str(path).encode()))
+
+    def write_snapshot_v2(self, path: str, with_t: bool = True):
+        """IGNS v2: + nz and, with_t, the T cache for a bit-exact restart."""
+        self._check(self._api["write_snapshot_v2"](self._h, str(path).encode(), int(with_t)))
+
+    def read_snapshot(self, path: str):
+        """read_snapshot + apply_snapshot (snapshot.hpp:78-145)."""
+        self._check(self._api["read_snapshot"](self._h, str(path).encode()))
+
     # ------------------------------------------------------------ measurement
     def profile_enable(self, on: bool = True):
         self._check(self._api["profile_enable"](self._h, int(on)))
@@ -313,6 +361,47 @@ class SlabGroup:
         out = np.empty(self.members[0].nc)
         self._check(self._api["group_conserved_totals"](self._g, _dptr(out)))
         return out
+
+    # advance() state and outputs live on the lead (slab 0) context
+    def lead_call(self, name, *args):
+        self._check(self.member_call(0, name, *args))
+
+    def set_integrator(self, fixed_dt=0.0, t_end=0.0, max_iter=2**63 - 1,
+                       chem_dt_limit=True, chem_dt_factor=0.1):
+        ig = abi.Integrator(fixed_dt, t_end, max_iter, int(chem_dt_limit), 0, chem_dt_factor)
+        for k in range(len(self.members)):
+            self._check(self.member_call(k, "set_integrator", C.byref(ig)))
+
+    def add_probe(self, i0, j0, i1, j1):
+        self.lead_call("add_probe", i0, j0, i1, j1)
+
+    def set_sampling(self, probe_interval=0, trace_interval=0):
+        self.lead_call("set_sampling", probe_interval, trace_interval)
+
+    def probe(self, k: int):
+        n = C.c_int64()
+        self.lead_call("probe_samples", k, C.byref(n), None, None)
+        t = np.empty(n.value)
+        r = np.empty((n.value, 5 + self.members[0].ns))
+        self.lead_call("probe_samples", k, C.byref(n), _dptr(t), _dptr(r))
+        return t, r
+
+    def trace(self):
+        n = C.c_int64()
+        self.lead_call("trace_samples", C.byref(n), None, None)
+        t, v = np.empty(n.value), np.empty(n.value)
+        self.lead_call("trace_samples", C.byref(n), _dptr(t), _dptr(v))
+        return t, v
+
+    def advance(self):
+        self._check(self._api["group_advance"](self._g))
+
+    def write_snapshot(self, path: str, version: int = 1, with_t: bool = False):
+        self._check(self._api["group_write_snapshot"](self._g, str(path).encode(), version,
+                                                       int(with_t)))
+
+    def read_snapshot(self, path: str):
+        self._check(self._api["group_read_snapshot"](self._g, str(path).encode()))
 
     def close(self):
         if getattr(self, "_g", None):
