@@ -13,6 +13,8 @@
 // Field access is by copy (get_state / set_state): the state lives on the GPU.
 #pragma once
 
+#include <cstdint>
+#include <cstdio>
 #include <functional>
 #include <stdexcept>
 #include <string>
@@ -57,14 +59,17 @@ public:
             throw_status(st, e);
         }
         ign_dims(h_, &nx_, &ny_, &g_, &ns_);
+        ign_dims3(h_, &nz_, nullptr, nullptr);
     }
     ~Simulation() { ign_destroy(h_); }
     Simulation(const Simulation&) = delete;
     Simulation& operator=(const Simulation&) = delete;
 
     int ns() const { return ns_; }
-    int ncomp() const { return ns_ + 3; }
-    size_t plane() const { return size_t(nx_ + 2 * g_) * (ny_ + 2 * g_); }
+    int ncomp() const { return ns_ + (nz_ > 0 ? 4 : 3); }
+    size_t plane() const {
+        return size_t(nx_ + 2 * g_) * (ny_ + 2 * g_) * (nz_ > 0 ? size_t(nz_ + 2 * g_) : 1);
+    }
 
     // solver.hpp:115-128
     void set_initial_condition(const std::function<ign_prim_point(double, double)>& ic) {
@@ -101,6 +106,26 @@ public:
     double time() const { double t; int64_t it; ign_get_time(h_, &t, &it); return t; }
     long iter() const { double t; int64_t it; ign_get_time(h_, &t, &it); return (long)it; }
     void set_integrator(const ign_integrator& in) { check(ign_set_integrator(h_, &in)); }
+
+    // outputs (solver.hpp:68-74, 130-135, 351-385)
+    struct ProbeSpec { int i0 = 0, j0 = 0, i1 = 0, j1 = 0; };
+    struct ProbeSeries { std::vector<double> times; std::vector<std::vector<double>> rows; };
+    void add_probe(const ProbeSpec& p) { check(ign_add_probe(h_, p.i0, p.j0, p.i1, p.j1)); }
+    void set_sampling(int probe_interval, int trace_interval) {
+        check(ign_set_sampling(h_, probe_interval, trace_interval));
+    }
+    ProbeSeries probe(int k) {
+        int64_t n = 0;
+        check(ign_probe_samples(h_, k, &n, nullptr, nullptr));
+        std::vector<double> t(n), r(n * (5 + ns_));
+        check(ign_probe_samples(h_, k, &n, t.data(), r.data()));
+        ProbeSeries ps{t, {}};
+        for (int64_t i = 0; i < n; ++i)
+            ps.rows.emplace_back(r.begin() + i * (5 + ns_), r.begin() + (i + 1) * (5 + ns_));
+        return ps;
+    }
+    std::uint64_t config_hash() const { std::uint64_t h; ign_get_config_hash(h_, &h); return h; }
+    void set_config_hash(std::uint64_t h) { check(ign_set_config_hash(h_, h)); }
     ign_context* handle() { return h_; }
 
 private:
@@ -111,7 +136,25 @@ private:
         throw_status(st, e);
     }
     ign_context* h_ = nullptr;
-    int32_t nx_ = 0, ny_ = 0, g_ = 0, ns_ = 0;
+    int32_t nx_ = 0, ny_ = 0, g_ = 0, ns_ = 0, nz_ = 0;
 };
+
+// snapshot.hpp:52-145: write_snapshot(sim, path); read_snapshot + apply_snapshot
+inline void write_snapshot(Simulation& sim, const std::string& path) {
+    const int st = ign_write_snapshot(sim.handle(), path.c_str());
+    if (st != IGN_OK) {
+        ign_error e{};
+        ign_last_error(sim.handle(), &e);
+        throw_status(st, e);
+    }
+}
+inline void read_and_apply_snapshot(Simulation& sim, const std::string& path) {
+    const int st = ign_read_snapshot(sim.handle(), path.c_str());
+    if (st != IGN_OK) {
+        ign_error e{};
+        ign_last_error(sim.handle(), &e);
+        throw_status(st, e);
+    }
+}
 
 }  // namespace ignis_b200
