@@ -293,6 +293,15 @@ int ign_group_advance(ign_group* grp);
 int ign_group_write_snapshot(ign_group* grp, const char* path, int version, int with_t);
 int ign_group_read_snapshot(ign_group* grp, const char* path);
 
+/* ---- ensemble (BASELINE configs[4]) ---------------------------------- */
+/* n independent single-GPU contexts on ONE device advanced nsteps each with
+ * their own pinned dt (rk3_steps semantics per member), launched
+ * step-interleaved on the members' streams so small members share the SMs.
+ * status[q] = member q's outcome (its message via ign_last_error); a failed
+ * member stops, the others continue.  Returns IGN_OK or a failing status. */
+int ign_ensemble_rk3_steps(ign_context** members, int n, const double* dt, int64_t nsteps,
+                           int* status);
+
 /* ---- outputs (the reference's field output and diagnostics) ------------ */
 /* Simulation::add_probe (solver.hpp:130-135): inclusive interior box in
  * global cell indices; ConfigError when out of range (2D only). */

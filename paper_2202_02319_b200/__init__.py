@@ -2,4 +2,4 @@
 solver, behind the reference's ``ignis::Simulation`` interface (C ABI in
 include/ignis_b200.h)."""
 from . import abi, configs, errors  # noqa: F401
-from .sim import Simulation  # noqa: F401
+from .sim import Ensemble, SlabGroup, Simulation  # noqa: F401

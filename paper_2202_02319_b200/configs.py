@@ -372,6 +372,19 @@ def wall_channel(n: int = 48, isothermal: bool = True, scheme: str = "teno6",
     return Case(f"wall_{n}", cfg, ic, 0.2 * (L / n) / 450.0)
 
 
+def ensemble_members(n: int = 64, *, seed: int = 1234, nxy=(500, 250), e_lo: float = 0.01,
+                     e_hi: float = 0.1, first: int = 0, count=None) -> list:
+    """BASELINE configs[4]: members of the H2/O2
+    counterflow case C on a 500 x 250 grid whose laser
+    energies are sampled U[e_lo, e_hi] with `seed`; members [first, first+count)
+    of the n-sample campaign (one GPU's share)."""
+    rng = np.random.default_rng(seed)
+    energies = rng.uniform(e_lo, e_hi, size=n)
+    count = n - first if count is None else count
+    return [h2o2_counterflow(nxy[0], nxy=nxy, energy=float(energies[k]))
+            for k in range(first, first + count)]
+
+
 def tgv3d(n: int = 256, *, viscous: bool = True, scheme: str = "teno6",
           split: str = "char", mach: float = 0.1, mu: float = 6.25e-4,
           nz=None) -> Case:

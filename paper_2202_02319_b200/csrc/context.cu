@@ -540,81 +540,138 @@ void for_all(const Team& T, const std::function<void(ign_context*)>& f) {
     for (ign_context* c : T.m) f(c);
 }
 
-// n consecutive steps; on a device failure reproduces the reference's state,
-// time/iter and last_clip at the point it would have thrown.
-void t_run_steps(const Team& T, double dt, int64_t n, bool post_prepare) {
-    if (n <= 0) return;
-    const int a0 = T.lead()->cur;
-    double t = T.lead()->time;
-    int64_t done = 0;
-    while (done < n) {
-        const int64_t chunk = std::min<int64_t>(n - done, 256);
-        for (int64_t k = 0; k < chunk; ++k) {
-            const int64_t s = done + k;
-            t_step(T, (int)((a0 + s) % 3), t, dt, (int)(s - done), post_prepare);
-            t += dt;
-        }
-        cuda_check(cudaGetLastError(), "kernel launch");
-        const DevFail f = sync_and_read(T);
-        unsigned long long red[8];
-        read_clips(T, red);
-        if (!f.any) {
-            const int last = (int)(chunk - 1);
-            const int slot = (last & 1) * 3;
-            const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
-                                       clip_of(red, slot + 2));
-            for_all(T, [&](ign_context* c) {
-                for (int64_t k = 0; k < chunk; ++k) {
-                    c->time += dt;
-                    ++c->iter;
-                }
-                c->last_clip = lc;
-                c->cur = (int)((a0 + done + chunk) % 3);
-            });
-            done += chunk;
-            continue;
-        }
-        const int64_t kk = f.step;  // failing step within this chunk
-        const int64_t k = done + kk;
-        double clip_prev = T.lead()->last_clip;
-        if (kk > 0) {
-            const int slot = ((int)(kk - 1) & 1) * 3;
-            clip_prev = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
-                                 clip_of(red, slot + 2));
-        }
-        const int ak = (int)((a0 + k) % 3);
-        const int slot = ((int)kk & 1) * 3;
-        const Error e = to_error(T.lead(), f);
-        if (f.stage == 4) {  // advance's prepare_stage(1) after a completed step
-            const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
-                                       clip_of(red, slot + 2));
-            for_all(T, [&](ign_context* c) {
-                for (int64_t q = done; q <= k; ++q) {
-                    c->time += dt;
-                    ++c->iter;
-                }
-                c->cur = (ak + 1) % 3;
-                c->last_clip = lc;
-            });
-            throw e;
-        }
-        // inside rk3_step: last_clip covers the stages that completed post_stage
-        double lc = clip_prev;
-        for (unsigned s = 1; s < f.stage; ++s)
-            lc = s == 1 ? clip_of(red, slot) : std::max(lc, clip_of(red, slot + s - 1));
-        const int cur = e.status == IGN_STEP_FAILURE ? ak  // restore U0
-                        : f.stage <= 1               ? ak
-                        : f.stage == 2               ? (ak + 1) % 3
-                                                     : (ak + 2) % 3;
+// Launch steps [done, done+chunk) of a run that started at buffer a0 and time
+// t (advanced in place); no host synchronisation.
+void t_enqueue_chunk(const Team& T, int a0, double& t, double dt, int64_t done, int64_t chunk,
+                     bool post_prepare) {
+    for (int64_t k = 0; k < chunk; ++k) {
+        const int64_t s = done + k;
+        t_step(T, (int)((a0 + s) % 3), t, dt, (int)(s - done), post_prepare);
+        t += dt;
+    }
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// Synchronise on a launched chunk and account it: time/iter/buffer/last_clip
+// advance; on a device failure reproduce the reference's state, time/iter and
+// last_clip at the point it would have thrown, then throw.
+void t_finish_chunk(const Team& T, int a0, double dt, int64_t done, int64_t chunk) {
+    const DevFail f = sync_and_read(T);
+    unsigned long long red[8];
+    read_clips(T, red);
+    if (!f.any) {
+        const int last = (int)(chunk - 1);
+        const int slot = (last & 1) * 3;
+        const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
+                                   clip_of(red, slot + 2));
         for_all(T, [&](ign_context* c) {
-            for (int64_t q = done; q < k; ++q) {
+            for (int64_t k = 0; k < chunk; ++k) {
                 c->time += dt;
                 ++c->iter;
             }
             c->last_clip = lc;
-            c->cur = cur;
+            c->cur = (int)((a0 + done + chunk) % 3);
+        });
+        return;
+    }
+    const int64_t kk = f.step;  // failing step within this chunk
+    const int64_t k = done + kk;
+    double clip_prev = T.lead()->last_clip;
+    if (kk > 0) {
+        const int slot = ((int)(kk - 1) & 1) * 3;
+        clip_prev = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
+                             clip_of(red, slot + 2));
+    }
+    const int ak = (int)((a0 + k) % 3);
+    const int slot = ((int)kk & 1) * 3;
+    const Error e = to_error(T.lead(), f);
+    if (f.stage == 4) {  // advance's prepare_stage(1) after a completed step
+        const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
+                                   clip_of(red, slot + 2));
+        for_all(T, [&](ign_context* c) {
+            for (int64_t q = done; q <= k; ++q) {
+                c->time += dt;
+                ++c->iter;
+            }
+            c->cur = (ak + 1) % 3;
+            c->last_clip = lc;
         });
         throw e;
+    }
+    // inside rk3_step: last_clip covers the stages that completed post_stage
+    double lc = clip_prev;
+    for (unsigned s = 1; s < f.stage; ++s)
+        lc = s == 1 ? clip_of(red, slot) : std::max(lc, clip_of(red, slot + s - 1));
+    const int cur = e.status == IGN_STEP_FAILURE ? ak  // restore U0
+                    : f.stage <= 1               ? ak
+                    : f.stage == 2               ? (ak + 1) % 3
+                                                 : (ak + 2) % 3;
+    for_all(T, [&](ign_context* c) {
+        for (int64_t q = done; q < k; ++q) {
+            c->time += dt;
+            ++c->iter;
+        }
+        c->last_clip = lc;
+        c->cur = cur;
+    });
+    throw e;
+}
+
+constexpr int64_t kChunk = 256;  // steps between host synchronisations
+
+// n consecutive steps (the advance() loop body with a pinned dt)
+void t_run_steps(const Team& T, double dt, int64_t n, bool post_prepare) {
+    if (n <= 0) return;
+    const int a0 = T.lead()->cur;
+    double t = T.lead()->time;
+    for (int64_t done = 0; done < n;) {
+        const int64_t chunk = std::min<int64_t>(n - done, kChunk);
+        t_enqueue_chunk(T, a0, t, dt, done, chunk, post_prepare);
+        t_finish_chunk(T, a0, dt, done, chunk);
+        done += chunk;
+    }
+}
+
+// Ensemble (BASELINE configs[4]): independent members on one GPU, each on its
+// own stream, launched step-interleaved so small members share the SMs; every
+// member keeps rk3_steps' semantics and its own failure (status per member,
+// text via ign_last_error) without stopping the others.
+void t_run_ensemble(const std::vector<ign_context*>& mem, const double* dt, int64_t n,
+                    int* status) {
+    const size_t M = mem.size();
+    std::vector<int> a0(M);
+    std::vector<double> t(M);
+    std::vector<char> live(M, 1);
+    for (size_t q = 0; q < M; ++q) {
+        a0[q] = mem[q]->cur;
+        t[q] = mem[q]->time;
+        status[q] = IGN_OK;
+    }
+    for (int64_t done = 0; done < n;) {
+        const int64_t chunk = std::min<int64_t>(n - done, kChunk);
+        for (int64_t k = 0; k < chunk; ++k)
+            for (size_t q = 0; q < M; ++q) {
+                if (!live[q]) continue;
+                try {
+                    t_step(solo(mem[q]), (int)((a0[q] + done + k) % 3), t[q], dt[q], (int)k, true);
+                    t[q] += dt[q];
+                } catch (const Error& e) {
+                    live[q] = 0;
+                    status[q] = e.status;
+                    set_error(&mem[q]->lasterr, e);
+                }
+            }
+        for (size_t q = 0; q < M; ++q) {
+            if (!live[q]) continue;
+            try {
+                t_finish_chunk(solo(mem[q]), a0[q], dt[q], done, chunk);
+            } catch (const Error& e) {
+                live[q] = 0;
+                status[q] = e.status;
+                set_error(&mem[q]->lasterr, e);
+            }
+        }
+        done += chunk;
     }
 }
 
@@ -1566,6 +1623,26 @@ int ign_rk3_step(ign_context* ctx, double dt) {
 
 int ign_rk3_steps(ign_context* ctx, double dt, int64_t n) {
     return guarded(ctx, [&] { t_run_steps(solo(ctx), dt, n, true); });
+}
+
+int ign_ensemble_rk3_steps(ign_context** members, int n, const double* dt, int64_t nsteps,
+                           int* status) {
+    if (!members || n <= 0 || !dt || !status) return IGN_USAGE_ERROR;
+    for (int q = 0; q < n; ++q)
+        if (!members[q] || members[q]->nranks > 1 || members[q]->device != members[0]->device)
+            return IGN_USAGE_ERROR;
+    try {
+        cuda_check(cudaSetDevice(members[0]->device), "cudaSetDevice");
+        t_run_ensemble(std::vector<ign_context*>(members, members + n), dt, nsteps, status);
+    } catch (const Error& e) {
+        return e.status;
+    } catch (const std::exception& e) {
+        return IGN_INTERNAL_ERROR;
+    }
+    int worst = IGN_OK;
+    for (int q = 0; q < n; ++q)
+        if (status[q] != IGN_OK) worst = status[q];
+    return worst;
 }
 
 int ign_advance(ign_context* ctx, ign_step_hook hook, void* user) {

@@ -413,3 +413,46 @@ class SlabGroup:
             self.close()
         except Exception:
             pass
+
+
+class Ensemble:
+    """Independent members on one GPU advanced together (BASELINE configs[4]):
+    ign_ensemble_rk3_steps interleaves the members' steps on their own streams.
+    Each member is a full Simulation (set_initial_condition, outputs, ...)."""
+
+    def __init__(self, cfgs, api: Optional[dict] = None):
+        from . import native
+        self._api = api or native.api()
+        self.members = [Simulation(c, self._api) for c in cfgs]
+
+    def __len__(self):
+        return len(self.members)
+
+    def rk3_steps(self, dt, n: int):
+        """n steps per member with dt (scalar or per member).  Returns the
+        per-member status list; raises the first failure's exception only when
+        every member failed (a failed member stops, the others continue)."""
+        M = len(self.members)
+        dts = np.ascontiguousarray(np.broadcast_to(np.asarray(dt, dtype=np.float64), (M,)))
+        hs = (C.c_void_p * M)(*[m.handle.value for m in self.members])
+        st = (C.c_int * M)()
+        self._api["ensemble_rk3_steps"](hs, M, _dptr(dts), n, st)
+        status = [int(x) for x in st]
+        if all(x != abi.IGN_OK for x in status):
+            self.members[0]._check(status[0])
+        return status
+
+    def error(self, k: int):
+        """The exception member k's last failure maps to (None when it is fine)."""
+        e = abi.Error()
+        self._api["last_error"](self.members[k].handle, C.byref(e))
+        if e.status == abi.IGN_OK:
+            return None
+        try:
+            raise_for(e.status, e)
+        except Exception as exc:  # noqa: BLE001 — returned, not raised
+            return exc
+
+    def close(self):
+        for m in self.members:
+            m.close()

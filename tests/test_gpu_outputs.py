@@ -174,3 +174,30 @@ def test_slab_outputs_match_single_domain(nslabs, tmp_path, cuda_device):
         assert bitwise_equal(grp2.Ut(r), single.Ut[:, lo:lo + cnt + 2 * g, :]), r
     grp.close()
     grp2.close()
+
+
+def test_ensemble_members_match_solo_runs(cuda_device):
+    """configs[4]: step-interleaved members equal their solo runs bit for bit;
+    a failing member reports its own StepFailure and the others finish."""
+    from paper_2202_02319_b200 import Ensemble
+    cases = configs.ensemble_members(5, nxy=(24, 16), first=0, count=3)
+    assert len({c.cfg.laser.energy for c in cases}) == 3
+    ens = Ensemble([clone_cfg(c.cfg) for c in cases])
+    solo = [Simulation(clone_cfg(c.cfg)) for c in cases]
+    for m, s, c in zip(ens.members, solo, cases):
+        for x in (m, s):
+            x.set_initial_condition(c.ic)
+            x.prepare_stage(1)
+    dts = [c.dt for c in cases]
+    dts[1] = 1e-2  # unstable: member 1 fails
+    status = ens.rk3_steps(dts, 6)
+    assert status[0] == status[2] == 0 and status[1] != 0
+    assert isinstance(ens.error(1), errors.IgnisError)
+    for k in (0, 2):
+        solo[k].rk3_steps(dts[k], 6)
+        assert bitwise_equal(ens.members[k].Ut, solo[k].Ut)
+        assert ens.members[k].iter == solo[k].iter == 6
+    with pytest.raises(errors.IgnisError):
+        solo[1].rk3_steps(dts[1], 6)
+    assert ens.members[1].iter == solo[1].iter
+    assert bitwise_equal(ens.members[1].Ut, solo[1].Ut)
