@@ -152,7 +152,7 @@ def cpu_reference_rate(n: int, target_s: float, threads: int, case: str = "tgv")
     the 3D TGV (no reference path) its 2D analogue, same physics and scheme."""
     from oracle import ref
     from paper_2202_02319_b200 import configs
-    c = configs.tgv2d(n) if case == "tgv" else configs.h2o2_counterflow(n)
+    c = configs.h2o2_counterflow(n) if case == "h2o2" else configs.tgv2d(n)
     sim = ref.simulation(c.cfg, partitions=threads)
     sim.set_initial_condition(c.ic)
     sim.prepare_stage(1)
@@ -201,6 +201,109 @@ def run_reference_arm(args, rank, world):
     }), flush=True)
 
 
+def run_ensemble(args, rank, world, local, dist):
+    """BASELINE configs[4]: 64 laser-ignition samples of the H2/O2 counterflow
+    case (500 x 250), `--members` per GPU (rank r takes samples [r M, r M + M)),
+    advanced together by ign_ensemble_rk3_steps; value = all members' cells x
+    steps / device time (max over member streams and ranks)."""
+    import ctypes
+    import torch
+    from paper_2202_02319_b200 import Ensemble, configs, native
+    M = args.members
+    cases = configs.ensemble_members(max(64, M * world), nxy=(args.n, args.n // 2),
+                                     first=rank * M, count=M)
+    for c in cases:
+        c.cfg.device = local
+    ens = Ensemble([c.cfg for c in cases])
+    for m, c in zip(ens.members, cases):
+        m.set_initial_condition(c.ic)
+        m.prepare_stage(1)
+    dts = [c.dt for c in cases]
+    cells = sum(c.cfg.nx * c.cfg.ny for c in cases)
+    streams = [torch.cuda.ExternalStream(m.stream_handle(), device=local) for m in ens.members]
+    ens.rk3_steps(dts, args.warmup)
+    launches0 = sum(m.kernel_launches() for m in ens.members)
+
+    def timed(fn):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ends = [torch.cuda.Event(enable_timing=True) for _ in streams]
+        torch.cuda.synchronize()
+        ev0.record(streams[0])
+        for st in streams[1:]:
+            st.wait_event(ev0)
+        fn()
+        for e, st in zip(ends, streams):
+            e.record(st)
+        torch.cuda.synchronize()
+        return max(ev0.elapsed_time(e) for e in ends)
+
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        ms = timed(lambda: ens.rk3_steps(dts, args.steps))
+        if dist:
+            dist.barrier()
+    launches = sum(m.kernel_launches() for m in ens.members) - launches0
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * cells * args.steps / (ms / 1e3)
+    # e2e: every step each member's state comes from pinned host memory and
+    # goes back (the C ABI set_state / rk3 / get_state path)
+    hosts = []
+    for m in ens.members:
+        h = torch.empty(m.nc * m.plane, dtype=torch.float64).pin_memory()
+        h.numpy()[:] = m.Ut.reshape(-1)
+        hosts.append(h)
+
+    def e2e_steps():
+        for _ in range(args.e2e_steps):
+            for m, h in zip(ens.members, hosts):
+                m.set_state(h.numpy())
+            ens.rk3_steps(dts, 1)
+            for m, h in zip(ens.members, hosts):
+                m._api["get_state"](m.handle, h.numpy().ctypes.data_as(
+                    ctypes.POINTER(ctypes.c_double)))
+    e2e_ms = timed(e2e_steps)
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    state_bytes = sum(m.nc * m.plane * 8 for m in ens.members)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            rate, k, el = cpu_reference_rate(128, args.cpu_seconds, threads, "h2o2")
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"one 128x128 member of the same H2/O2 case, {k} RK3 steps in "
+                             f"{el:.1f} s, unmodified reference via oracle/_ref"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic counterflow initial condition, sampled laser energies)",
+            "config": {"workload": f"ensemble (configs[4]): {M} members per GPU of the H2/O2 "
+                                   f"counterflow case at {args.n}x{args.n // 2}, laser energy "
+                                   "U[0.01, 0.1] seed 1234", "members_per_gpu": M,
+                       "global_batch": world * cells, "parallelism": "replicas (no collective)",
+                       "l2": "members' states stream from HBM; no flush"},
+            "e2e": {"value": world * cells * args.e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": state_bytes, "d2h_bytes_per_step": state_bytes,
+                    "steps": args.e2e_steps},
+            "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clk.summary(),
+        }), flush=True)
+    ens.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -209,7 +312,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=None,
                     help="cells per side (default 256 for tgv3d, 4096 tgv, 512 h2o2)")
-    ap.add_argument("--case", default="tgv3d", choices=["tgv3d", "tgv", "h2o2"])
+    ap.add_argument("--case", default="tgv3d", choices=["tgv3d", "tgv", "h2o2", "ensemble"])
+    ap.add_argument("--members", type=int, default=8, help="ensemble members per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -218,7 +322,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.n is None:
-        args.n = {"tgv3d": 256, "tgv": 4096, "h2o2": 512}[args.case]
+        args.n = {"tgv3d": 256, "tgv": 4096, "h2o2": 512, "ensemble": 500}[args.case]
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     dist = None
@@ -236,6 +340,9 @@ def main():
     import torch
     torch.cuda.set_device(local)
     from paper_2202_02319_b200 import Simulation, native
+    if args.case == "ensemble":
+        run_ensemble(args, rank, world, local, dist)
+        return
 
     slabs = world > 1 or args.force_slabs
     case, workload = make_case(args, world)
