@@ -152,7 +152,10 @@ def cpu_reference_rate(n: int, target_s: float, threads: int, case: str = "tgv")
     the 3D TGV (no reference path) its 2D analogue, same physics and scheme."""
     from oracle import ref
     from paper_2202_02319_b200 import configs
-    c = configs.h2o2_counterflow(n) if case == "h2o2" else configs.tgv2d(n)
+    if case == "ensemble":  # one member of the campaign (moderate laser energy)
+        c = configs.ensemble_members(64, nxy=(n, n // 2), count=1)[0]
+    else:
+        c = configs.h2o2_counterflow(n) if case == "h2o2" else configs.tgv2d(n)
     sim = ref.simulation(c.cfg, partitions=threads)
     sim.set_initial_condition(c.ic)
     sim.prepare_stage(1)
@@ -163,7 +166,7 @@ def cpu_reference_rate(n: int, target_s: float, threads: int, case: str = "tgv")
     t0 = time.perf_counter()
     sim.rk3_steps(c.dt, k)
     el = time.perf_counter() - t0
-    return n * n * k / el, k, el
+    return c.cfg.nx * c.cfg.ny * k / el, k, el
 
 
 def run_reference_arm(args, rank, world):
@@ -174,7 +177,10 @@ def run_reference_arm(args, rank, world):
     from oracle import ref
     from paper_2202_02319_b200 import configs
     n = 512 if args.case == "tgv3d" else min(args.n, 1024)
-    c = configs.h2o2_counterflow(n) if args.case == "h2o2" else configs.tgv2d(n)
+    if args.case == "ensemble":  # one member of the campaign, full size
+        c = configs.ensemble_members(64, nxy=(args.n, args.n // 2), count=1)[0]
+    else:
+        c = configs.h2o2_counterflow(n) if args.case == "h2o2" else configs.tgv2d(n)
     sim = ref.simulation(c.cfg, partitions=threads)
     sim.set_initial_condition(c.ic)
     sim.prepare_stage(1)
@@ -182,10 +188,12 @@ def run_reference_arm(args, rank, world):
     t0 = time.perf_counter()
     sim.rk3_steps(c.dt, args.steps)
     el = time.perf_counter() - t0
-    rate = n * n * args.steps / el
-    _, workload = make_case(args)
-    sample = (f"{n}x{n} sub-problem of the same workload per step (same physics and scheme), "
-              f"reference advance() loop body, {threads} threads")
+    cells = c.cfg.nx * c.cfg.ny
+    rate = cells * args.steps / el
+    workload = (f"ensemble (configs[4]) member, H2/O2 counterflow {c.cfg.nx}x{c.cfg.ny}"
+                if args.case == "ensemble" else make_case(args)[1])
+    sample = (f"{c.cfg.nx}x{c.cfg.ny} sub-problem of the same workload per step (same physics "
+              f"and scheme), reference advance() loop body, {threads} threads")
     if args.case == "tgv3d":
         sample = (f"2D analogue {n}x{n} (the reference has no 3D path; same TGV physics, "
                   f"TENO6 characteristic, viscous), advance() loop body, {threads} threads")
@@ -194,7 +202,7 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload, "global_batch": n * n, "parallelism": "cpu-threads"},
+        "config": {"workload": workload, "global_batch": cells, "parallelism": "cpu-threads"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -275,9 +283,9 @@ def run_ensemble(args, rank, world, local, dist):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             threads = os.cpu_count() or 1
-            rate, k, el = cpu_reference_rate(128, args.cpu_seconds, threads, "h2o2")
+            rate, k, el = cpu_reference_rate(128, args.cpu_seconds, threads, "ensemble")
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"one 128x128 member of the same H2/O2 case, {k} RK3 steps in "
+                   "sample": f"one 128x64 member of the same campaign, {k} RK3 steps in "
                              f"{el:.1f} s, unmodified reference via oracle/_ref"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
