@@ -135,6 +135,53 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         }
     };
 
+    int my_f, my_col;
+    if (DIR == 0) {
+        xface(threadIdx.x, my_col, my_f);
+    } else {
+        my_f = f0 + warp;
+        my_col = i0 + lane;
+    }
+    const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < nrows)
+                                    : (my_col < P.nx && my_f <= nd);
+    const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;  // z faces share the y code
+    auto err_index = [&](int f, int col) -> unsigned long long {
+        // face f of the line through col (DIR 0: flattened row k ny + j): global
+        // line-major order
+        if (DIR == 0) return ((unsigned long long)col + (unsigned long long)P.j0 * P.ny) *
+                                 (P.nx + 1) + f;
+        if (DIR == 1)
+            return ((unsigned long long)(kb + P.j0) * P.nx + col) * (P.ny + 1) + f;
+        return ((unsigned long long)jb * P.nx + col) * (P.nz_glob + 1) + (f + P.j0);
+    };
+    // face plane offset (x: (nx+1) ny nz, y: nx (ny+1) nz, z: nx ny (nz+1))
+    auto out_index = [&](int f, int col) -> long long {
+        if (DIR == 0) return (long long)col * (P.nx + 1) + f;
+        if (DIR == 1) return ((long long)kb * (P.ny + 1) + f) * P.nx + col;
+        return ((long long)f * P.ny + jb) * P.nx + col;
+    };
+    const long long il = node(my_f - 1, my_col), ir = il + step_n;
+    double m1f = 0.0, m2f = 0.0;
+    if (my_active) {
+        const long long l2 = il % P.sxy, r2 = ir % P.sxy;
+        m1f = 0.5 * (ldg(m1a + l2) + ldg(m1a + r2));
+        m2f = 0.5 * (ldg(m2a + l2) + ldg(m2a + r2));
+    }
+    // this thread's face state, loaded before the window staging so the
+    // global-load latency overlaps it (phase 1 consumes it after the loop)
+    double pl[5], pr[5], Yl[NS], Yr[NS];
+    if (CHAR && my_active) {
+        pl[0] = ldg(PRHO3(P) + il), pl[1] = ldg(PT3(P) + il), pl[2] = ldg(PU3(P) + il);
+        pl[3] = ldg(PV3(P) + il), pl[4] = ldg(PW3(P) + il);
+        pr[0] = ldg(PRHO3(P) + ir), pr[1] = ldg(PT3(P) + ir), pr[2] = ldg(PU3(P) + ir);
+        pr[3] = ldg(PV3(P) + ir), pr[4] = ldg(PW3(P) + ir);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            Yl[s] = ldg(PY3(P, s) + il);
+            Yr[s] = ldg(PY3(P, s) + ir);
+        }
+    }
+
     // ---------------- phase 1a: node window -> shared memory
     for (int t = threadIdx.x; t < NT; t += blockDim.x) {
         int a, col;
@@ -176,53 +223,13 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         S.c[t] = ldg(PC3(P) + id);
     }
 
-    int my_f, my_col;
-    if (DIR == 0) {
-        xface(threadIdx.x, my_col, my_f);
-    } else {
-        my_f = f0 + warp;
-        my_col = i0 + lane;
-    }
-    const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < nrows)
-                                    : (my_col < P.nx && my_f <= nd);
-    const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;  // z faces share the y code
-    auto err_index = [&](int f, int col) -> unsigned long long {
-        // face f of the line through col (DIR 0: flattened row k ny + j): global
-        // line-major order
-        if (DIR == 0) return ((unsigned long long)col + (unsigned long long)P.j0 * P.ny) *
-                                 (P.nx + 1) + f;
-        if (DIR == 1)
-            return ((unsigned long long)(kb + P.j0) * P.nx + col) * (P.ny + 1) + f;
-        return ((unsigned long long)jb * P.nx + col) * (P.nz_glob + 1) + (f + P.j0);
-    };
-    // face plane offset (x: (nx+1) ny nz, y: nx (ny+1) nz, z: nx ny (nz+1))
-    auto out_index = [&](int f, int col) -> long long {
-        if (DIR == 0) return (long long)col * (P.nx + 1) + f;
-        if (DIR == 1) return ((long long)kb * (P.ny + 1) + f) * P.nx + col;
-        return ((long long)f * P.ny + jb) * P.nx + col;
-    };
-    const long long il = node(my_f - 1, my_col), ir = il + step_n;
-    double m1f = 0.0, m2f = 0.0;
-    if (my_active) {
-        const long long l2 = il % P.sxy, r2 = ir % P.sxy;
-        m1f = 0.5 * (ldg(m1a + l2) + ldg(m1a + r2));
-        m2f = 0.5 * (ldg(m2a + l2) + ldg(m2a + r2));
-    }
-
     if (CHAR) {
         int bad = 0;
         if (my_active) {
-            double Yl[NS], Yr[NS], Ya[NS];
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                Yl[s] = ldg(PY3(P, s) + il);
-                Yr[s] = ldg(PY3(P, s) + ir);
-            }
+            double Ya[NS];
             double Ta, ua, va, wa;
-            roe_average3<NS>(ldg(PRHO3(P) + il), Yl, ldg(PT3(P) + il), ldg(PU3(P) + il),
-                             ldg(PV3(P) + il), ldg(PW3(P) + il), ldg(PRHO3(P) + ir), Yr,
-                             ldg(PT3(P) + ir), ldg(PU3(P) + ir), ldg(PV3(P) + ir),
-                             ldg(PW3(P) + ir), P.mix, Ya, Ta, ua, va, wa);
+            roe_average3<NS>(pl[0], Yl, pl[1], pl[2], pl[3], pl[4], pr[0], Yr, pr[1], pr[2],
+                             pr[3], pr[4], P.mix, Ya, Ta, ua, va, wa);
             Eigen3<NS> es;
             const int est = eigen_at_state3<NS, DIR == 2 ? 2 : 0>(Ya, Ta, ua, va, wa, m1f, m2f,
                                                                   P.mix, es);
