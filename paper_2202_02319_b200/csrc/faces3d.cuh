@@ -37,6 +37,7 @@ template <int NS, int DIR, bool TENO> struct FaceSmem3 {
     double E[NE][NF];
     double L[NV][4][32];  // dp, dun, dut1, dut2
     double amp[NC][NF];
+    double alpha[3][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
     int bad[NF];
 };
 
@@ -321,6 +322,26 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         using ER = ERow<NS, DIR>;
         const double n1 = ER::n1(S, face), n2 = ER::n2(S, face), n3 = ER::n3(S, face);
         const double un = S.E[F3UN][face], ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
+        // (kap eu) q_u etc.: the reference's left-to-right products, hoisted
+        const double keu = kap * eu, kev = kap * ev, kew = kap * ew;
+        // the three distinct LLF wave speeds of the face (solver.hpp:555-566;
+        // the convective one serves every species and shear field), by the
+        // warps with the fewest projection vectors
+        if (warp >= NC - 3 && !S.bad[face]) {
+            const int kind = NC - 1 - warp;  // 0: un - c, 1: un, 2: un + c
+            const double es = S.E[F3S][face];
+            double alpha = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node3<DIR, W>(g, lane, k, L0);
+                const double unk =
+                    DIR < 2 ? n1 * S.vel[0][t] + n2 * S.vel[DIR < 2][t] : n3 * S.vel[0][t];
+                const double ck = S.c[t];
+                const double lam = es * (kind == 0 ? unk + -1.0 * ck : kind == 2 ? unk + ck : unk);
+                alpha = smax(alpha, fabs(lam));
+            }
+            S.alpha[kind][lane] = alpha;
+        }
         for (int vec = warp; vec < NV; vec += NC) {
             const int k = vec >> 1;
             const int t = tile_node3<DIR, W>(g, lane, k, L0);
@@ -330,8 +351,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             double drho = 0.0;
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) drho += q[sp];
-            double dp = kap * q[NS + 3] - kap * eu * q[NS] - kap * ev * q[NS + 1] -
-                        kap * ew * q[NS + 2];
+            double dp = kap * q[NS + 3] - keu * q[NS] - kev * q[NS + 1] - kew * q[NS + 2];
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) dp += S.E[F3Y0 + NS + sp][face] * q[sp];
             S.L[vec][0][lane] = dp;
@@ -359,26 +379,14 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             const double Ys = S.E[F3Y0 + sp_i][face];
             const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
             double lf[W], lu[W];
-            unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
+            if (sh1 || sh2) {
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR, W>(g, lane, k, L0);
-#pragma unroll
-                for (int vu = 0; vu < 2; ++vu) {
-                    const int vec = 2 * k + vu;
-                    const double dp = S.L[vec][0][lane];
-                    const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                    const double fd = fdiv_pos_try(num, den, yden, bad);
-                    const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
-                    const double wv = ac    ? fd
-                                      : sh1 ? S.L[vec][2][lane]
-                                      : sh2 ? S.L[vec][3][lane]
-                                            : qs - fd;
-                    if (vu) lu[k] = wv;
-                    else lf[k] = wv;
+                for (int k = 0; k < W; ++k) {
+                    lf[k] = S.L[2 * k][sh1 ? 2 : 3][lane];
+                    lu[k] = S.L[2 * k + 1][sh1 ? 2 : 3][lane];
                 }
-            }
-            if (!(sh1 || sh2) && bad) {
+            } else {
+                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
                     const int t = tile_node3<DIR, W>(g, lane, k, L0);
@@ -387,24 +395,33 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                         const int vec = 2 * k + vu;
                         const double dp = S.L[vec][0][lane];
                         const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                        const double fd = div_cold(num, den);
+                        const double fd = fdiv_pos_try(num, den, yden, bad);
                         const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
                         const double wv = ac ? fd : qs - fd;
                         if (vu) lu[k] = wv;
                         else lf[k] = wv;
                     }
                 }
-            }
-            double alpha = 0.0;
+                if (bad) {
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR, W>(g, lane, k, L0);
-                const double unk =
-                    DIR < 2 ? n1 * S.vel[0][t] + n2 * S.vel[DIR < 2][t] : n3 * S.vel[0][t];
-                const double ck = S.c[t];
-                const double lam = es * (ac ? unk + sgn * ck : unk);
-                alpha = smax(alpha, fabs(lam));
+                    for (int k = 0; k < W; ++k) {
+                        const int t = tile_node3<DIR, W>(g, lane, k, L0);
+#pragma unroll
+                        for (int vu = 0; vu < 2; ++vu) {
+                            const int vec = 2 * k + vu;
+                            const double dp = S.L[vec][0][lane];
+                            const double num =
+                                ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
+                            const double fd = div_cold(num, den);
+                            const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
+                            const double wv = ac ? fd : qs - fd;
+                            if (vu) lu[k] = wv;
+                            else lf[k] = wv;
+                        }
+                    }
+                }
             }
+            const double alpha = S.alpha[fl == 0 ? 0 : fl == NC - 1 ? 2 : 1][lane];
             if (!isfinite(alpha)) {
                 report(P.err, stage, phase, err_index(f, col), 1, step);
             } else {
