@@ -45,6 +45,7 @@ template <int NS, int DIR, bool TENO> struct FaceSmem {
     double E[NE][NF];         // eigen data per face (char); [0] alpha, [1] sf (comp)
     double L[NV][3][32];      // dp, dun, dut of one group's vectors
     double amp[NC][NF];
+    double alpha[3][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
     int bad[NF];
 };
 
@@ -70,10 +71,11 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     constexpr int NV = Smem::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-    __shared__ int s_dead;  // one read of the error word per CTA keeps exits uniform
-    if (threadIdx.x == 0) s_dead = failed(P.err);
-    __syncthreads();
-    if (s_dead) return;
+    // an earlier failure (error word set) ends the kernel after phase 1: the
+    // load's latency hides behind the window staging (garbage phase-1 reports
+    // carry larger keys than the first one)
+    __shared__ int s_dead;
+    const bool dead0 = threadIdx.x == 0 && failed(P.err);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long step_n = DIR == 0 ? 1 : P.sx;
@@ -174,7 +176,9 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         }
         S.bad[threadIdx.x] = my_active ? bad : 1;
     }
+    if (threadIdx.x == 0) s_dead = dead0;
     __syncthreads();
+    if (s_dead) return;
     if (!CHAR) {
         // ---------------- phase 1b (comp): LLF wave speed of my face (solver.hpp:537-548)
         int bad = 1;
@@ -226,6 +230,24 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         const double kap = S.E[EKAPPA][face], eu = S.E[EU][face], ev = S.E[EV][face];
         const double n1 = S.E[EN1][face], n2 = S.E[EN2][face];
         const double un = S.E[EUN][face], ut = S.E[EUT][face];
+        // (kap eu) q_u: the reference's left-to-right products, hoisted
+        const double keu = kap * eu, kev = kap * ev;
+        // the three distinct LLF wave speeds of the face (EigenSystem::field_speed,
+        // flux.hpp:143-147; the convective one serves species and shear fields)
+        if (warp >= NC - 3 && !S.bad[face]) {
+            const int kind = NC - 1 - warp;  // 0: un - c, 1: un, 2: un + c
+            const double es = S.E[ES][face];
+            double alpha = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node<DIR>(g, lane, k);
+                const double unk = n1 * S.u[t] + n2 * S.v[t];
+                const double ck = S.c[t];
+                const double lam = es * (kind == 0 ? unk + -1.0 * ck : kind == 2 ? unk + ck : unk);
+                alpha = smax(alpha, fabs(lam));
+            }
+            S.alpha[kind][lane] = alpha;
+        }
         for (int vec = warp; vec < NV; vec += NC) {
             const int k = vec >> 1;
             const int t = tile_node<DIR>(g, lane, k);
@@ -235,7 +257,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             double drho = 0.0;
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) drho += q[sp];
-            double dp = kap * q[NS + 2] - kap * eu * q[NS] - kap * ev * q[NS + 1];
+            double dp = kap * q[NS + 2] - keu * q[NS] - kev * q[NS + 1];
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) dp += S.E[EY0 + NS + sp][face] * q[sp];
             S.L[vec][0][lane] = dp;
@@ -246,7 +268,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         // (b) row fl of L on the stencil, wave speed, split, reconstruction
         double amp = 0.0;
         if (live) {
-            const double es = S.E[ES][face], ec = S.E[EC][face];
+            const double ec = S.E[EC][face];
             const double c2 = S.E[EC2][face], yc2 = S.E[EYC2][face];
             // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
             const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
@@ -262,23 +284,14 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             const double sgn = fl == 0 ? -1.0 : 1.0;
             const double Ys = S.E[EY0 + sp_i][face];
             const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
-            unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
+            if (sh) {
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const int t = tile_node<DIR>(g, lane, k);
-#pragma unroll
-                for (int vu = 0; vu < 2; ++vu) {
-                    const int vec = 2 * k + vu;
-                    const double dp = S.L[vec][0][lane];
-                    const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                    const double fd = fdiv_pos_try(num, den, yden, bad);
-                    const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
-                    const double w = ac ? fd : sh ? S.L[vec][2][lane] : qs - fd;
-                    if (vu) lu[k] = w;
-                    else lf[k] = w;
+                for (int k = 0; k < W; ++k) {
+                    lf[k] = S.L[2 * k][2][lane];
+                    lu[k] = S.L[2 * k + 1][2][lane];
                 }
-            }
-            if (!sh && bad) {  // exact redo (rare): plain IEEE quotients
+            } else {
+                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
                     const int t = tile_node<DIR>(g, lane, k);
@@ -287,24 +300,34 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                         const int vec = 2 * k + vu;
                         const double dp = S.L[vec][0][lane];
                         const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                        const double fd = div_cold(num, den);
+                        const double fd = fdiv_pos_try(num, den, yden, bad);
                         const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
                         const double w = ac ? fd : qs - fd;
                         if (vu) lu[k] = w;
                         else lf[k] = w;
                     }
                 }
-            }
-            // EigenSystem::field_speed at each node's normal velocity (flux.hpp:143-147)
-            double alpha = 0.0;
+                if (bad) {  // exact redo (rare): plain IEEE quotients
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const int t = tile_node<DIR>(g, lane, k);
-                const double unk = n1 * S.u[t] + n2 * S.v[t];
-                const double ck = S.c[t];
-                const double lam = es * (ac ? unk + sgn * ck : unk);
-                alpha = smax(alpha, fabs(lam));
+                    for (int k = 0; k < W; ++k) {
+                        const int t = tile_node<DIR>(g, lane, k);
+#pragma unroll
+                        for (int vu = 0; vu < 2; ++vu) {
+                            const int vec = 2 * k + vu;
+                            const double dp = S.L[vec][0][lane];
+                            const double num =
+                                ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
+                            const double fd = div_cold(num, den);
+                            const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
+                            const double w = ac ? fd : qs - fd;
+                            if (vu) lu[k] = w;
+                            else lf[k] = w;
+                        }
+                    }
+                }
             }
+            // EigenSystem::field_speed (flux.hpp:143-147), computed once per kind
+            const double alpha = S.alpha[fl == 0 ? 0 : fl == NC - 1 ? 2 : 1][lane];
             if (!isfinite(alpha)) {
                 report(P.err, stage, phase, err_index(f, col), 1, step);
             } else {

@@ -369,7 +369,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         // (b) row fl of L, wave speed, LLF split, reconstruction
         double amp = 0.0;
         if (live) {
-            const double es = S.E[F3S][face], ec = S.E[F3C][face];
+            const double ec = S.E[F3C][face];
             const double c2 = S.E[F3C2][face], yc2 = S.E[F3YC2][face];
             const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
             const bool ac = fl == 0 || fl == NC - 1;
