@@ -103,14 +103,15 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         double Uk[NC], Fk[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
-        mapped_flux<NS>(Uk, ldg(PP(P) + id), ldg(m1a + id), ldg(m2a + id), Fk);
+        const double nu = ldg(PU(P) + id), nv = ldg(PV(P) + id);
+        mapped_flux_uv<NS>(Uk, ldg(PP(P) + id), nu, nv, ldg(m1a + id), ldg(m2a + id), Fk);
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             S.U[c][t] = Uk[c];
             S.F[c][t] = Fk[c];
         }
-        S.u[t] = ldg(PU(P) + id);
-        S.v[t] = ldg(PV(P) + id);
+        S.u[t] = nu;
+        S.v[t] = nv;
         S.c[t] = ldg(PC(P) + id);
     }
 

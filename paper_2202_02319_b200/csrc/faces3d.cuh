@@ -209,17 +209,19 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         double Uk[NC], Fk[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
-        mapped_flux3<NS, DIR>(Uk, ldg(PP3(P) + id), ldg(m1a + id2), ldg(m2a + id2), Fk);
+        const double nu = ldg(PU3(P) + id), nv = ldg(PV3(P) + id), nw = ldg(PW3(P) + id);
+        mapped_flux3<NS, DIR>(Uk, ldg(PP3(P) + id), nu, nv, nw, ldg(m1a + id2), ldg(m2a + id2),
+                              Fk);
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             S.U[c][t] = Uk[c];
             S.F[c][t] = Fk[c];
         }
         if (DIR < 2) {
-            S.vel[0][t] = ldg(PU3(P) + id);
-            S.vel[DIR < 2 ? 1 : 0][t] = ldg(PV3(P) + id);
+            S.vel[0][t] = nu;
+            S.vel[DIR < 2 ? 1 : 0][t] = nv;
         } else {
-            S.vel[0][t] = ldg(PW3(P) + id);
+            S.vel[0][t] = nw;
         }
         S.c[t] = ldg(PC3(P) + id);
     }

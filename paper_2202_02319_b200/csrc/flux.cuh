@@ -22,6 +22,21 @@ IGN_HD void mapped_flux(const double* U, double p, double m1, double m2, double*
     Ft[NS + 2] = (U[NS + 2] + p) * uhat;
 }
 
+// mapped_flux with the velocity quotients supplied: u = U[NS]/rho and
+// v = U[NS+1]/rho are exactly the primitive cache's u, v (primitives_from_
+// conservative divides the same U by the same rho, correctly rounded), so the
+// face kernels skip two IEEE divisions per node
+template <int NS>
+IGN_HD void mapped_flux_uv(const double* U, double p, double u, double v, double m1, double m2,
+                           double* Ft) {
+    const double uhat = m1 * u + m2 * v;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) Ft[s] = U[s] * uhat;
+    Ft[NS] = U[NS] * uhat + m1 * p;
+    Ft[NS + 1] = U[NS + 1] * uhat + m2 * p;
+    Ft[NS + 2] = (U[NS + 2] + p) * uhat;
+}
+
 // roe_average (flux.hpp:157-186): returns Y, T, u, v of the face state
 template <int NS>
 IGN_HD void roe_average(double rho_l, const double* Yl, double Tl, double ul, double vl,

@@ -61,14 +61,13 @@ IGN_HD int primitives_from_conservative3(const double* U, const DMix& m, double 
     return P_OK;
 }
 
-// mapped_flux (flux.hpp:39-50); DIR < 2: (m1, m2, 0), DIR 2: (0, 0, m3)
+// mapped_flux (flux.hpp:39-50); DIR < 2: (m1, m2, 0), DIR 2: (0, 0, m3).
+// u, v, w are the cache's velocities, i.e. exactly U[NS..NS+2] / rho
+// (see mapped_flux_uv)
 template <int NS, int DIR>
-IGN_HD void mapped_flux3(const double* U, double p, double m1, double m2, double* Ft) {
-    double rho = 0.0;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) rho += U[s];
-    const double uhat = DIR < 2 ? m1 * (U[NS] / rho) + m2 * (U[NS + 1] / rho)
-                                : m1 * (U[NS + 2] / rho);
+IGN_HD void mapped_flux3(const double* U, double p, double u, double v, double w, double m1,
+                         double m2, double* Ft) {
+    const double uhat = DIR < 2 ? m1 * u + m2 * v : m1 * w;
 #pragma unroll
     for (int s = 0; s < NS; ++s) Ft[s] = U[s] * uhat;
     if (DIR < 2) {

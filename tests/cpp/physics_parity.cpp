@@ -158,6 +158,14 @@ static void check_mixture(const ignis::MixtureModel& mix, const char* name, unsi
         ign::mapped_flux<NS>(q, back.p, m1, m2, F1);
         ignis::mapped_flux(q, back.p, m1, m2, ignis::CompIndex{NS}, F2);
         for (int c = 0; c < NS + 3; ++c) EXPECT_BITWISE("mapped_flux", F1[c], F2[c]);
+        // the face kernels' form: velocities from the primitive path's quotients
+        double rq = 0.0;
+        for (int s = 0; s < NS; ++s) rq += q[s];
+        const double yq = 1.0 / rq;
+        double F3[NS + 3];
+        ign::mapped_flux_uv<NS>(q, back.p, ign::fdiv(q[NS], rq, yq), ign::fdiv(q[NS + 1], rq, yq),
+                                m1, m2, F3);
+        for (int c = 0; c < NS + 3; ++c) EXPECT_BITWISE("mapped_flux_uv", F3[c], F2[c]);
     }
 }
 
