@@ -58,8 +58,8 @@ UNIT = "cell-updates/s"
 OPS = {  # case -> (inviscid ops per cell-stage, whole-step ops per cell)
     "tgv": (4274, 14333),
     "tgv3d": (None, 25800),
-    "h2o2": (None, 29738),
-}
+    "h2o2": (7515, 29738),      # inviscid: 4274 x 1.758 (4-species faces / gamma-gas
+}                               # faces FP64 instructions per cell-stage, ncu, 512^2)
 INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
 INVISCID_OPS_PER_CELL_STAGE = 4274
 TRAFFIC = {("tgv3d", 256): (1.790325 + 1.825101 + 2.307236 + 0.652938 + 0.657513 + 0.664158) * 1e9}

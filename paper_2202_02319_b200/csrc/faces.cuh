@@ -36,7 +36,8 @@ template <int NS, int DIR, bool TENO> struct FaceSmem {
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;  // faces per CTA
-    static constexpr int NT = DIR == 0 ? NF + W - 1 : 32 * (NC + W - 1);
+    // x: up to two row segments of the flattened face order (see k_faces3)
+    static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
     static constexpr int NE = 14 + 2 * NS;
     static constexpr int NV = 2 * W;  // stencil vectors: F and U of each node
     double U[NC][NT];
@@ -56,8 +57,15 @@ enum : int {
 };
 
 // window node of stencil slot k for lane of group g
-template <int DIR> __device__ __forceinline__ int tile_node(int g, int lane, int k) {
-    return DIR == 0 ? g * 32 + lane + k : (g + k) * 32 + lane;
+// window slot of stencil node k of face (g, lane); x faces past the first row
+// segment (q >= L0) sit W-1 slots further (their segment's own halo)
+template <int DIR, int W>
+__device__ __forceinline__ int tile_node(int g, int lane, int k, int L0) {
+    if (DIR == 0) {
+        const int q = g * 32 + lane;
+        return q + k + (q >= L0 ? W - 1 : 0);
+    }
+    return (g + k) * 32 + lane;
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR>
@@ -81,18 +89,52 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     const long long step_n = DIR == 0 ? 1 : P.sx;
     const double* m1a = DIR == 0 ? P.mxx : P.mex;
     const double* m2a = DIR == 0 ? P.mxy : P.mey;
-    // x: faces f0 .. f0+NF-1 of row j0;  y: columns i0 .. i0+31, face rows f0 .. f0+NC-1
-    const int f0 = DIR == 0 ? blockIdx.x * NF : blockIdx.y * NC;
-    const int j0 = blockIdx.y, i0 = blockIdx.x * 32;
-    const long long win0 = DIR == 0 ? pidx(P, f0 - H, j0) : pidx(P, i0, f0 - H);
+    // x: NF consecutive faces of the flattened (row j, face f) order — at most
+    // two row segments when nx+1 >= NF, else one row segment per CTA;
+    // y: columns i0 .. i0+31, face rows f0 .. f0+NC-1
+    int f0, r0 = 0, L0 = NF;
+    if (DIR == 0) {
+        if (P.nx + 1 >= NF) {
+            const long long F0 = (long long)blockIdx.x * NF;
+            r0 = (int)(F0 / (P.nx + 1));
+            f0 = (int)(F0 % (P.nx + 1));
+            L0 = min(NF, P.nx + 1 - f0);
+        } else {
+            r0 = blockIdx.y;
+            f0 = blockIdx.x * NF;
+        }
+    } else {
+        f0 = blockIdx.y * NC;
+    }
+    const int i0 = blockIdx.x * 32;
+    const long long win0 = DIR == 0 ? 0 : pidx(P, i0, f0 - H);
+    // x face q of this CTA -> (row, f)
+    auto xface = [&](int q, int& row, int& f) {
+        if (q < L0) {
+            row = r0;
+            f = f0 + q;
+        } else {
+            row = r0 + 1;
+            f = q - L0;
+        }
+    };
 
     // ---------------- phase 1a: node window -> shared memory
     for (int t = threadIdx.x; t < NT; t += blockDim.x) {
         long long id;
         bool ok;
         if (DIR == 0) {
-            id = win0 + t;
-            ok = f0 - H + t < P.nx + P.g;
+            const int n0 = L0 + W - 1;  // window slots of the first segment
+            int a, row;
+            if (t < n0) {
+                a = f0 - H + t;
+                row = r0;
+            } else {
+                a = -H + (t - n0);
+                row = r0 + 1;
+            }
+            id = pidx(P, a, row);
+            ok = a < P.nx + P.g && row < P.ny && (t < n0 || t - n0 < NF - L0 + W - 1);
         } else {
             const int r = t / 32, l = t % 32;
             id = win0 + (long long)r * P.sx + l;
@@ -116,9 +158,15 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     }
 
     // this thread's face in phase 1b: group = warp, lane
-    const int my_f = DIR == 0 ? f0 + threadIdx.x : f0 + warp;     // face index along the line
-    const int my_col = DIR == 0 ? j0 : i0 + lane;                 // row (x) / column (y)
-    const bool my_active = DIR == 0 ? my_f <= P.nx : (my_col < P.nx && my_f <= P.ny);
+    int my_f, my_col;  // face index along the line; row (x) / column (y)
+    if (DIR == 0) {
+        xface(threadIdx.x, my_col, my_f);
+    } else {
+        my_f = f0 + warp;
+        my_col = i0 + lane;
+    }
+    const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < P.ny)
+                                    : (my_col < P.nx && my_f <= P.ny);
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
     auto err_index = [&](int f, int col) -> unsigned long long {
         // global (line, face) order of inviscid_direction (solver.hpp:450-481)
@@ -188,7 +236,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node<DIR>(warp, lane, k);
+                const int t = tile_node<DIR, W>(warp, lane, k, L0);
                 const double un = (m1f * S.u[t] + m2f * S.v[t]) / sf;
                 alpha = smax(alpha, sf * (fabs(un) + S.c[t]));
             }
@@ -208,8 +256,13 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     const int fl = warp;  // field / component this warp evaluates
     for (int g = 0; g < NC; ++g) {
         const int face = g * 32 + lane;  // slot in the CTA
-        const int f = DIR == 0 ? f0 + face : f0 + g;
-        const int col = DIR == 0 ? j0 : i0 + lane;
+        int f, col;
+        if (DIR == 0) {
+            xface(face, col, f);
+        } else {
+            f = f0 + g;
+            col = i0 + lane;
+        }
         const bool live = !S.bad[face];
         const long long o = DIR == 0 ? (long long)col * (P.nx + 1) + f : (long long)f * P.nx + col;
         if (!CHAR) {
@@ -219,7 +272,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 double wp[W], wm[W];
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int t = tile_node<DIR>(g, lane, k);
+                    const int t = tile_node<DIR, W>(g, lane, k, L0);
                     wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
                     wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
                 }
@@ -241,7 +294,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node<DIR>(g, lane, k);
+                const int t = tile_node<DIR, W>(g, lane, k, L0);
                 const double unk = n1 * S.u[t] + n2 * S.v[t];
                 const double ck = S.c[t];
                 const double lam = es * (kind == 0 ? unk + -1.0 * ck : kind == 2 ? unk + ck : unk);
@@ -251,7 +304,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         }
         for (int vec = warp; vec < NV; vec += NC) {
             const int k = vec >> 1;
-            const int t = tile_node<DIR>(g, lane, k);
+            const int t = tile_node<DIR, W>(g, lane, k, L0);
             double q[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) q[c] = (vec & 1) ? S.U[c][t] : S.F[c][t];
@@ -295,7 +348,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int t = tile_node<DIR>(g, lane, k);
+                    const int t = tile_node<DIR, W>(g, lane, k, L0);
 #pragma unroll
                     for (int vu = 0; vu < 2; ++vu) {
                         const int vec = 2 * k + vu;
@@ -311,7 +364,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 if (bad) {  // exact redo (rare): plain IEEE quotients
 #pragma unroll
                     for (int k = 0; k < W; ++k) {
-                        const int t = tile_node<DIR>(g, lane, k);
+                        const int t = tile_node<DIR, W>(g, lane, k, L0);
 #pragma unroll
                         for (int vu = 0; vu < 2; ++vu) {
                             const int vec = 2 * k + vu;
@@ -350,8 +403,13 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     for (int g = 0; g < NC; ++g) {
         const int face = g * 32 + lane;
         if (S.bad[face]) continue;
-        const int f = DIR == 0 ? f0 + face : f0 + g;
-        const int col = DIR == 0 ? j0 : i0 + lane;
+        int f, col;
+        if (DIR == 0) {
+            xface(face, col, f);
+        } else {
+            f = f0 + g;
+            col = i0 + lane;
+        }
         const long long o = DIR == 0 ? (long long)col * (P.nx + 1) + f : (long long)f * P.nx + col;
         const double am = S.amp[0][face];
         const double ap = S.amp[2 + NS][face];
@@ -408,8 +466,13 @@ inline void launch_faces3(const KParams& P, const double* Ut, int stage, int ste
         configured = true;
     }
     const int NF = 32 * NC;
-    dim3 grid(DIR == 0 ? (P.nx + 1 + NF - 1) / NF : (P.nx + 31) / 32,
-              DIR == 0 ? P.ny : (P.ny + 1 + NC - 1) / NC);
+    dim3 grid;
+    if (DIR == 0)
+        grid = P.nx + 1 >= NF  // flattened rows: (nx+1) ny faces in runs of NF
+                   ? dim3((unsigned)(((long long)(P.nx + 1) * P.ny + NF - 1) / NF), 1)
+                   : dim3((P.nx + 1 + NF - 1) / NF, P.ny);
+    else
+        grid = dim3((P.nx + 31) / 32, (P.ny + 1 + NC - 1) / NC);
     kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step);
 }
 

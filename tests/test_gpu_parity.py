@@ -32,6 +32,9 @@ CASES = {
     "h2o2_counterflow_inflow": (lambda: configs.h2o2_counterflow(32), False, 20),
     "wall_isothermal": (lambda: configs.wall_channel(24), False, 10),
     "wall_adiabatic_weno3z": (lambda: configs.wall_channel(24, isothermal=False, scheme="weno3z"), False, 10),
+    # nx + 1 >= 32 NC: the x-face kernels' flattened-row mode (CTAs straddle rows)
+    "tgv_wide_flat_x": (lambda: configs.tgv2d(160), True, 6),
+    "h2o2_wide_flat_x": (lambda: configs.h2o2_counterflow(240, nxy=(240, 12)), False, 6),
 }
 
 
