@@ -1012,6 +1012,7 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->nc = nc;
     const size_t P2 = static_cast<size_t>(nx + 2 * g) * (ny + 2 * g);  // one (x, y) plane
     const size_t P = P2 * (nz > 0 ? nz + 2 * g : 1);
+    if (P >= (1ull << 31)) throw config_error("padded box too large for one context (>= 2^31 nodes)");
     ctx->plane = P;
     cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
     ctx->stream = ctx->own_stream;

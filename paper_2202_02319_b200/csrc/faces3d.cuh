@@ -120,10 +120,20 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     const double* m1a = DIR == 0 ? P.mxx : DIR == 1 ? P.mex : P.mzz;
     const double* m2a = DIR == 0 ? P.mxy : DIR == 1 ? P.mey : P.mzz;
     // a = index along DIR; col = i (DIR 1, 2) or the flattened row (DIR 0)
+    // rows r0, r0+1 of the flattened x order as (j, k), once per CTA
+    const int xj0 = DIR == 0 ? r0 % P.ny : 0, xk0 = DIR == 0 ? r0 / P.ny : 0;
+    const int xj1 = DIR == 0 ? (xj0 + 1 == P.ny ? 0 : xj0 + 1) : 0;
+    const int xk1 = DIR == 0 ? (xj0 + 1 == P.ny ? xk0 + 1 : xk0) : 0;
     auto node = [&](int a, int col) -> long long {
-        if (DIR == 0) return pidx3(P, a, col % P.ny, col / P.ny);
+        if (DIR == 0) return col == r0 ? pidx3(P, a, xj0, xk0) : pidx3(P, a, xj1, xk1);
         if (DIR == 1) return pidx3(P, col, a, kb);
         return pidx3(P, col, jb, a);
+    };
+    // the (x, y) metric-plane index of the same node (the mesh is extruded)
+    auto node2 = [&](int a, int col) -> int {
+        if (DIR == 0) return ((col == r0 ? xj0 : xj1) + P.g) * P.sx + (a + P.g);
+        if (DIR == 1) return (a + P.g) * P.sx + (col + P.g);
+        return (jb + P.g) * P.sx + (col + P.g);
     };
     // x face q of this CTA -> (row, f)
     auto xface = [&](int q, int& row, int& f) {
@@ -164,7 +174,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     const long long il = node(my_f - 1, my_col), ir = il + step_n;
     double m1f = 0.0, m2f = 0.0;
     if (my_active) {
-        const long long l2 = il % P.sxy, r2 = ir % P.sxy;
+        const int l2 = node2(my_f - 1, my_col);
+        const int r2 = DIR == 0 ? l2 + 1 : DIR == 1 ? l2 + P.sx : l2;
         m1f = 0.5 * (ldg(m1a + l2) + ldg(m1a + r2));
         m2f = 0.5 * (ldg(m2a + l2) + ldg(m2a + r2));
     }
@@ -204,7 +215,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         }
         if (!ok) continue;
         const long long id = node(a, col);
-        const long long id2 = id % P.sxy;
+        const int id2 = node2(a, col);
         const double J = ldg(P.jac + id2);
         double Uk[NC], Fk[NC];
 #pragma unroll

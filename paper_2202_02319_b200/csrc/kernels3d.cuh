@@ -23,27 +23,33 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
     const int na = pass == 0 ? P.ny : P.nx + 2 * g;        // first transverse index
     const int nb = pass == 2 ? P.ny + 2 * g : P.nz;       // second
     const int a0 = pass == 0 ? 0 : -g, b0 = pass == 2 ? -g : 0;
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= 2LL * na * nb) return;
-    const int side = (int)(tid / ((long long)na * nb));
-    const long long rem = tid % ((long long)na * nb);
-    const int a = a0 + (int)(rem % na), b = b0 + (int)(rem / na);
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;  // < 2 (nx+2g)(ny+2g)
+    if (tid >= 2 * na * nb) return;
+    const int side = tid / (na * nb);
+    const int rem = tid - side * na * nb;
+    const int a = a0 + rem % na, b = b0 + rem / na;
     const int n = pass == 0 ? P.nx : pass == 1 ? P.ny : P.nz;
     for (int k = 1; k <= g; ++k) {
         const int sidx = side == 0 ? n - k : k - 1;
         const int didx = side == 0 ? -k : n - 1 + k;
         long long s, d;
+        int s2, d2;  // (x, y) plane indices of the metric arrays
         if (pass == 0) {
             s = pidx3(P, sidx, a, b);
             d = pidx3(P, didx, a, b);
+            s2 = (a + g) * P.sx + (sidx + g);
+            d2 = (a + g) * P.sx + (didx + g);
         } else if (pass == 1) {
             s = pidx3(P, a, sidx, b);
             d = pidx3(P, a, didx, b);
+            s2 = (sidx + g) * P.sx + (a + g);
+            d2 = (didx + g) * P.sx + (a + g);
         } else {
             s = pidx3(P, a, b, sidx);
             d = pidx3(P, a, b, didx);
+            s2 = d2 = (b + g) * P.sx + (a + g);
         }
-        const double ratio = P.jac[s % P.sxy] / P.jac[d % P.sxy];
+        const double ratio = P.jac[s2] / P.jac[d2];
 #pragma unroll
         for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
     }
@@ -55,9 +61,10 @@ __global__ void __launch_bounds__(256) k_prim3(const __grid_constant__ KParams P
                                                const double* __restrict__ Ut, int stage,
                                                int step) {
     if (failed(P.err)) return;
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= P.plane) return;
-    const double J = P.jac[id % P.sxy];
+    const int id2 = blockIdx.x * blockDim.x + threadIdx.x;  // (x, y) plane index
+    if (id2 >= P.sxy) return;
+    const long long id = (long long)blockIdx.y * P.sxy + id2;  // blockIdx.y: padded k
+    const double J = P.jac[id2];
     double U[NS + 4];
 #pragma unroll
     for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
@@ -297,11 +304,12 @@ __global__ void __launch_bounds__(256) k_dt3(const __grid_constant__ KParams P) 
         s_chem = 0x7ff0000000000000ull;
     }
     __syncthreads();
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;  // (i, j) of plane k = blockIdx.y
     double lam_loc = 0.0, chem_loc = __longlong_as_double(0x7ff0000000000000ll);
-    if (t < (long long)P.nx * P.ny * P.nz) {
-        const int i = (int)(t % P.nx), j = (int)((t / P.nx) % P.ny), k = (int)(t / ((long long)P.nx * P.ny));
-        const long long id = pidx3(P, i, j, k), id2 = id % P.sxy;
+    if (t < P.nx * P.ny) {
+        const int i = t % P.nx, j = t / P.nx, k = blockIdx.y;
+        const long long id = pidx3(P, i, j, k);
+        const int id2 = (j + P.g) * P.sx + (i + P.g);
         const double J = ldg(P.jac + id2);
         const double mxx = ldg(P.mxx + id2), mxy = ldg(P.mxy + id2);
         const double mex = ldg(P.mex + id2), mey = ldg(P.mey + id2), mzz = ldg(P.mzz + id2);
@@ -364,7 +372,7 @@ template <int NS> struct Launch3 {
         return 1;
     }
     static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        const unsigned nb = (unsigned)((P.plane + 255) / 256);
+        const dim3 nb((unsigned)((P.sxy + 255) / 256), P.nz + 2 * P.g);
         if (P.viscous) k_prim3<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step);
         else k_prim3<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step);
         return 1;
@@ -404,8 +412,8 @@ template <int NS> struct Launch3 {
         return 1;
     }
     static int dt(const KParams& P, cudaStream_t s) {
-        const long long n = (long long)P.nx * P.ny * P.nz;
-        k_dt3<NS><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P);
+        const dim3 grid((unsigned)((P.nx * P.ny + 255) / 256), P.nz);
+        k_dt3<NS><<<grid, 256, 0, s>>>(P);
         return 1;
     }
     static KernelSet make() { return KernelSet{&bc, &prim, &faces, &visc, &assemble, &dt}; }
