@@ -966,10 +966,8 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     if (three_d) {
         // 3D extension: the (x, y) mesh extruded over lz (flux3.cuh)
         if (!(cfg->lz > 0.0)) throw config_error("3D: lz must be positive");
-        if (!cfg->periodic_x || !cfg->periodic_y || !cfg->periodic_z)
-            throw usage_error("3D: only periodic boundaries are supported");
-        if (cfg->laser.present && cfg->laser.energy != 0.0)
-            throw usage_error("3D: the laser source has no 3D form in the reference");
+        // x / y edges take the reference's 2D rules on every z plane; z is periodic
+        if (!cfg->periodic_z) throw usage_error("3D: z must be periodic");
         int k0 = 0;
         slab_rows(cfg->nz, ctx->nranks, ctx->rank, k0, nz);
         if (nz < cfg->g) throw config_error("3D: every z-slab needs >= g planes");
@@ -1031,7 +1029,7 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
                               cudaMemcpyHostToDevice),
                    "cache init");
     }
-    ctx->geom = dalloc(12 * P2);
+    ctx->geom = dalloc((nz > 0 ? 14 : 12) * P2);
     {
         // 2D: mesh x, y in slots 10, 11 (laser); 3D: the zeta metrics there
         const std::vector<double>* f[12] = {
@@ -1043,6 +1041,14 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
             cuda_check(cudaMemcpy(ctx->geom + k * P2, f[k]->data(), P2 * sizeof(double),
                                   cudaMemcpyHostToDevice),
                        "geometry upload");
+        if (nz > 0) {  // 3D: mesh x, y in slots 12, 13 (laser)
+            cuda_check(cudaMemcpy(ctx->geom + 12 * P2, ctx->mesh.x.d.data(), P2 * sizeof(double),
+                                  cudaMemcpyHostToDevice),
+                       "geometry upload");
+            cuda_check(cudaMemcpy(ctx->geom + 13 * P2, ctx->mesh.y.d.data(), P2 * sizeof(double),
+                                  cudaMemcpyHostToDevice),
+                       "geometry upload");
+        }
     }
     const size_t nzc = nz > 0 ? nz : 1;
     ctx->Fx = dalloc(static_cast<size_t>(nc) * (nx + 1) * ny * nzc);
@@ -1161,6 +1167,8 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     if (nz > 0) {
         k.mzz = ctx->geom + 10 * P2;
         k.vmzz = ctx->geom + 11 * P2;
+        k.xc = ctx->geom + 12 * P2;
+        k.yc = ctx->geom + 13 * P2;
     } else {
         k.xc = ctx->geom + 10 * P2;
         k.yc = ctx->geom + 11 * P2;

@@ -13,11 +13,45 @@
 namespace ign {
 
 // ---------------------------------------------------------------- ghost fill
-// periodic copies (boundary.hpp:146-149, 203-209) pass by pass: x over the
-// interior (j, k), y over all i and interior k, z over all (i, j)
+// fill_ghosts (boundary.hpp:136-258) on every interior z plane: x edges over
+// rows 0..ny-1, then y edges over -g..nx+g-1 (corners take the y rule), with
+// the reference's 2D edge rules extended by w (walls mirror it, inflow sets
+// w = 0); then z (periodic) over whole (x, y) planes unless the z ghost planes
+// come from the neighbouring z-slabs.
+template <int NS>
+__device__ int bc3_prim_at(const KParams& P, const double* Ut, int i, int j, int k,
+                           Prim3<NS>& pt, double& rs) {
+    const long long id = pidx3(P, i, j, k);
+    const double J = P.jac[(j + P.g) * P.sx + (i + P.g)];
+    double U[NS + 4];
+#pragma unroll
+    for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
+    return primitives_from_conservative3<NS>(U, P.mix, 300.0, pt, &rs);
+}
+
+template <int NS>
+__device__ void bc3_store(const KParams& P, double* Ut, const Prim3<NS>& pt, int i, int j, int k) {
+    double U[NS + 4];
+    conservative_from_primitives3<NS>(pt, P.mix, U);
+    const long long id = pidx3(P, i, j, k);
+    const double invJ = 1.0 / P.jac[(j + P.g) * P.sx + (i + P.g)];
+#pragma unroll
+    for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + id] = U[c] * invJ;
+}
+
+template <int NS>
+__device__ void bc3_copy_scaled(const KParams& P, double* Ut, int is, int js, int id_, int jd,
+                                int k) {
+    const long long s = pidx3(P, is, js, k), d = pidx3(P, id_, jd, k);
+    const double ratio =
+        P.jac[(js + P.g) * P.sx + (is + P.g)] / P.jac[(jd + P.g) * P.sx + (id_ + P.g)];
+#pragma unroll
+    for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+}
+
 template <int NS>
 __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, double* Ut,
-                                             int pass) {
+                                             int pass, int stage, int step) {
     if (failed(P.err)) return;
     const int g = P.g;
     const int na = pass == 0 ? P.ny : P.nx + 2 * g;        // first transverse index
@@ -29,29 +63,100 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
     const int rem = tid - side * na * nb;
     const int a = a0 + rem % na, b = b0 + rem / na;
     const int n = pass == 0 ? P.nx : pass == 1 ? P.ny : P.nz;
-    for (int k = 1; k <= g; ++k) {
-        const int sidx = side == 0 ? n - k : k - 1;
-        const int didx = side == 0 ? -k : n - 1 + k;
-        long long s, d;
-        int s2, d2;  // (x, y) plane indices of the metric arrays
-        if (pass == 0) {
-            s = pidx3(P, sidx, a, b);
-            d = pidx3(P, didx, a, b);
-            s2 = (a + g) * P.sx + (sidx + g);
-            d2 = (a + g) * P.sx + (didx + g);
-        } else if (pass == 1) {
-            s = pidx3(P, a, sidx, b);
-            d = pidx3(P, a, didx, b);
-            s2 = (sidx + g) * P.sx + (a + g);
-            d2 = (didx + g) * P.sx + (a + g);
-        } else {
-            s = pidx3(P, a, b, sidx);
-            d = pidx3(P, a, b, didx);
-            s2 = d2 = (b + g) * P.sx + (a + g);
-        }
-        const double ratio = P.jac[s2] / P.jac[d2];
+    if (pass == 2) {  // periodic z: the (x, y) metrics are z-independent
+        for (int k = 1; k <= g; ++k) {
+            const long long s = pidx3(P, a, b, side == 0 ? n - k : k - 1);
+            const long long d = pidx3(P, a, b, side == 0 ? -k : n - 1 + k);
+            const int q = (b + g) * P.sx + (a + g);
+            const double ratio = P.jac[q] / P.jac[q];
 #pragma unroll
-        for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+            for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+        }
+        return;
+    }
+    const int edge = 2 * pass + side;  // 0 left, 1 right, 2 bottom, 3 top
+    const int type = P.bc_type[edge];
+    const int t = a, kz = b;
+    auto ij = [&](int e, int& i, int& j) {  // index e along the edge normal
+        if (pass) { i = t; j = e; } else { i = e; j = t; }
+    };
+    // (plane, edge, t, k) order: deterministic, unique per ghost node
+    const unsigned long long ekey =
+        ((((unsigned long long)(kz + P.j0) * 4 + edge) * (P.nx + P.ny + 4 * g) + (t + g)) *
+         (g + 1));
+    int gi, gj;
+    switch (type) {
+    case 0: {  // Periodic (boundary.hpp:203-209)
+        for (int k = 1; k <= g; ++k) {
+            int si, sj;
+            ij(side == 0 ? n - k : k - 1, si, sj);
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            bc3_copy_scaled<NS>(P, Ut, si, sj, gi, gj, kz);
+        }
+        break;
+    }
+    case 1:
+    case 2: {  // No-slip walls (boundary.hpp:210-226), w mirrored too
+        for (int k = 1; k <= g; ++k) {
+            int mi, mj;
+            ij(side == 0 ? k - 1 : n - k, mi, mj);
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            Prim3<NS> pt;
+            double rs;
+            const int st = bc3_prim_at<NS>(P, Ut, mi, mj, kz, pt, rs);
+            if (st) {
+                report(P.err, stage, PH_BC, ekey + k, st, step);
+                return;
+            }
+            pt.u = -pt.u;
+            pt.v = -pt.v;
+            pt.w = -pt.w;
+            if (type == 1) {
+                const double tg = 2.0 * P.T_wall[edge] - pt.T;
+                pt.T = smax(tg, 0.05 * P.T_wall[edge]);
+            }
+            pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
+            bc3_store<NS>(P, Ut, pt, gi, gj, kz);
+        }
+        break;
+    }
+    case 3: {  // Inflow (boundary.hpp:227-241): the host-built (x, y) profile, w = 0
+        int ii, ji;
+        ij(side == 0 ? 0 : n - 1, ii, ji);
+        Prim3<NS> inner;
+        double rs;
+        const int st = bc3_prim_at<NS>(P, Ut, ii, ji, kz, inner, rs);
+        if (st) {
+            report(P.err, stage, PH_BC, ekey, st, step);
+            return;
+        }
+        const int tlo = pass ? -g : 0;
+        const double* prof = P.inflow[edge] + (long long)(t - tlo) * g * (3 + NS);
+        for (int k = 1; k <= g; ++k) {
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            const double* q = prof + (k - 1) * (3 + NS);
+            Prim3<NS> pt;
+            pt.u = q[0];
+            pt.v = q[1];
+            pt.w = 0.0;
+            pt.T = q[2];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) pt.Y[s] = q[3 + s];
+            pt.p = inner.p;
+            pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
+            bc3_store<NS>(P, Ut, pt, gi, gj, kz);
+        }
+        break;
+    }
+    default: {  // Outflow (boundary.hpp:242-249)
+        int ii, ji;
+        ij(side == 0 ? 0 : n - 1, ii, ji);
+        for (int k = 1; k <= g; ++k) {
+            ij(side == 0 ? -k : n - 1 + k, gi, gj);
+            bc3_copy_scaled<NS>(P, Ut, ii, ji, gi, gj, kz);
+        }
+        break;
+    }
     }
 }
 
@@ -189,6 +294,78 @@ __global__ void __launch_bounds__(128) k_visc3(const __grid_constant__ KParams P
     }
 }
 
+// ---------------------------------------------------------------- LODI outflow
+// lodi_outflow_override (solver.hpp:717-788) on the right-edge column of
+// plane k, with the second transverse wave (w) appended: L4 = out dw/dn
+template <int NS>
+__device__ void lodi_dfx3(const KParams& P, int j, int kz, double* dF) {
+    const int i = P.nx - 1;
+    const long long id = pidx3(P, i, j, kz), i1 = id - 1, i2 = id - 2;
+    const int q = (j + P.g) * P.sx + (i + P.g);
+    const double vj = ldg(P.vjac + q);
+    const double xi_x = ldg(P.vmxx + q) * vj;
+    const double xi_y = ldg(P.vmxy + q) * vj;
+    const double sn = ghypot(xi_x, xi_y);
+    const double n1 = xi_x / sn, n2 = xi_y / sn;
+    auto ddn = [&](const double* f) {
+        return sn * 0.5 * (3.0 * ldg(f + id) - 4.0 * ldg(f + i1) + ldg(f + i2));
+    };
+    const double rr = ldg(PRHO3(P) + id), cc0 = ldg(PC3(P) + id), pp = ldg(PP3(P) + id);
+    const double uu = ldg(PU3(P) + id), vv = ldg(PV3(P) + id), ww = ldg(PW3(P) + id);
+    const double un = n1 * uu + n2 * vv;
+    const double M = smin(fabs(un) / cc0, 0.99);
+    const double drdn = ddn(PRHO3(P));
+    const double dpdn = ddn(PP3(P));
+    const double dundn = n1 * ddn(PU3(P)) + n2 * ddn(PV3(P));
+    const double dutdn = -n2 * ddn(PU3(P)) + n1 * ddn(PV3(P));
+    const double dwdn = ddn(PW3(P));
+    const double K = P.sigma_out_right * cc0 * (1.0 - M * M) / P.lx;
+    const double L1 = K * (pp - P.p_target_right);
+    const double out = un > 0.0 ? un : 0.0;
+    const double L2 = out * (cc0 * cc0 * drdn - dpdn);
+    const double L3 = out * dutdn;
+    const double L4 = out * dwdn;
+    const double L5 = (un + cc0) * (dpdn + rr * cc0 * dundn);
+    const double drdt = -(L2 + 0.5 * (L5 + L1)) / (cc0 * cc0);
+    const double dundt = -(L5 - L1) / (2.0 * rr * cc0);
+    const double dutdt = -L3;
+    const double dwdt = -L4;
+    const double dpdt = -0.5 * (L5 + L1);
+    double Y[NS], dYdt[NS];
+    double sumRdY = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        Y[s] = ldg(PY3(P, s) + id);
+        dYdt[s] = -out * ddn(PY3(P, s));
+        sumRdY += divW(P.mix.sp[s], P.mix.R) * dYdt[s];
+    }
+    const double rbar = r_specific<NS>(Y, P.mix);
+    const double Tt = ldg(PT3(P) + id);
+    const double dTdt = Tt * (dpdt / pp - drdt / rr - sumRdY / rbar);
+    const double dudt = n1 * dundt - n2 * dutdt;
+    const double dvdt = n2 * dundt + n1 * dutdt;
+    const double k = 0.5 * ((uu * uu + vv * vv) + ww * ww);
+    const double e = e_mass_rs<NS>(Tt, Y, rbar, P.mix);
+    const double cv = cp_mass<NS>(Tt, Y, P.mix) - rbar;
+    double sum_es_dY = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const double esn = h_species(Tt, P.mix.sp[s], P.mix.R) - divW(P.mix.sp[s], P.mix.R) * Tt;
+        sum_es_dY += esn * dYdt[s];
+    }
+    double dU[NS + 4];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) dU[s] = Y[s] * drdt + rr * dYdt[s];
+    dU[NS] = uu * drdt + rr * dudt;
+    dU[NS + 1] = vv * drdt + rr * dvdt;
+    dU[NS + 2] = ww * drdt + rr * dwdt;
+    dU[NS + 3] = (e + k) * drdt + rr * cv * dTdt + rr * sum_es_dY +
+                 rr * ((uu * dudt + vv * dvdt) + ww * dwdt);
+    const double invJ = 1.0 / ldg(P.jac + q);
+#pragma unroll
+    for (int c = 0; c < NS + 4; ++c) dF[c] = -dU[c] * invJ;
+}
+
 // ---------------------------------------------------------------- assemble + update
 template <int NS, int MODE>
 __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KParams P,
@@ -222,9 +399,12 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
             const long long fy = ((long long)k * (P.ny + 1) + j) * P.nx + i;
             const long long fz = ((long long)k * P.ny + j) * P.nx + i;
             double r[NC];
+            double dFl[NC];
+            const bool lodi = P.lodi && i == P.nx - 1;
+            if (lodi) lodi_dfx3<NS>(P, j, k, dFl);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                const double dF = P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
+                const double dF = lodi ? dFl[c] : P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
                 const double dG = P.Gy[c * fyp + fy + P.nx] - P.Gy[c * fyp + fy];
                 const double dH = P.Hz[c * fzp + fz + (long long)P.nx * P.ny] - P.Hz[c * fzp + fz];
                 r[c] = -((dF + dG) + dH);
@@ -250,6 +430,12 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
                 source_terms<NS>(ldg(PRHO3(P) + id), ldg(PT3(P) + id), Y, P.mix, P.mech, wdot);
 #pragma unroll
                 for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
+            }
+            // laser_power (laser.hpp:88-91) of the node's (x, y): the
+            // reference's 2D kernel, uniform along z
+            if (P.laser.on) {
+                const int q = (j + P.g) * P.sx + (i + P.g);
+                r[NS + 3] += laser_power(ldg(P.xc + q), ldg(P.yc + q), t_stage, P.laser) * invJ;
             }
             const unsigned long long cell =
                 ((unsigned long long)(k + P.j0) * P.ny + j) * P.nx + i;
@@ -356,19 +542,17 @@ template <int NS> struct Launch3 {
     // exchanged z planes carry their x/y ghosts; ypass 1: z copies (single
     // domain) — with z-slabs the z ghost planes came from the peers instead
     static int bc(const KParams& P, double* Ut, int ypass, int stage, int step, cudaStream_t s) {
-        (void)stage;
-        (void)step;
         const int g = P.g;
         if (ypass == 0) {
-            const long long n0 = 2LL * P.ny * P.nz;
-            k_bc3<NS><<<(unsigned)((n0 + 127) / 128), 128, 0, s>>>(P, Ut, 0);
-            const long long n1 = 2LL * (P.nx + 2 * g) * P.nz;
-            k_bc3<NS><<<(unsigned)((n1 + 127) / 128), 128, 0, s>>>(P, Ut, 1);
+            const int n0 = 2 * P.ny * P.nz;
+            k_bc3<NS><<<(unsigned)((n0 + 127) / 128), 128, 0, s>>>(P, Ut, 0, stage, step);
+            const int n1 = 2 * (P.nx + 2 * g) * P.nz;
+            k_bc3<NS><<<(unsigned)((n1 + 127) / 128), 128, 0, s>>>(P, Ut, 1, stage, step);
             return 2;
         }
         if (P.zhalo) return 0;
-        const long long n2 = 2LL * (P.nx + 2 * g) * (P.ny + 2 * g);
-        k_bc3<NS><<<(unsigned)((n2 + 127) / 128), 128, 0, s>>>(P, Ut, 2);
+        const int n2 = 2 * (P.nx + 2 * g) * (P.ny + 2 * g);
+        k_bc3<NS><<<(unsigned)((n2 + 127) / 128), 128, 0, s>>>(P, Ut, 2, stage, step);
         return 1;
     }
     static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {

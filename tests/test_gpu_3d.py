@@ -11,6 +11,9 @@ z-extrusion cross-check of SURVEY §8c:
     dy = 1) exercises the zeta-face kernel; equal to the 2D oracle within a
     tolerance (the 2D oracle's y metrics carry ulp noise the uniform z
     metrics do not).
+  * The non-periodic x / y edges (walls, inflow, outflow with LODI) and the
+    laser run the reference's 2D rules on every z plane: the same extrusion
+    check covers them (wall, counterflow, Sod/LODI cases).
   * 3D TGV: periodic conservation of mass, momenta and energy.
 """
 import ctypes as C
@@ -39,6 +42,13 @@ EXTRUDE = {
     "ch4_react_char": (lambda: configs.reacting_ch4(20, laser=False), False, 8),
     "ch4_react_comp_weno3z": (lambda: configs.reacting_ch4(20, scheme="weno3z", split="comp",
                                                           laser=False), False, 8),
+    # the reference's non-periodic edges on every z plane
+    "ch4_react_laser": (lambda: configs.reacting_ch4(20), False, 8),
+    "wall_isothermal": (lambda: configs.wall_channel(20), False, 6),
+    "wall_adiabatic_weno3z": (lambda: configs.wall_channel(20, isothermal=False,
+                                                           scheme="weno3z"), False, 6),
+    "h2o2_inflow_outflow_laser": (lambda: configs.h2o2_counterflow(24), False, 6),
+    "sod_lodi_outflow": (lambda: configs.sod_strip(120), False, 12),
 }
 
 NZ = 7
