@@ -59,7 +59,9 @@ OPS = {  # case -> (inviscid ops per cell-stage, whole-step ops per cell)
     "tgv": (4274, 14333),
     "tgv3d": (None, 25800),
     "h2o2": (7515, 29738),      # inviscid: 4274 x 1.758 (4-species faces / gamma-gas
-}                               # faces FP64 instructions per cell-stage, ncu, 512^2)
+                                # faces FP64 instructions per cell-stage, ncu, 512^2)
+    "jet3d": (None, None),      # 4 species, 3D, WENO3Z componentwise: not counted yet
+}
 INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
 INVISCID_OPS_PER_CELL_STAGE = 4274
 TRAFFIC = {("tgv3d", 256): (1.790325 + 1.825101 + 2.307236 + 0.652938 + 0.657513 + 0.664158) * 1e9}
@@ -138,6 +140,11 @@ def make_case(args, nslabs: int = 1):
         return (configs.tgv3d(n, nz=n * nslabs),
                 f"TGV 3D {n}^3 per GPU (BASELINE configs[1]), viscous Re 1600, Ma 0.1, TENO6 "
                 "characteristic, gamma-gas, fixed dt; 3D extension (the reference is 2D-only)")
+    if args.case == "jet3d":
+        nz = args.n // 16
+        return (configs.jet3d(args.n, args.n // 2, nz * nslabs),
+                f"3D H2 jet (configs[3] form): {args.n}x{args.n // 2}x{nz} per GPU, inflow / "
+                "LODI outflow / walls, one-step chemistry, shaped laser, WENO3Z comp; z-slabs")
     if args.case == "h2o2":
         c = configs.h2o2_counterflow(args.n, nxy=(args.n, args.n * nslabs))
         return c, f"H2/O2 one-step counterflow flame {args.n}^2 per GPU (configs[2])"
@@ -320,7 +327,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=None,
                     help="cells per side (default 256 for tgv3d, 4096 tgv, 512 h2o2)")
-    ap.add_argument("--case", default="tgv3d", choices=["tgv3d", "tgv", "h2o2", "ensemble"])
+    ap.add_argument("--case", default="tgv3d",
+                    choices=["tgv3d", "tgv", "h2o2", "ensemble", "jet3d"])
     ap.add_argument("--members", type=int, default=8, help="ensemble members per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -330,7 +338,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.n is None:
-        args.n = {"tgv3d": 256, "tgv": 4096, "h2o2": 512, "ensemble": 500}[args.case]
+        args.n = {"tgv3d": 256, "tgv": 4096, "h2o2": 512, "ensemble": 500, "jet3d": 512}[args.case]
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     dist = None
@@ -432,13 +440,14 @@ def main():
     dom = max(prof, key=lambda k: prof[k][0])
     f_ms, f_n = prof["faces"]
     inv_ops, step_ops = OPS[args.case]
-    if inv_ops is None:
-        inv_ops = INVISCID_OPS_PER_CELL_STAGE * (INVISCID_3D_OVER_2D if args.case == "tgv3d" else 1.0)
-    face_ops = cells * inv_ops  # per timed faces region = one stage, all directions
-    achieved = face_ops / (f_ms / f_n / 1e3) / 1e12 if f_n else None
+    if inv_ops is None and args.case == "tgv3d":
+        inv_ops = INVISCID_OPS_PER_CELL_STAGE * INVISCID_3D_OVER_2D
+    # per timed faces region = one stage, all directions
+    face_ops = cells * inv_ops if inv_ops else None
+    achieved = face_ops / (f_ms / f_n / 1e3) / 1e12 if (f_n and face_ops) else None
     roofline = {
         "bound": "fp64",
-        "kernel": ("k_faces3d<x,y,z>" if args.case == "tgv3d" else "k_faces3<x>+k_faces3<y>")
+        "kernel": ("k_faces3d<x,y,z>" if args.case in ("tgv3d", "jet3d") else "k_faces3<x>+k_faces3<y>")
                   + " (inviscid face fluxes, one stage)",
         "ops_per_cell_stage": inv_ops,
         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
@@ -454,8 +463,9 @@ def main():
         "peak_source": "live DFMA-chain microbenchmark (ign_probe_fp64_peak), 2 flop/FMA",
         "whole_step": {
             "ops_per_cell_step": step_ops,
-            "fp64_tflops": value / world * step_ops / 1e12,
-            "fp64_frac": value / world * step_ops / 1e12 / peak.value if peak.value else None,
+            "fp64_tflops": value / world * step_ops / 1e12 if step_ops else None,
+            "fp64_frac": (value / world * step_ops / 1e12 / peak.value
+                          if step_ops and peak.value else None),
             "hbm_gbs": value / world * BYTES_PER_CELL_STEP(nc) / 1e9,
             "hbm_frac": value / world * BYTES_PER_CELL_STEP(nc) / 1e9 / 6451.8,
         },

@@ -421,6 +421,69 @@ def tgv3d(n: int = 256, *, viscous: bool = True, scheme: str = "teno6",
                 dict(p0=p0, c0=c0))
 
 
+def jet3d(nx: int = 512, ny: int = 256, nz: int = 32, *, scheme: str = "weno3z",
+          split: str = "comp", energy: float = 0.05) -> Case:
+    """BASELINE configs[3] in the form the 3D extension runs (SURVEY §8d config
+    D; no reference path): an H2/N2 jet (tanh-smoothed inflow segment, 100 m/s)
+    into air coflow (5 m/s) through a 4 cm x 2 cm channel — left inflow, right
+    outflow with LODI toward 1 atm, no-slip adiabatic walls at the y edges, z
+    periodic with dz = dx — one-step H2/O2 chemistry, the shaped laser kernel
+    focused in the shear layer; WENO3Z componentwise.  Weak
+    scaling stacks z: 512 x 256 x 32 per GPU, 512 x 256 x 256 on 8 GPUs."""
+    Lx, Ly = 0.04, 0.02
+    dx = Lx / nx
+    cfg = base_config(nx, ny, Lx, Ly, center=(0.5 * Lx, 0.0), periodic=(False, False))
+    cfg.nz, cfg.periodic_z, cfg.lz, cfg.center_z = nz, 1, dx * nz, 0.0
+    species = h2_o2_species()
+    fill_mixture(cfg.mix, species)
+    set_scheme(cfg, scheme, split)
+    cfg.viscous = 1
+    Ws = [sp.W for sp in species]
+    Yjet = [0.1, 0.0, 0.0, 0.9]
+    Yair = [0.0, 0.23, 0.0, 0.77]
+    d = 0.002  # jet half width
+    e = cfg.bc.left
+    e.type = abi.INFLOW
+    e.nseg = 3
+    e.smooth_width = 2e-4
+    for k, (lo, hi, u, Ys) in enumerate(((-0.5 * Ly, -d, 5.0, Yair), (-d, d, 100.0, Yjet),
+                                         (d, 0.5 * Ly, 5.0, Yair))):
+        sg = e.seg[k]
+        sg.lo, sg.hi, sg.u, sg.v, sg.T = lo, hi, u, 0.0, 300.0
+        for q in range(4):
+            sg.Y[q] = Ys[q]
+    cfg.bc.right.type = abi.OUTFLOW
+    cfg.bc.right.p_target = 101325.0
+    cfg.bc.bottom.type = cfg.bc.top.type = abi.NOSLIP_ADIABATIC
+    m = cfg.mech
+    m.present = 1
+    m.A, m.Ta, m.a, m.b, m.T_cutoff = 1e9, 15000.0, 1.0, 1.0, 300.0
+    m.i_fuel, m.i_ox, m.i_co2, m.i_h2o = 0, 1, -1, 2
+    for q, nu in enumerate((-2.0, -1.0, 2.0, 0.0)):
+        m.nu[q] = nu
+    la = cfg.laser
+    la.present = 1
+    la.kernel = abi.LASER_SHAPED
+    la.energy, la.sigma_r, la.sigma_t = energy, 5e-4, 1e-6
+    la.x0, la.y0, la.t0 = 0.01, d, 3e-6
+
+    def ic(X, Y, Z):
+        f = 0.5 * (np.tanh((Y + d) / 2e-4) - np.tanh((Y - d) / 2e-4))  # 1 in the jet
+        f = f * np.exp(-np.maximum(X, 0.0) / 0.005)                    # decaying core
+        Ys = [Yjet[q] * f + Yair[q] * (1 - f) for q in range(4)]
+        T = np.full_like(X, 300.0)
+        rbar = R_UNIVERSAL * sum(Ys[q] / Ws[q] for q in range(4))
+        rho = 101325.0 / (rbar * T)
+        # jet velocity with a weak spanwise perturbation so 3D structure develops
+        lz = cfg.lz
+        u = 5.0 + 95.0 * f * (1.0 + 0.02 * np.sin(2 * math.pi * Z / lz))
+        w = 2.0 * f * np.sin(2 * math.pi * X / 0.01)
+        return rho, u, np.zeros_like(X), w, T, Ys
+
+    c_max = 1300.0  # sound speed bound of the H2/N2 jet at 300 K
+    return Case(f"jet3d_{nx}x{ny}x{nz}", cfg, ic, 0.3 * dx / (c_max + 100.0))
+
+
 def extrude_z(case: Case, nz: int = 7) -> Case:
     """The z-extrusion cross-check of SURVEY §8c: a 2D periodic case on the 3D
     path with nz >= 2g+1 planes, dz = 1.0 exactly (lz = nz), w = 0 and data
