@@ -83,6 +83,7 @@ CASES3 = {
     "tgv3d_comp_weno3z_visc": lambda: configs.tgv3d(12, nz=18, scheme="weno3z", split="comp"),
     "h2o2_inflow_outflow_3d": lambda: configs.extrude_z(configs.h2o2_counterflow(12), 18),
     "wall_channel_3d": lambda: configs.extrude_z(configs.wall_channel(12), 18),
+    "jet3d_inflow_lodi_walls_laser": lambda: configs.jet3d(48, 24, 12),
 }
 
 
