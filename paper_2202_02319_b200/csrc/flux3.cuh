@@ -36,7 +36,7 @@ IGN_HD void conservative_from_primitives3(const Prim3<NS>& pt, const DMix& m, do
 }
 
 // primitives_from_conservative (state.hpp:26-44) + w
-template <int NS>
+template <int NS, bool BF = false>
 IGN_HD int primitives_from_conservative3(const double* U, const DMix& m, double T_guess,
                                          Prim3<NS>& pt, double* rs_out) {
     double rho = 0.0;
@@ -54,7 +54,7 @@ IGN_HD int primitives_from_conservative3(const double* U, const DMix& m, double 
         fdiv(U[NS + 3], rho, yr) - 0.5 * ((pt.u * pt.u + pt.v * pt.v) + pt.w * pt.w);
     const double rs = r_specific<NS>(pt.Y, m);
     int st;
-    pt.T = temperature_from_energy<NS>(e, pt.Y, rs, m, T_guess, &st);
+    pt.T = temperature_from_energy<NS, BF>(e, pt.Y, rs, m, T_guess, &st);
     if (st != T_OK) return st;
     pt.p = pt.rho * rs * pt.T;
     *rs_out = rs;

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
     for (int c = 0; c < NS + 3; ++c) U[c] = Ut[c * P.plane + id] * J;
     Prim<NS> pt;
     double rs;
-    const int st = primitives_from_conservative<NS>(U, P.mix, PT(P)[id], pt, &rs);
+    const int st = primitives_from_conservative<NS, true>(U, P.mix, PT(P)[id], pt, &rs);
     if (st) {
         report(P.err, stage, PH_PRIM, (unsigned long long)(id + (long long)P.j0 * P.sx), st,
                step);
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
     PV(P)[id] = pt.v;
     PP(P)[id] = pt.p;
     PT(P)[id] = pt.T;
-    PC(P)[id] = sound_speed_rs<NS>(pt.T, pt.Y, rs, P.mix);
+    PC(P)[id] = sound_speed_rs<NS, true>(pt.T, pt.Y, rs, P.mix);
 #pragma unroll
     for (int s = 0; s < NS; ++s) PY(P, s)[id] = pt.Y[s];
     if (WX) {

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) k_prim3(const __grid_constant__ KParams P
     for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
     Prim3<NS> pt;
     double rs;
-    const int st = primitives_from_conservative3<NS>(U, P.mix, PT3(P)[id], pt, &rs);
+    const int st = primitives_from_conservative3<NS, true>(U, P.mix, PT3(P)[id], pt, &rs);
     if (st) {
         report(P.err, stage, PH_PRIM, (unsigned long long)(id + (long long)P.j0 * P.sxy), st,
                step);
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) k_prim3(const __grid_constant__ KParams P
     PW3(P)[id] = pt.w;
     PP3(P)[id] = pt.p;
     PT3(P)[id] = pt.T;
-    PC3(P)[id] = sound_speed_rs<NS>(pt.T, pt.Y, rs, P.mix);
+    PC3(P)[id] = sound_speed_rs<NS, true>(pt.T, pt.Y, rs, P.mix);
 #pragma unroll
     for (int s = 0; s < NS; ++s) PY3(P, s)[id] = pt.Y[s];
     if (WX) {

@@ -78,10 +78,17 @@ static void check_mixture(const ignis::MixtureModel& mix, const char* name, unsi
         EXPECT_BITWISE(lbl, ign::cp_mass<NS>(T, Yp, dm), ignis::thermo::cp_mass(T, Y, mix));
         std::snprintf(lbl, sizeof lbl, "%s h_mass", name);
         EXPECT_BITWISE(lbl, ign::h_mass<NS>(T, Yp, dm), ignis::thermo::h_mass(T, Y, mix));
+        // the branch-free (full Horner) forms of the primitive kernels
+        std::snprintf(lbl, sizeof lbl, "%s cp_mass bf", name);
+        EXPECT_BITWISE(lbl, (ign::cp_mass<NS, true>(T, Yp, dm)), ignis::thermo::cp_mass(T, Y, mix));
+        std::snprintf(lbl, sizeof lbl, "%s h_mass bf", name);
+        EXPECT_BITWISE(lbl, (ign::h_mass<NS, true>(T, Yp, dm)), ignis::thermo::h_mass(T, Y, mix));
         const double rs = ign::r_specific<NS>(Yp, dm);
         EXPECT_BITWISE("r_specific", rs, ignis::thermo::r_specific(Y, mix));
         EXPECT_BITWISE("e_mass", ign::e_mass_rs<NS>(T, Yp, rs, dm), ignis::thermo::e_mass(T, Y, mix));
         EXPECT_BITWISE("sound_speed", ign::sound_speed_rs<NS>(T, Yp, rs, dm),
+                       ignis::thermo::sound_speed(T, Y, mix));
+        EXPECT_BITWISE("sound_speed bf", (ign::sound_speed_rs<NS, true>(T, Yp, rs, dm)),
                        ignis::thermo::sound_speed(T, Y, mix));
         EXPECT_BITWISE("mean_molar_mass", ign::mean_molar_mass<NS>(Yp, dm),
                        ignis::thermo::mean_molar_mass(Y, mix));
@@ -127,6 +134,14 @@ static void check_mixture(const ignis::MixtureModel& mix, const char* name, unsi
         EXPECT_BITWISE("prim T", bp.T, back.T);
         EXPECT_BITWISE("prim p", bp.p, back.p);
         EXPECT_BITWISE("prim u", bp.u, back.u);
+        ign::Prim<NS> bq;
+        double rsq;
+        if (ign::primitives_from_conservative<NS, true>(U.data(), dm, guess, bq, &rsq) == 0) {
+            EXPECT_BITWISE("prim T bf", bq.T, back.T);
+            EXPECT_BITWISE("prim p bf", bq.p, back.p);
+        } else {
+            ++g_fail;
+        }
         // Roe average + eigensystem (flux.hpp:55-186) between two random states
         ignis::SpeciesArray Y2{};
         double Y2p[NS], s2 = 0.0;
