@@ -367,7 +367,15 @@ __device__ void lodi_dfx3(const KParams& P, int j, int kz, double* dF) {
 }
 
 // ---------------------------------------------------------------- assemble + update
-template <int NS, int MODE>
+// laser_power out of line: the common (laser-free) update stays small
+static __device__ __noinline__ double laser_cold(double x, double y, double t, const DLaser& p) {
+    return laser_power(x, y, t, p);
+}
+
+// EDGE = false: every padded node except, when LODI is on, the right-edge
+// column; EDGE = true: that column alone (grid over its (j, k)), with the LODI
+// x-flux difference — so the LODI code never enters the bulk update.
+template <int NS, int MODE, bool EDGE>
 __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KParams P,
                                                    const double* __restrict__ U0,
                                                    const double* __restrict__ Ucur,
@@ -379,14 +387,26 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
     if (threadIdx.x == 0) s_clip = 0ull;
     __syncthreads();
     const bool dead = failed(P.err);
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long id;
+    bool in_range;
+    if (EDGE) {
+        const int t = blockIdx.x * blockDim.x + threadIdx.x;  // (j, k) of the column
+        in_range = t < P.ny * P.nz;
+        id = in_range ? pidx3(P, P.nx - 1, t % P.ny, t / P.ny) : 0;
+    } else {
+        id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        in_range = id < P.plane;
+    }
     double clip = 0.0;
-    if (!dead && id < P.plane) {
+    if (!dead && in_range) {
         const int ip = (int)(id % P.sx), jp = (int)((id / P.sx) % (P.ny + 2 * P.g));
         const int kp = (int)(id / P.sxy);
         const int i = ip - P.g, j = jp - P.g, k = kp - P.g;
         const bool interior = i >= 0 && i < P.nx && j >= 0 && j < P.ny && k >= 0 && k < P.nz;
-        if (!interior) {
+        const bool lodi = P.lodi && i == P.nx - 1;
+        if (!EDGE && interior && lodi) {
+            // the right-edge column is the EDGE launch's
+        } else if (!interior) {
             if (MODE != 0) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = Ucur[c * P.plane + id];
@@ -399,12 +419,11 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
             const long long fy = ((long long)k * (P.ny + 1) + j) * P.nx + i;
             const long long fz = ((long long)k * P.ny + j) * P.nx + i;
             double r[NC];
-            double dFl[NC];
-            const bool lodi = P.lodi && i == P.nx - 1;
-            if (lodi) lodi_dfx3<NS>(P, j, k, dFl);
+            double dFl[EDGE ? NC : 1];
+            if (EDGE) lodi_dfx3<NS>(P, j, k, dFl);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                const double dF = lodi ? dFl[c] : P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
+                const double dF = EDGE ? dFl[EDGE ? c : 0] : P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
                 const double dG = P.Gy[c * fyp + fy + P.nx] - P.Gy[c * fyp + fy];
                 const double dH = P.Hz[c * fzp + fz + (long long)P.nx * P.ny] - P.Hz[c * fzp + fz];
                 r[c] = -((dF + dG) + dH);
@@ -435,7 +454,7 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
             // reference's 2D kernel, uniform along z
             if (P.laser.on) {
                 const int q = (j + P.g) * P.sx + (i + P.g);
-                r[NS + 3] += laser_power(ldg(P.xc + q), ldg(P.yc + q), t_stage, P.laser) * invJ;
+                r[NS + 3] += laser_cold(ldg(P.xc + q), ldg(P.yc + q), t_stage, P.laser) * invJ;
             }
             const unsigned long long cell =
                 ((unsigned long long)(k + P.j0) * P.ny + j) * P.nx + i;
@@ -580,20 +599,29 @@ template <int NS> struct Launch3 {
         k_visc3<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, stage, step);
         return 1;
     }
+    template <bool EDGE>
+    static void assemble_t(const KParams& P, int mode, const double* U0, const double* Ucur,
+                           double* Uout, double dt, double w, double t_stage, int stage,
+                           int step, int clip_slot, unsigned nb, cudaStream_t s) {
+        if (mode == 0)
+            k_assemble3<NS, 0, EDGE><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage,
+                                                        step, clip_slot);
+        else if (mode == 1)
+            k_assemble3<NS, 1, EDGE><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage,
+                                                        step, clip_slot);
+        else
+            k_assemble3<NS, 2, EDGE><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage,
+                                                        step, clip_slot);
+    }
     static int assemble(const KParams& P, int mode, const double* U0, const double* Ucur,
                         double* Uout, double dt, double w, double t_stage, int stage, int step,
                         int clip_slot, cudaStream_t s) {
-        const unsigned nb = (unsigned)((P.plane + 255) / 256);
-        if (mode == 0)
-            k_assemble3<NS, 0><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
-                                                  clip_slot);
-        else if (mode == 1)
-            k_assemble3<NS, 1><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
-                                                  clip_slot);
-        else
-            k_assemble3<NS, 2><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
-                                                  clip_slot);
-        return 1;
+        assemble_t<false>(P, mode, U0, Ucur, Uout, dt, w, t_stage, stage, step, clip_slot,
+                          (unsigned)((P.plane + 255) / 256), s);
+        if (!P.lodi) return 1;
+        assemble_t<true>(P, mode, U0, Ucur, Uout, dt, w, t_stage, stage, step, clip_slot,
+                         (unsigned)((P.ny * P.nz + 255) / 256), s);
+        return 2;
     }
     static int dt(const KParams& P, cudaStream_t s) {
         const dim3 grid((unsigned)((P.nx * P.ny + 255) / 256), P.nz);
