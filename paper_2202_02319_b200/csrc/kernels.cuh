@@ -351,7 +351,15 @@ __device__ void lodi_dfx(const KParams& P, int j, double* dF) {
 // U <- U0 + dt r (axpy_interior :799-807).  MODE 2: U <- U0 + w((U-U0) + dt r)
 // (blend_interior :810-821).  MODE 1/2 also clip + validate (post_stage
 // :826-849) and carry the ghost ring of Ucur into Uout.
-template <int NS, int MODE>
+// laser_power out of line: the common (laser-free) update stays small
+static __device__ __noinline__ double laser_cold2(double x, double y, double t, const DLaser& p) {
+    return laser_power(x, y, t, p);
+}
+
+// EDGE = false: every padded node except, when LODI is on, the right-edge
+// column; EDGE = true: that column alone (grid over j), with the LODI x-flux
+// difference — the LODI code never enters the bulk update.
+template <int NS, int MODE, bool EDGE>
 __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParams P,
                                                   const double* __restrict__ U0,
                                                   const double* __restrict__ Ucur,
@@ -363,13 +371,24 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParam
     if (threadIdx.x == 0) s_clip = 0ull;
     __syncthreads();
     const bool dead = failed(P.err);
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long id;
+    bool in_range;
+    if (EDGE) {
+        const int t = blockIdx.x * blockDim.x + threadIdx.x;  // row j of the column
+        in_range = t < P.ny;
+        id = in_range ? pidx(P, P.nx - 1, t) : 0;
+    } else {
+        id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        in_range = id < P.plane;
+    }
     double clip = 0.0;
-    if (!dead && id < P.plane) {
+    if (!dead && in_range) {
         const int ip = (int)(id % P.sx), jp = (int)(id / P.sx);
         const int i = ip - P.g, j = jp - P.g;
         const bool interior = i >= 0 && i < P.nx && j >= 0 && j < P.ny;
-        if (!interior) {
+        if (!EDGE && interior && P.lodi && i == P.nx - 1) {
+            // the right-edge column is the EDGE launch's
+        } else if (!interior) {
             if (MODE != 0) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = Ucur[c * P.plane + id];
@@ -380,12 +399,11 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParam
             const long long fyp = (long long)P.nx * (P.ny + 1);
             const long long fx = (long long)j * (P.nx + 1) + i;
             const long long fy = (long long)j * P.nx + i;
-            double dFl[NC];
-            const bool lodi = P.lodi && i == P.nx - 1;
-            if (lodi) lodi_dfx<NS>(P, j, dFl);
+            double dFl[EDGE ? NC : 1];
+            if (EDGE) lodi_dfx<NS>(P, j, dFl);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                const double dF = lodi ? dFl[c] : P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
+                const double dF = EDGE ? dFl[EDGE ? c : 0] : P.Fx[c * fxp + fx + 1] - P.Fx[c * fxp + fx];
                 const double dG = P.Gy[c * fyp + fy + P.nx] - P.Gy[c * fyp + fy];
                 r[c] = -(dF + dG);
             }
@@ -410,7 +428,7 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParam
                 for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
             }
             if (P.laser.on)
-                r[NS + 2] += laser_power(ldg(P.xc + id), ldg(P.yc + id), t_stage, P.laser) * invJ;
+                r[NS + 2] += laser_cold2(ldg(P.xc + id), ldg(P.yc + id), t_stage, P.laser) * invJ;
             const unsigned long long cell = (unsigned long long)(j + P.j0) * P.nx + i;
             bool bad = false;
 #pragma unroll
@@ -548,20 +566,29 @@ template <int NS> struct Launch {
         k_visc<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, stage, step);
         return 1;
     }
+    template <bool EDGE>
+    static void assemble_t(const KParams& P, int mode, const double* U0, const double* Ucur,
+                           double* Uout, double dt, double w, double t_stage, int stage,
+                           int step, int clip_slot, unsigned nb, cudaStream_t s) {
+        if (mode == 0)
+            k_assemble<NS, 0, EDGE><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage,
+                                                       step, clip_slot);
+        else if (mode == 1)
+            k_assemble<NS, 1, EDGE><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage,
+                                                       step, clip_slot);
+        else
+            k_assemble<NS, 2, EDGE><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage,
+                                                       step, clip_slot);
+    }
     static int assemble(const KParams& P, int mode, const double* U0, const double* Ucur,
                         double* Uout, double dt, double w, double t_stage, int stage, int step,
                         int clip_slot, cudaStream_t s) {
-        const unsigned nb = (unsigned)((P.plane + 255) / 256);
-        if (mode == 0)
-            k_assemble<NS, 0><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
-                                                 clip_slot);
-        else if (mode == 1)
-            k_assemble<NS, 1><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
-                                                 clip_slot);
-        else
-            k_assemble<NS, 2><<<nb, 256, 0, s>>>(P, U0, Ucur, Uout, dt, w, t_stage, stage, step,
-                                                 clip_slot);
-        return 1;
+        assemble_t<false>(P, mode, U0, Ucur, Uout, dt, w, t_stage, stage, step, clip_slot,
+                          (unsigned)((P.plane + 255) / 256), s);
+        if (!P.lodi) return 1;
+        assemble_t<true>(P, mode, U0, Ucur, Uout, dt, w, t_stage, stage, step, clip_slot,
+                         (unsigned)((P.ny + 255) / 256), s);
+        return 2;
     }
     static int dt(const KParams& P, cudaStream_t s) {
         const long long n = (long long)P.nx * P.ny;
