@@ -38,7 +38,7 @@ __device__ int bc_prim_at(const KParams& P, const double* Ut, int i, int j, Prim
     double U[NS + 3];
 #pragma unroll
     for (int c = 0; c < NS + 3; ++c) U[c] = Ut[c * P.plane + id] * J;
-    return primitives_from_conservative<NS>(U, P.mix, 300.0, pt, &rs);
+    return primitives_from_conservative<NS, true>(U, P.mix, 300.0, pt, &rs);
 }
 
 template <int NS>

@@ -26,7 +26,7 @@ __device__ int bc3_prim_at(const KParams& P, const double* Ut, int i, int j, int
     double U[NS + 4];
 #pragma unroll
     for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
-    return primitives_from_conservative3<NS>(U, P.mix, 300.0, pt, &rs);
+    return primitives_from_conservative3<NS, true>(U, P.mix, 300.0, pt, &rs);
 }
 
 template <int NS>
