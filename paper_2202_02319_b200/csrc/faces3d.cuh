@@ -444,11 +444,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                     wp[k] = 0.5 * (lf[k] + alpha * lu[k]);
                     wm[k] = 0.5 * (lf[k] - alpha * lu[k]);
                 }
-#ifdef IGN_EXP_NOTENO
-                amp = 0.5 * (wp[H - 1] + wm[H]);
-#else
                 amp = face_pm<TENO>(wp, wm, P.rp);
-#endif
             }
         }
         S.amp[fl][face] = amp;
