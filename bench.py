@@ -3,7 +3,7 @@
 "FP64 cell-updates/s per RK step").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--case tgv3d|tgv|h2o2] [--n N]
+                    [--case tgv3d|tgv|h2o2|ensemble|jet3d] [--size N]
 
 A "step" is one full SSP-RK3 step (three RHS evaluations + updates + the
 advance-loop prepare_stage(1), solver.hpp:304-345) over the whole grid.
@@ -325,7 +325,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=None,
+    ap.add_argument("--size", "--n", dest="n", type=int, default=None,
                     help="cells per side (default 256 for tgv3d, 4096 tgv, 512 h2o2)")
     ap.add_argument("--case", default="tgv3d",
                     choices=["tgv3d", "tgv", "h2o2", "ensemble", "jet3d"])
