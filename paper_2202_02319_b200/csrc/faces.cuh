@@ -31,22 +31,28 @@
 
 namespace ign {
 
-template <int NS, int DIR, bool TENO> struct FaceSmem {
+// CHAR = false (componentwise) needs only the node window and one LLF speed
+// per face: the characteristic tables shrink to one row so more CTAs fit
+template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
     static constexpr int NC = NS + 3;
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;  // faces per CTA
     // x: up to two row segments of the flattened face order (see k_faces3)
     static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
-    static constexpr int NE = 14 + 2 * NS;
+    static constexpr int NE_CHAR = 14 + 2 * NS;
+    static constexpr int NE = CHAR ? NE_CHAR : 1;
     static constexpr int NV = 2 * W;  // stencil vectors: F and U of each node
+    static constexpr int NV_S = CHAR ? NV : 1;   // projection table rows
+    static constexpr int NA_S = CHAR ? NC : 1;   // amplitude table rows
+    static constexpr int NK_S = CHAR ? 3 : 1;    // LLF speed kinds
     double U[NC][NT];
     double F[NC][NT];
     double u[NT], v[NT], c[NT];
     double E[NE][NF];         // eigen data per face (char); [0] alpha, [1] sf (comp)
-    double L[NV][3][32];      // dp, dun, dut of one group's vectors
-    double amp[NC][NF];
-    double alpha[3][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
+    double L[NV_S][3][32];      // dp, dun, dut of one group's vectors
+    double amp[NA_S][NF];
+    double alpha[NK_S][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
     int bad[NF];
 };
 
@@ -74,7 +80,7 @@ template <int NS, int DIR, bool TENO, bool CHAR>
 #endif
 __global__ void __launch_bounds__(32 * (NS + 3), (NS == 1 ? IGN_FACES_MINB : 1))
 k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {
-    using Smem = FaceSmem<NS, DIR, TENO>;
+    using Smem = FaceSmem<NS, DIR, TENO, CHAR>;
     constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
     constexpr int NV = Smem::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -450,7 +456,7 @@ template <int NS, int DIR, bool TENO, bool CHAR>
 inline void launch_faces3(const KParams& P, const double* Ut, int stage, int step,
                           cudaStream_t s) {
     constexpr int NC = NS + 3;
-    const size_t smem = sizeof(FaceSmem<NS, DIR, TENO>);
+    const size_t smem = sizeof(FaceSmem<NS, DIR, TENO, CHAR>);
     auto kern = k_faces3<NS, DIR, TENO, CHAR>;
     static bool configured = false;  // per instantiation
     if (!configured) {

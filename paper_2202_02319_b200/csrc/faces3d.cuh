@@ -18,7 +18,9 @@ __device__ __forceinline__ long long pidx3(const KParams& P, int i, int j, int k
     return (long long)(k + P.g) * P.sxy + (long long)(j + P.g) * P.sx + (i + P.g);
 }
 
-template <int NS, int DIR, bool TENO> struct FaceSmem3 {
+// CHAR = false (componentwise) needs only the node window and one LLF speed
+// per face: the characteristic tables shrink to one row so more CTAs fit
+template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     static constexpr int NC = NS + 4;
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
@@ -27,17 +29,21 @@ template <int NS, int DIR, bool TENO> struct FaceSmem3 {
     static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
     // eigen table rows: 12 common + Y, Theta + the direction's own (n1, n2, ut1
     // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w)
-    static constexpr int NE = 12 + 2 * NS + (DIR < 2 ? 3 : 1);
+    static constexpr int NE_CHAR = 12 + 2 * NS + (DIR < 2 ? 3 : 1);
+    static constexpr int NE = CHAR ? NE_CHAR : 1;
     static constexpr int NV = 2 * W;
+    static constexpr int NV_S = CHAR ? NV : 1;   // projection table rows
+    static constexpr int NA_S = CHAR ? NC : 1;   // amplitude table rows
+    static constexpr int NK_S = CHAR ? 3 : 1;    // LLF speed kinds
     static constexpr int NVEL = DIR < 2 ? 2 : 1;  // wave speed: (u, v) or w
     double U[NC][NT];
     double F[NC][NT];
     double vel[NVEL][NT];
     double c[NT];
     double E[NE][NF];
-    double L[NV][4][32];  // dp, dun, dut1, dut2
-    double amp[NC][NF];
-    double alpha[3][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
+    double L[NV_S][4][32];  // dp, dun, dut1, dut2
+    double amp[NA_S][NF];
+    double alpha[NK_S][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
     int bad[NF];
 };
 
@@ -80,7 +86,7 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
 template <int NS, int DIR, bool TENO, bool CHAR>
 __global__ void __launch_bounds__(32 * (NS + 4))
 k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {
-    using Smem = FaceSmem3<NS, DIR, TENO>;
+    using Smem = FaceSmem3<NS, DIR, TENO, CHAR>;
     constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
     constexpr int NV = Smem::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -512,7 +518,7 @@ template <int NS, int DIR, bool TENO, bool CHAR>
 inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int step,
                            cudaStream_t s) {
     constexpr int NC = NS + 4;
-    const size_t smem = sizeof(FaceSmem3<NS, DIR, TENO>);
+    const size_t smem = sizeof(FaceSmem3<NS, DIR, TENO, CHAR>);
     auto kern = k_faces3d<NS, DIR, TENO, CHAR>;
     static bool configured = false;
     if (!configured) {
