@@ -302,6 +302,8 @@ DMix build_mix(const ign_mixture& mx) {
                        : 0;
         d._pad = 0;
     }
+    m.all_simple = 1;
+    for (int s = 0; s < mx.ns; ++s) m.all_simple &= m.sp[s].simple;
     // W-only factors of Wilke's rule (thermo.hpp:249-251), same glibc calls
     for (int i = 0; i < mx.ns; ++i)
         for (int j = 0; j < mx.ns; ++j) {
