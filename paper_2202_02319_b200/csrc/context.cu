@@ -304,7 +304,12 @@ struct DevFail {
     int step = 0;
 };
 
+void t_errsync(const Team& T);
+
+// Every rank reads the same (MIN-reduced) error word: a failure in the last
+// kernels before this point (e.g. a step's final update) is seen everywhere.
 DevFail sync_and_read(const Team& T) {
+    t_errsync(T);
     cuda_check(cudaStreamSynchronize(T.stream()), "kernel execution");
     cuda_check(cudaGetLastError(), "kernel launch");
     for (ign_context* c : T.m) prof_harvest(c);
