@@ -461,6 +461,12 @@ def main():
         "ops_per_launch": face_ops, "avg_launch_ms": f_ms / f_n if f_n else None,
         "share_of_step": f_ms / total_prof if total_prof else None,
         "peak_source": "live DFMA-chain microbenchmark (ign_probe_fp64_peak), 2 flop/FMA",
+        # bitwise parity forbids contracting the reference's a*b+c into FMAs
+        # (-fmad=false): every algorithmic op issues as one DADD/DMUL, whose
+        # instruction peak is half the FMA flop peak
+        "peak_no_fma": peak.value / 2 if peak.value else None,
+        "frac_of_no_fma_peak": (achieved / (peak.value / 2)
+                                if achieved and peak.value else None),
         "whole_step": {
             "ops_per_cell_step": step_ops,
             "fp64_tflops": value / world * step_ops / 1e12 if step_ops else None,
