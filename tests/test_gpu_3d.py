@@ -302,3 +302,21 @@ def test_jet3d_runs_and_develops_3d_structure(cuda_device):
     assert np.isfinite(T).all() and T.min() > 250.0
     assert np.abs(c["w"][g:-g, g:-g, g:-g]).max() > 0.0
     assert sim.iter == 60
+
+
+def test_3d_state_failure_location(cuda_device):
+    """A non-positive density in a 3D state raises StepFailure at prepare time
+    with the node's (i, j) and its plane k in the message (the reference's
+    error kinds; ign_error carries i, j)."""
+    from paper_2202_02319_b200 import errors
+    case = configs.tgv3d(12)
+    sim = Simulation(case.cfg)
+    sim.set_initial_condition(case.ic)
+    U = sim.Ut
+    U[0, 3 + 4, 3 + 5, 3 + 6] = -1.0  # node (i=6, j=5, k=4)
+    sim.set_state(U)
+    with pytest.raises(errors.StepFailure) as ei:
+        sim.prepare_stage(2)
+    e = ei.value
+    assert (e.stage, e.i, e.j) == (2, 6, 5)
+    assert "k=4" in str(e)
