@@ -306,11 +306,16 @@ int ign_ensemble_rk3_steps(ign_context** members, int n, const double* dt, int64
 /* Simulation::add_probe (solver.hpp:130-135): inclusive interior box in
  * global cell indices; ConfigError when out of range (2D only). */
 int ign_add_probe(ign_context* ctx, int32_t i0, int32_t j0, int32_t i1, int32_t j1);
+/* 3D extension: box [i0,i1] x [j0,j1] x [k0,k1] (global k), sampled k-outermost;
+ * rows are rho, u, v, w, p, T, Y_s (6 + ns values). */
+int ign_add_probe3(ign_context* ctx, int32_t i0, int32_t j0, int32_t k0, int32_t i1, int32_t j1,
+                   int32_t k1);
 /* probe_interval / trace_interval (solver.hpp:71-73): advance() samples the
  * probes and the product-fraction trace every k-th iteration (0 = off). */
 int ign_set_sampling(ign_context* ctx, int32_t probe_interval, int32_t trace_interval);
 /* ProbeSeries (solver.hpp:42-46): n samples; times[n], rows[n][5+ns] =
- * box means of rho, u, v, p, T, Y_s.  NULL arrays: query n only. */
+ * box means of rho, u, v, p, T, Y_s (3D: rows[n][6+ns] with w after v).
+ * NULL arrays: query n only. */
 int ign_probe_samples(const ign_context* ctx, int32_t probe, int64_t* n, double* times,
                       double* rows);
 /* TraceSeries product_fraction (solver.hpp:48-51, 379-384) */

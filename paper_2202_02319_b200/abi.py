@@ -196,6 +196,7 @@ PRODUCT_ONLY = {
     "group_write_snapshot": (_I, [_P, C.c_char_p, _I, _I]),
     "group_read_snapshot": (_I, [_P, C.c_char_p]),
     "write_snapshot_v2": (_I, [_P, C.c_char_p, _I]),
+    "add_probe3": (_I, [_P] + [C.c_int32] * 6),
     "ensemble_rk3_steps": (_I, [C.POINTER(_P), _I, _D, C.c_int64, C.POINTER(C.c_int)]),
 }
 IGN_NCCL_ID_BYTES = 128

@@ -267,6 +267,20 @@ int ign_add_probe(ign_context* ctx, int32_t i0, int32_t j0, int32_t i1, int32_t 
     });
 }
 
+int ign_add_probe3(ign_context* ctx, int32_t i0, int32_t j0, int32_t k0, int32_t i1, int32_t j1,
+                   int32_t k1) {
+    return guarded_err(&ctx->lasterr, ctx->device, [&] {
+        if (ctx->nz == 0) throw usage_error("probes: ign_add_probe3 is for 3D contexts");
+        if (i0 < 0 || j0 < 0 || k0 < 0 || i1 >= ctx->nx || j1 >= ctx->ny || k1 >= ctx->nz_glob ||
+            i0 > i1 || j0 > j1 || k0 > k1)
+            throw config_error("probe box out of range");
+        ign_context::Probe p{i0, j0, i1, j1, {}, {}};
+        p.k0 = k0;
+        p.k1 = k1;
+        ctx->probes.push_back(p);
+    });
+}
+
 int ign_set_sampling(ign_context* ctx, int32_t probe_interval, int32_t trace_interval) {
     ctx->probe_interval = probe_interval;
     ctx->trace_interval = trace_interval;

@@ -74,6 +74,7 @@ struct ign_context {
     int probe_interval = 0, trace_interval = 0;
     struct Probe {
         int i0, j0, i1, j1;  // inclusive interior box, GLOBAL indices
+        int k0 = 0, k1 = 0;  // 3D extension: global plane range
         std::vector<double> times, rows;
     };
     std::vector<Probe> probes;

@@ -140,6 +140,28 @@ __global__ void k_probe(const double* __restrict__ prim, long long plane, int sx
     out[q] = acc;
 }
 
+__global__ void k_probe3(const double* __restrict__ prim, long long plane, int sx, long long sxy,
+                         int g, int ns, int i0, int j0, int k0, int i1, int j1, int k1,
+                         const double* __restrict__ init, double* __restrict__ out) {
+    const int q = threadIdx.x;
+    if (q >= 6 + ns) return;
+    // rho, u, v, w, p, T, then Y_s (3D cache slots 0..5, 7 + s; slot 6 is c)
+    const double* f = prim + (q < 6 ? q : q + 1) * plane;
+    double acc = init[q];
+    for (int k = k0; k <= k1; ++k)
+        for (int j = j0; j <= j1; ++j) {
+            const double* row = f + (long long)(k + g) * sxy + (long long)(j + g) * sx + g;
+            for (int i = i0; i <= i1; ++i) acc += row[i];
+        }
+    out[q] = acc;
+}
+
+void launch_probe3(const double* prim, long long plane, int sx, long long sxy, int g, int ns,
+                   int i0, int j0, int k0, int i1, int j1, int k1, const double* init,
+                   double* out, cudaStream_t s) {
+    k_probe3<<<1, 32, 0, s>>>(prim, plane, sx, sxy, g, ns, i0, j0, k0, i1, j1, k1, init, out);
+}
+
 void launch_probe(const double* prim, long long plane, int sx, int g, int ns, int i0, int j0,
                   int i1, int j1, const double* init, double* out, cudaStream_t s) {
     k_probe<<<1, 32, 0, s>>>(prim, plane, sx, g, ns, i0, j0, i1, j1, init, out);

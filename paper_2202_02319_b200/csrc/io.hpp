@@ -40,5 +40,10 @@ Snapshot snapshot_read(const std::string& path);
 // thread per quantity, so every sum is the serial one.  Writes `out`.
 void launch_probe(const double* prim, long long plane, int sx, int g, int ns, int i0, int j0,
                   int i1, int j1, const double* init, double* out, cudaStream_t s);
+// 3D extension: k-outermost box over local planes [k0, k1], 6 + ns values
+// (rho, u, v, w, p, T, Y_s); sxy = padded (x, y) plane size
+void launch_probe3(const double* prim, long long plane, int sx, long long sxy, int g, int ns,
+                   int i0, int j0, int k0, int i1, int j1, int k1, const double* init,
+                   double* out, cudaStream_t s);
 
 }  // namespace ign

@@ -124,25 +124,34 @@ void t_sample(const Team& T) {
     const bool want_probe = L->probe_interval > 0 && (L->iter % L->probe_interval == 0);
     const bool want_trace = L->trace_interval > 0 && (L->iter % L->trace_interval == 0);
     if (want_probe) {
-        const int nq = 5 + L->ns;
+        const bool three_d = L->nz > 0;
+        const int nq = (three_d ? 6 : 5) + L->ns;
         double* d = dalloc(2 * static_cast<size_t>(nq));
         try {
             for (auto& pr : L->probes) {
                 std::vector<double> row(nq, 0.0);
                 fold_ranks(T, row, [&](ign_context* c, std::vector<double>& a) {
-                    const int jlo = std::max(pr.j0, c->mesh.j0);
-                    const int jhi = std::min(pr.j1, c->mesh.j0 + c->ny - 1);
-                    if (jlo > jhi) return;
+                    // this slab's share of the box: 2D y rows, 3D z planes
+                    const int off = three_d ? c->k0 : c->mesh.j0;
+                    const int cnt = three_d ? c->nz : c->ny;
+                    const int lo = std::max(three_d ? pr.k0 : pr.j0, off);
+                    const int hi = std::min(three_d ? pr.k1 : pr.j1, off + cnt - 1);
+                    if (lo > hi) return;
                     cuda_check(cudaMemcpyAsync(d, a.data(), nq * 8, cudaMemcpyHostToDevice,
                                                c->stream), "probe");
-                    launch_probe(c->prim, (long long)c->plane, c->kp.sx, c->g, c->ns, pr.i0,
-                                 jlo - c->mesh.j0, pr.i1, jhi - c->mesh.j0, d, d + nq, c->stream);
+                    if (three_d)
+                        launch_probe3(c->prim, (long long)c->plane, c->kp.sx, c->kp.sxy, c->g,
+                                      c->ns, pr.i0, pr.j0, lo - off, pr.i1, pr.j1, hi - off, d,
+                                      d + nq, c->stream);
+                    else
+                        launch_probe(c->prim, (long long)c->plane, c->kp.sx, c->g, c->ns, pr.i0,
+                                     lo - off, pr.i1, hi - off, d, d + nq, c->stream);
                     c->launches += 1;
                     cuda_check(cudaMemcpyAsync(a.data(), d + nq, nq * 8, cudaMemcpyDeviceToHost,
                                                c->stream), "probe");
                     cuda_check(cudaStreamSynchronize(c->stream), "probe");
                 });
-                const int n = (pr.i1 - pr.i0 + 1) * (pr.j1 - pr.j0 + 1);
+                const int n = (pr.i1 - pr.i0 + 1) * (pr.j1 - pr.j0 + 1) * (pr.k1 - pr.k0 + 1);
                 for (auto& x : row) x /= n;
                 pr.times.push_back(L->time);
                 pr.rows.insert(pr.rows.end(), row.begin(), row.end());

@@ -234,6 +234,10 @@ class Simulation:
         """Simulation::add_probe (solver.hpp:130-135), ProbeSpec{i0, j0, i1, j1}."""
         self._check(self._api["add_probe"](self._h, i0, j0, i1, j1))
 
+    def add_probe3(self, i0: int, j0: int, k0: int, i1: int, j1: int, k1: int):
+        """3D extension: probe box over global planes k0..k1 (rows add w)."""
+        self._check(self._api["add_probe3"](self._h, i0, j0, k0, i1, j1, k1))
+
     def set_sampling(self, probe_interval: int = 0, trace_interval: int = 0):
         """probe_interval / trace_interval (solver.hpp:71-73)."""
         self._check(self._api["set_sampling"](self._h, probe_interval, trace_interval))
@@ -243,7 +247,7 @@ class Simulation:
         n = C.c_int64()
         self._check(self._api["probe_samples"](self._h, k, C.byref(n), None, None))
         t = np.empty(n.value)
-        r = np.empty((n.value, 5 + self.ns))
+        r = np.empty((n.value, (6 if self.nz else 5) + self.ns))
         self._check(self._api["probe_samples"](self._h, k, C.byref(n), _dptr(t), _dptr(r)))
         return t, r
 
@@ -382,7 +386,8 @@ class SlabGroup:
         n = C.c_int64()
         self.lead_call("probe_samples", k, C.byref(n), None, None)
         t = np.empty(n.value)
-        r = np.empty((n.value, 5 + self.members[0].ns))
+        m0 = self.members[0]
+        r = np.empty((n.value, (6 if m0.nz else 5) + m0.ns))
         self.lead_call("probe_samples", k, C.byref(n), _dptr(t), _dptr(r))
         return t, r
 

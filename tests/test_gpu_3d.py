@@ -320,3 +320,45 @@ def test_3d_state_failure_location(cuda_device):
     e = ei.value
     assert (e.stage, e.i, e.j) == (2, 6, 5)
     assert "k=4" in str(e)
+
+
+def test_3d_probes_match_2d_oracle_on_one_plane(oracle_api, cuda_device):
+    """A 3D probe box on a single z plane of an extruded case samples exactly
+    the 2D oracle's box means (rows gain w = 0); a full-depth box over z-slabs
+    equals the undecomposed run's."""
+    from paper_2202_02319_b200.sim import SlabGroup
+    case = configs.tgv2d(24)
+    refs = Simulation(clone_cfg(case.cfg), oracle_api)
+    refs.set_initial_condition(case.ic)
+    case3 = configs.extrude_z(case, NZ)
+    p3 = Simulation(clone_cfg(case3.cfg))
+    p3.set_state(configs.state_2d_to_3d(refs.Ut, refs.ns, NZ))
+    boxes = [(0, 0, 23, 23), (3, 5, 9, 12)]
+    for b in boxes:
+        refs.add_probe(*b)
+        p3.add_probe3(b[0], b[1], 2, b[2], b[3], 2)
+    for s in (refs, p3):
+        s.set_sampling(2, 0)
+        s.set_integrator(fixed_dt=case.dt, t_end=4.5 * case.dt)
+        s.advance()
+    for k in range(len(boxes)):
+        (ta, ra), (tb, rb) = p3.probe(k), refs.probe(k)
+        assert np.array_equal(ta, tb)
+        assert not np.any(ra[:, 3])  # w
+        assert same_values(np.delete(ra, 3, axis=1), rb)
+    # full-depth box over z-slabs vs the single domain
+    c3 = configs.tgv3d(12, nz=18)
+    single = Simulation(clone_cfg(c3.cfg))
+    single.set_initial_condition(c3.ic)
+    grp = SlabGroup(c3.cfg, 3)
+    U0 = single.Ut
+    for r in range(3):
+        grp.set_state(r, U0[:, 6 * r:6 * r + 12])
+    for s in (single, grp):
+        s.lead_call("add_probe3", 1, 2, 0, 10, 9, 17) if s is grp else s.add_probe3(1, 2, 0, 10, 9, 17)
+        s.set_sampling(1, 0)
+        s.set_integrator(fixed_dt=c3.dt, t_end=2.5 * c3.dt)
+        s.advance()
+    (ta, ra), (tb, rb) = single.probe(0), grp.probe(0)
+    assert np.array_equal(ta, tb) and np.array_equal(ra.view(np.uint64), rb.view(np.uint64))
+    grp.close()
