@@ -27,9 +27,10 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     static constexpr int NF = 32 * NC;
     // x: up to two row segments of the flattened face order (see k_faces3d)
     static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
-    // eigen table rows: 12 common + Y, Theta + the direction's own (n1, n2, ut1
-    // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w)
-    static constexpr int NE_CHAR = 12 + 2 * NS + (DIR < 2 ? 3 : 1);
+    // eigen table rows: 11 common + Y, Theta + the direction's own (n1, n2
+    // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w;
+    // un and ut1 are recomputed from them by the eigensystem's own expressions)
+    static constexpr int NE_CHAR = 11 + 2 * NS + (DIR < 2 ? 2 : 1);
     static constexpr int NE = CHAR ? NE_CHAR : 1;
     static constexpr int NV = 2 * W;
     static constexpr int NV_S = CHAR ? NV : 1;   // projection table rows
@@ -44,11 +45,11 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     double L[NV_S][4][32];  // dp, dun, dut1, dut2
     double amp[NA_S][NF];
     double alpha[NK_S][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
-    int bad[NF];
+    unsigned char bad[NF];
 };
 
 enum : int {
-    F3S = 0, F3U, F3V, F3W, F3UN, F3K, F3H, F3C, F3C2, F3KAPPA, F3YC2, F3YKAPPA, F3Y0
+    F3S = 0, F3U, F3V, F3W, F3K, F3H, F3C, F3C2, F3KAPPA, F3YC2, F3YKAPPA, F3Y0
 };
 
 // direction-specific eigen rows (FaceSmem3::E): ut2 is w (xi/eta) or v
@@ -64,8 +65,14 @@ template <int NS, int DIR> struct ERow {
     template <class Sm> __device__ static double n3(const Sm& S, int f) {
         return DIR == 2 ? S.E[X0][f] : 0.0;
     }
+    // EigenSystem::at_state's un and ut1 (flux3.cuh eigen_at_state3), same
+    // operations on the same stored values
+    template <class Sm> __device__ static double un(const Sm& S, int f) {
+        return DIR < 2 ? n1(S, f) * S.E[F3U][f] + n2(S, f) * S.E[F3V][f]
+                       : n3(S, f) * S.E[F3W][f];
+    }
     template <class Sm> __device__ static double ut1(const Sm& S, int f) {
-        return DIR < 2 ? S.E[X0 + 2][f] : S.E[F3U][f];
+        return DIR < 2 ? -n2(S, f) * S.E[F3U][f] + n1(S, f) * S.E[F3V][f] : S.E[F3U][f];
     }
     template <class Sm> __device__ static double ut2(const Sm& S, int f) {
         return DIR < 2 ? S.E[F3W][f] : S.E[F3V][f];
@@ -83,8 +90,11 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
     return (g + k) * 32 + lane;
 }
 
+#ifndef IGN_X_MINB
+#define IGN_X_MINB 1
+#endif
 template <int NS, int DIR, bool TENO, bool CHAR>
-__global__ void __launch_bounds__(32 * (NS + 4))
+__global__ void __launch_bounds__(32 * (NS + 4), (NS == 1 && DIR == 0 && CHAR) ? IGN_X_MINB : 1)
 k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {
     using Smem = FaceSmem3<NS, DIR, TENO, CHAR>;
     constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
@@ -258,8 +268,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 bad = 1;
             }
             const int t = threadIdx.x;
-            const double vals[F3Y0] = {es.s, es.u,  es.v,     es.w,   es.un,     es.k,
-                                       es.H, es.c,  es.c2,    es.kappa, es.yc2, es.ykappa};
+            const double vals[F3Y0] = {es.s, es.u,  es.v,     es.w,   es.k,     es.H,
+                                       es.c, es.c2, es.kappa, es.yc2, es.ykappa};
 #pragma unroll
             for (int q = 0; q < F3Y0; ++q) S.E[q][t] = vals[q];
 #pragma unroll
@@ -271,7 +281,6 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             if (DIR < 2) {
                 S.E[X0][t] = es.n1;
                 S.E[X0 + (DIR < 2 ? 1 : 0)][t] = es.n2;
-                S.E[X0 + (DIR < 2 ? 2 : 0)][t] = es.ut1;
             } else {
                 S.E[X0][t] = es.n3;
             }
@@ -340,7 +349,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                      ew = S.E[F3W][face];
         using ER = ERow<NS, DIR>;
         const double n1 = ER::n1(S, face), n2 = ER::n2(S, face), n3 = ER::n3(S, face);
-        const double un = S.E[F3UN][face], ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
+        const double un = ER::un(S, face), ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
         // (kap eu) q_u etc.: the reference's left-to-right products, hoisted
         const double keu = kap * eu, kev = kap * ev, kew = kap * ew;
         // the three distinct LLF wave speeds of the face (solver.hpp:555-566;
@@ -495,7 +504,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 r = DIR < 2 ? w * am + w * ap + w * asum + at2
                             : (w - c * n3) * am + (w + c * n3) * ap + w * asum;
             } else {  // E
-                const double Hh = S.E[F3H][face], un = S.E[F3UN][face];
+                const double Hh = S.E[F3H][face], un = ER::un(S, face);
                 const double ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
                 const double kk = S.E[F3K][face], kappa = S.E[F3KAPPA][face];
                 const double ykappa = S.E[F3YKAPPA][face];
