@@ -27,10 +27,10 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     static constexpr int NF = 32 * NC;
     // x: up to two row segments of the flattened face order (see k_faces3d)
     static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
-    // eigen table rows: 11 common + Y, Theta + the direction's own (n1, n2
+    // eigen table rows: 10 common + Y, Theta + the direction's own (n1, n2
     // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w;
-    // un and ut1 are recomputed from them by the eigensystem's own expressions)
-    static constexpr int NE_CHAR = 11 + 2 * NS + (DIR < 2 ? 2 : 1);
+    // un, ut1 and k are recomputed by the eigensystem's own expressions)
+    static constexpr int NE_CHAR = 10 + 2 * NS + (DIR < 2 ? 2 : 1);
     static constexpr int NE = CHAR ? NE_CHAR : 1;
     static constexpr int NV = 2 * W;
     static constexpr int NV_S = CHAR ? NV : 1;   // projection table rows
@@ -49,7 +49,7 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
 };
 
 enum : int {
-    F3S = 0, F3U, F3V, F3W, F3K, F3H, F3C, F3C2, F3KAPPA, F3YC2, F3YKAPPA, F3Y0
+    F3S = 0, F3U, F3V, F3W, F3H, F3C, F3C2, F3KAPPA, F3YC2, F3YKAPPA, F3Y0
 };
 
 // direction-specific eigen rows (FaceSmem3::E): ut2 is w (xi/eta) or v
@@ -268,8 +268,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 bad = 1;
             }
             const int t = threadIdx.x;
-            const double vals[F3Y0] = {es.s, es.u,  es.v,     es.w,   es.k,     es.H,
-                                       es.c, es.c2, es.kappa, es.yc2, es.ykappa};
+            const double vals[F3Y0] = {es.s,     es.u,   es.v,     es.w,  es.H,
+                                       es.c,     es.c2,  es.kappa, es.yc2, es.ykappa};
 #pragma unroll
             for (int q = 0; q < F3Y0; ++q) S.E[q][t] = vals[q];
 #pragma unroll
@@ -506,7 +506,9 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             } else {  // E
                 const double Hh = S.E[F3H][face], un = ER::un(S, face);
                 const double ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
-                const double kk = S.E[F3K][face], kappa = S.E[F3KAPPA][face];
+                // EigenSystem's k (eigen_at_state3), from the stored velocity
+                const double kk = 0.5 * ((u * u + v * v) + w * w);
+                const double kappa = S.E[F3KAPPA][face];
                 const double ykappa = S.E[F3YKAPPA][face];
                 double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut1 * at1;
                 en = en + ut2 * at2;
