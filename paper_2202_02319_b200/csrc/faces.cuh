@@ -40,7 +40,7 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
     static constexpr int NF = 32 * NC;  // faces per CTA
     // x: up to two row segments of the flattened face order (see k_faces3)
     static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
-    static constexpr int NE_CHAR = 14 + 2 * NS;
+    static constexpr int NE_CHAR = 11 + 2 * NS;
     static constexpr int NE = CHAR ? NE_CHAR : 1;
     static constexpr int NV = 2 * W;  // stencil vectors: F and U of each node
     static constexpr int NV_S = CHAR ? NV : 1;   // projection table rows
@@ -58,11 +58,22 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
 
 // Eigen data slots in FaceSmem::E
 enum : int {
-    EN1 = 0, EN2, ES, EU, EV, EUN, EUT, EK, EH, EC, EC2, EKAPPA, EYC2, EYKAPPA,
-    EY0  // then Y[NS], Theta[NS]
+    EN1 = 0, EN2, ES, EU, EV, EH, EC, EC2, EKAPPA, EYC2, EYKAPPA,
+    EY0  // then Y[NS], Theta[NS]; un, ut and k are recomputed (eigen_un etc.)
 };
 
-// window node of stencil slot k for lane of group g
+// EigenSystem::at_state's un, ut and k (flux.hpp:72-104, flux.cuh), the same
+// operations on the stored normal and velocity
+template <class Sm> __device__ __forceinline__ double eigen_un(const Sm& S, int f) {
+    return S.E[EN1][f] * S.E[EU][f] + S.E[EN2][f] * S.E[EV][f];
+}
+template <class Sm> __device__ __forceinline__ double eigen_ut(const Sm& S, int f) {
+    return -S.E[EN2][f] * S.E[EU][f] + S.E[EN1][f] * S.E[EV][f];
+}
+template <class Sm> __device__ __forceinline__ double eigen_k(const Sm& S, int f) {
+    return 0.5 * (S.E[EU][f] * S.E[EU][f] + S.E[EV][f] * S.E[EV][f]);
+}
+
 // window slot of stencil node k of face (g, lane); x faces past the first row
 // segment (q >= L0) sit W-1 slots further (their segment's own halo)
 template <int DIR, int W>
@@ -214,9 +225,6 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             S.E[ES][t] = es.s;
             S.E[EU][t] = es.u;
             S.E[EV][t] = es.v;
-            S.E[EUN][t] = es.un;
-            S.E[EUT][t] = es.ut;
-            S.E[EK][t] = es.k;
             S.E[EH][t] = es.H;
             S.E[EC][t] = es.c;
             S.E[EC2][t] = es.c2;
@@ -289,7 +297,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         // (a) field-independent parts of L q for this group's stencil vectors
         const double kap = S.E[EKAPPA][face], eu = S.E[EU][face], ev = S.E[EV][face];
         const double n1 = S.E[EN1][face], n2 = S.E[EN2][face];
-        const double un = S.E[EUN][face], ut = S.E[EUT][face];
+        const double un = eigen_un(S, face), ut = eigen_ut(S, face);
         // (kap eu) q_u: the reference's left-to-right products, hoisted
         const double keu = kap * eu, kev = kap * ev;
         // the three distinct LLF wave speeds of the face (EigenSystem::field_speed,
@@ -435,8 +443,8 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 const double v = S.E[EV][face], n1 = S.E[EN1][face], n2 = S.E[EN2][face];
                 r = (v - c * n2) * am + (v + c * n2) * ap + v * asum + n1 * at;
             } else {
-                const double Hh = S.E[EH][face], un = S.E[EUN][face], ut = S.E[EUT][face];
-                const double kk = S.E[EK][face], kappa = S.E[EKAPPA][face];
+                const double Hh = S.E[EH][face], un = eigen_un(S, face), ut = eigen_ut(S, face);
+                const double kk = eigen_k(S, face), kappa = S.E[EKAPPA][face];
                 const double ykappa = S.E[EYKAPPA][face];
                 double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut * at;
 #pragma unroll
