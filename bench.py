@@ -64,7 +64,7 @@ OPS = {  # case -> (inviscid ops per cell-stage, whole-step ops per cell)
 }
 INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
 INVISCID_OPS_PER_CELL_STAGE = 4274
-TRAFFIC = {("tgv3d", 256): (1.789204 + 1.821171 + 2.184680 + 0.653781 + 0.656973 + 0.662250) * 1e9}
+TRAFFIC = {("tgv3d", 256): (1.789594 + 1.821264 + 2.173752 + 0.652562 + 0.656228 + 0.661791) * 1e9}
 STEP_OPS_PER_CELL = 14333
 BYTES_PER_CELL_STEP = lambda nc: 8 * (8 * nc + 6)  # noqa: E731  SURVEY §8d B_alg
 
