@@ -13,16 +13,23 @@ Taylor-Green vortex at 256^3 = 16.8 M cells (gamma-gas, TENO6 characteristic,
 Re 1600, Ma 0.1, fixed dt), on the 3D extension (flux3.cuh; validated by the
 z-extrusion cross-check against the 2D oracle, tests/test_gpu_3d.py).
 --case tgv runs the 2D analogue (4096^2, the same cell count), --case h2o2
-configs[2].  The state (5 x 144 MB per buffer) is larger than the 126 MB L2
-and every stage streams several such buffers, so no flush is needed.
+configs[2] (512^2), --case jet3d configs[3] in its z-periodic channel form
+(512 x 256 x 32 per GPU), --case ensemble configs[4] (8 members of the H2/O2
+case at 500 x 250 per GPU, advanced together on their own streams).  The
+state (5 x 144 MB per buffer at 256^3) is larger than the 126 MB L2 and every
+stage streams several such buffers, so no flush is needed.
 
 value   = cells x K / device time of K steps, inputs resident in HBM (CUDA
           events on the library's stream, max over ranks);
 e2e     = same metric through the C ABI with host buffers: every step copies
           the state in from pinned host memory and back out;
 roofline = the dominant kernel class (inviscid faces) against the measured
-          FP64 peak (DFMA microbenchmark run here), algorithmic FP64 ops per
-          cell-stage from the reference's own code (SURVEY §8d);
+          FP64 peak (DFMA microbenchmark run here; also against the no-FMA
+          peak, since bitwise parity keeps every add/mul separate),
+          algorithmic FP64 ops per cell-stage from the reference's own code
+          (the 3D and 4-species counts scaled by measured FP64
+          instruction ratios, profiles/r1_fp64_inst_ratio*.txt), traffic from
+          the ncu capture in profiles/;
 cpu_baseline = the CPU oracle (unmodified reference, all host cores) on a
           bounded sample of the same workload.
 
