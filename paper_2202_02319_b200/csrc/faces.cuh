@@ -302,8 +302,12 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         const double keu = kap * eu, kev = kap * ev;
         // the three distinct LLF wave speeds of the face (EigenSystem::field_speed,
         // flux.hpp:143-147; the convective one serves species and shear fields)
-        if (warp >= NC - 3 && !S.bad[face]) {
-            const int kind = NC - 1 - warp;  // 0: un - c, 1: un, 2: un + c
+        // work split of (a): the shear warps (no projection quotients in (b))
+        // take the extra stencil vectors, the three lightest other warps the
+        // LLF speeds — the fields then reach the group barrier together
+        const int rot = (warp + 2) % NC;
+        if (rot >= NC - 3 && !S.bad[face]) {
+            const int kind = NC - 1 - rot;  // 0: un - c, 1: un, 2: un + c
             const double es = S.E[ES][face];
             double alpha = 0.0;
 #pragma unroll
@@ -316,7 +320,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             }
             S.alpha[kind][lane] = alpha;
         }
-        for (int vec = warp; vec < NV; vec += NC) {
+        for (int vec = rot; vec < NV; vec += NC) {
             const int k = vec >> 1;
             const int t = tile_node<DIR, W>(g, lane, k, L0);
             double q[NC];

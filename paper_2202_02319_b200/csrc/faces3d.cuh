@@ -355,8 +355,12 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         // the three distinct LLF wave speeds of the face (solver.hpp:555-566;
         // the convective one serves every species and shear field), by the
         // warps with the fewest projection vectors
-        if (warp >= NC - 3 && !S.bad[face]) {
-            const int kind = NC - 1 - warp;  // 0: un - c, 1: un, 2: un + c
+        // work split of (a): the shear warps (no projection quotients in (b))
+        // take the extra stencil vectors, the three lightest other warps the
+        // LLF speeds — the fields then reach the group barrier together
+        const int rot = (warp + 3) % NC;
+        if (rot >= NC - 3 && !S.bad[face]) {
+            const int kind = NC - 1 - rot;  // 0: un - c, 1: un, 2: un + c
             const double es = S.E[F3S][face];
             double alpha = 0.0;
 #pragma unroll
@@ -370,7 +374,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             }
             S.alpha[kind][lane] = alpha;
         }
-        for (int vec = warp; vec < NV; vec += NC) {
+        for (int vec = rot; vec < NV; vec += NC) {
             const int k = vec >> 1;
             const int t = tile_node3<DIR, W>(g, lane, k, L0);
             double q[NC];
