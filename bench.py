@@ -40,6 +40,7 @@ side move over NCCL send/recv each stage; dt / error word / clip all-reduce.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -228,9 +229,8 @@ def run_ensemble(args, rank, world, local, dist):
     case (500 x 250), `--members` per GPU (rank r takes samples [r M, r M + M)),
     advanced together by ign_ensemble_rk3_steps; value = all members' cells x
     steps / device time (max over member streams and ranks)."""
-    import ctypes
     import torch
-    from paper_2202_02319_b200 import Ensemble, configs, native
+    from paper_2202_02319_b200 import Ensemble, configs
     M = args.members
     cases = configs.ensemble_members(max(64, M * world), nxy=(args.n, args.n // 2),
                                      first=rank * M, count=M)
@@ -374,7 +374,6 @@ def main():
         case.cfg.slab_count, case.cfg.slab_rank = world, rank
     sim = Simulation(case.cfg)
     if slabs:
-        import ctypes
         uid = ctypes.create_string_buffer(128)
         if rank == 0:
             st = native.api()["nccl_unique_id"](uid)
@@ -429,7 +428,7 @@ def main():
         sim.set_state(hbuf)          # H2D of the step's input state
         sim.rk3_steps(case.dt, 1)
         sim._api["get_state"](sim.handle, hbuf.ctypes.data_as(
-            __import__("ctypes").POINTER(__import__("ctypes").c_double)))  # D2H result
+            ctypes.POINTER(ctypes.c_double)))  # D2H result
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -441,8 +440,8 @@ def main():
     bytes_state = nc * sim.plane * 8
 
     # ---------------- roofline of the dominant kernel class (inviscid faces)
-    peak = __import__("ctypes").c_double()
-    native.api()["probe_fp64_peak"](local, __import__("ctypes").byref(peak))
+    peak = ctypes.c_double()
+    native.api()["probe_fp64_peak"](local, ctypes.byref(peak))
     total_prof = sum(v[0] for v in prof.values())
     dom = max(prof, key=lambda k: prof[k][0])
     f_ms, f_n = prof["faces"]
