@@ -159,17 +159,19 @@ typedef struct {
     /* 3D extension (BASELINE configs[1]; no reference path — SURVEY §0):
      * nz > 0 extrudes the (x, y) mesh uniformly over lz in z.  Component order
      * then [rhoY_s, rho u, rho v, rho w, E]; primitive cache rho,u,v,w,p,T,c,Y;
-     * periodic boundaries in all directions. */
+     * the x / y edges take the reference's rules on every z plane, z is
+     * periodic (periodic_z = 1).  With slab_count > 1, 3D contexts split z. */
     int32_t nz;
     int32_t periodic_z;
     int32_t _pad;
     double lz, center_z;
 } ign_config;
 
-/* errors.hpp:29-35 StepFailure payload + message */
+/* errors.hpp:29-35 StepFailure payload + message; k is the z plane of a 3D
+ * failure (0 in 2D — the reference's payload is (stage, i, j)) */
 typedef struct {
     int32_t status;
-    int32_t stage, i, j;
+    int32_t stage, i, j, k;
     char msg[256];
 } ign_error;
 
@@ -254,7 +256,7 @@ int64_t ign_kernel_launches(const ign_context* ctx);
 #define IGN_PROF_CLASSES 8
 #define IGN_PROF_BC 0       /* ghost fill (x+y passes)           */
 #define IGN_PROF_PRIM 1     /* primitive cache / Newton T solve  */
-#define IGN_PROF_FACES 2    /* inviscid faces, x and y           */
+#define IGN_PROF_FACES 2    /* inviscid faces, every direction   */
 #define IGN_PROF_VISC 3     /* viscous node fluxes               */
 #define IGN_PROF_ASSEMBLE 4 /* RHS assembly + RK update + clip   */
 #define IGN_PROF_DT 5       /* stable_dt reduction               */

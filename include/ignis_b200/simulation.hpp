@@ -28,8 +28,9 @@ struct ConfigError : std::runtime_error { using std::runtime_error::runtime_erro
 struct StateError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct NumericsError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct StepFailure : NumericsError {
-    StepFailure(const std::string& w, int s, int i_, int j_) : NumericsError(w), stage(s), i(i_), j(j_) {}
-    int stage, i, j;
+    StepFailure(const std::string& w, int s, int i_, int j_, int k_ = 0)
+        : NumericsError(w), stage(s), i(i_), j(j_), k(k_) {}
+    int stage, i, j, k;  // k: z plane (3D extension), 0 in 2D
 };
 struct FormatError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct UsageError : std::runtime_error { using std::runtime_error::runtime_error; };
@@ -42,7 +43,7 @@ inline void throw_status(int st, const ign_error& e) {
     case IGN_CONFIG_ERROR: throw ConfigError(m);
     case IGN_STATE_ERROR: throw StateError(m);
     case IGN_NUMERICS_ERROR: throw NumericsError(m);
-    case IGN_STEP_FAILURE: throw StepFailure(m, e.stage, e.i, e.j);
+    case IGN_STEP_FAILURE: throw StepFailure(m, e.stage, e.i, e.j, e.k);
     case IGN_FORMAT_ERROR: throw FormatError(m);
     case IGN_USAGE_ERROR: throw UsageError(m);
     default: throw DeviceError(m);

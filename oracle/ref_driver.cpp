@@ -38,6 +38,7 @@ void set_err(ign_error* e, int status, const char* msg, int stage = 0,
     e->stage = stage;
     e->i = i;
     e->j = j;
+    e->k = 0;
     std::snprintf(e->msg, sizeof(e->msg), "%s", msg);
 }
 

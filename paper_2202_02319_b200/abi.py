@@ -117,7 +117,7 @@ class Config(C.Structure):
 
 class Error(C.Structure):
     _fields_ = [("status", C.c_int32), ("stage", C.c_int32), ("i", C.c_int32),
-                ("j", C.c_int32), ("msg", C.c_char * 256)]
+                ("j", C.c_int32), ("k", C.c_int32), ("msg", C.c_char * 256)]
 
 
 class PrimPoint(C.Structure):

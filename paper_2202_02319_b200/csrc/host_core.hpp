@@ -17,18 +17,19 @@ namespace ign {
 // Exception types mirroring errors.hpp:10-47; mapped to ign_status at the ABI.
 struct Error : std::runtime_error {
     int status;
-    int stage = 0, i = 0, j = 0;
+    int stage = 0, i = 0, j = 0, k = 0;  // k: z plane of a 3D failure
     Error(int st, const std::string& w) : std::runtime_error(w), status(st) {}
 };
 inline Error config_error(const std::string& w) { return Error(IGN_CONFIG_ERROR, w); }
 inline Error numerics_error(const std::string& w) { return Error(IGN_NUMERICS_ERROR, w); }
 inline Error usage_error(const std::string& w) { return Error(IGN_USAGE_ERROR, w); }
 inline Error state_error(const std::string& w) { return Error(IGN_STATE_ERROR, w); }
-inline Error step_failure(const std::string& w, int stage, int i, int j) {
+inline Error step_failure(const std::string& w, int stage, int i, int j, int k = 0) {
     Error e(IGN_STEP_FAILURE, w);
     e.stage = stage;
     e.i = i;
     e.j = j;
+    e.k = k;
     return e;
 }
 

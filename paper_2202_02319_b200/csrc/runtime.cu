@@ -58,6 +58,7 @@ void set_error(ign_error* out, const Error& e) {
     out->stage = e.stage;
     out->i = e.i;
     out->j = e.j;
+    out->k = e.k;
     std::snprintf(out->msg, sizeof(out->msg), "%s", e.what());
 }
 
@@ -140,7 +141,7 @@ Error to_error(const ign_context* ctx, const DevFail& f) {
             const int k = (int)(f.idx / (sx * sy)) - ctx->g;
             return step_failure(std::string("stage state failure: ") + pstatus_msg(f.sub) +
                                     " (k=" + std::to_string(k) + ")",
-                                rep_stage, i, j);
+                                rep_stage, i, j, k);
         }
         const int i = (int)(f.idx % sx) - ctx->g, j = (int)(f.idx / sx) - ctx->g;
         return step_failure(std::string("stage state failure: ") + pstatus_msg(f.sub),
@@ -155,14 +156,16 @@ Error to_error(const ign_context* ctx, const DevFail& f) {
         const unsigned long long cell = f.idx;
         const int i = (int)(cell % ctx->nx);
         const int j = (int)(ctx->nz > 0 ? (cell / ctx->nx) % ctx->ny : cell / ctx->nx);
-        return step_failure("non-finite RHS", rep_stage, i, j);
+        const int k = ctx->nz > 0 ? (int)(cell / ((unsigned long long)ctx->nx * ctx->ny)) : 0;
+        return step_failure("non-finite RHS", rep_stage, i, j, k);
     }
     default: {
         const unsigned long long cell = f.idx / 2;
         const int i = (int)(cell % ctx->nx);
         const int j = (int)(ctx->nz > 0 ? (cell / ctx->nx) % ctx->ny : cell / ctx->nx);
+        const int k = ctx->nz > 0 ? (int)(cell / ((unsigned long long)ctx->nx * ctx->ny)) : 0;
         return step_failure(f.idx % 2 ? "non-finite state" : "non-positive density", rep_stage,
-                            i, j);
+                            i, j, k);
     }
     }
 }

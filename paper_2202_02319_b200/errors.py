@@ -24,9 +24,9 @@ class StepFailure(NumericsError):
     """errors.hpp:29-35: a step produced an invalid state at (stage, i, j)."""
     status = abi.IGN_STEP_FAILURE
 
-    def __init__(self, what: str, stage: int, i: int, j: int):
+    def __init__(self, what: str, stage: int, i: int, j: int, k: int = 0):
         super().__init__(what)
-        self.stage, self.i, self.j = stage, i, j
+        self.stage, self.i, self.j, self.k = stage, i, j, k  # k: 3D extension
 
 
 class FormatError(IgnisError):
@@ -51,5 +51,5 @@ def raise_for(status: int, err: "abi.Error") -> None:
         return
     msg = err.msg.decode(errors="replace")
     if status == abi.IGN_STEP_FAILURE:
-        raise StepFailure(msg, err.stage, err.i, err.j)
+        raise StepFailure(msg, err.stage, err.i, err.j, err.k)
     raise _BY_STATUS.get(status, IgnisError)(msg)

@@ -306,8 +306,8 @@ def test_jet3d_runs_and_develops_3d_structure(cuda_device):
 
 def test_3d_state_failure_location(cuda_device):
     """A non-positive density in a 3D state raises StepFailure at prepare time
-    with the node's (i, j) and its plane k in the message (the reference's
-    error kinds; ign_error carries i, j)."""
+    with the node's (i, j, k) — k in ign_error.k and in the message (the
+    reference's error kinds; its payload is (stage, i, j))."""
     from paper_2202_02319_b200 import errors
     case = configs.tgv3d(12)
     sim = Simulation(case.cfg)
@@ -318,7 +318,7 @@ def test_3d_state_failure_location(cuda_device):
     with pytest.raises(errors.StepFailure) as ei:
         sim.prepare_stage(2)
     e = ei.value
-    assert (e.stage, e.i, e.j) == (2, 6, 5)
+    assert (e.stage, e.i, e.j, e.k) == (2, 6, 5, 4)
     assert "k=4" in str(e)
 
 
