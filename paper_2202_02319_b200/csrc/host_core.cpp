@@ -300,10 +300,21 @@ DMix build_mix(const ign_mixture& mx) {
                     !std::signbit(d.pc[0].c0))
                        ? 1
                        : 0;
-        d._pad = 0;
+        d.lin2 = a.npieces >= 1 && a.npieces <= 2;
+        for (int k = 0; k < a.npieces; ++k) {
+            const DPiece& p = d.pc[k];
+            if (p.inv_terms || p.cp_deg > 1 || (p.cp_deg == 0 && std::signbit(p.c0))) d.lin2 = 0;
+        }
+        if (d.lin2 && a.npieces == 1) d.pc[1] = d.pc[0];
     }
     m.all_simple = 1;
-    for (int s = 0; s < mx.ns; ++s) m.all_simple &= m.sp[s].simple;
+    m.all_lin2 = 1;
+    m._pad = 0;
+    for (int s = 0; s < mx.ns; ++s) {
+        m.all_simple &= m.sp[s].simple;
+        m.all_lin2 &= m.sp[s].lin2;
+    }
+    if (m.all_simple) m.all_lin2 = 0;
     // W-only factors of Wilke's rule (thermo.hpp:249-251), same glibc calls
     for (int i = 0; i < mx.ns; ++i)
         for (int j = 0; j < mx.ns; ++j) {

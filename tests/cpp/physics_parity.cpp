@@ -312,7 +312,21 @@ int main() {
     gas.species[0].pieces[0].t_hi = 1e6;
     check_recon();
     check_teno_cutoff_boundary();
-    check_mixture<4>(ch4, "ch4_o2", 1234);
+    check_mixture<4>(ch4, "ch4_o2", 1234);  // two linear-cp ranges: DSpecies::lin2 path
+    // the repo's H2/O2 table (one linear range and two), and a quartic variant
+    // of the CH4 table that keeps the general branch-free piece path covered
+    const ignis::MixtureModel h2 = ignis::load_mixture_file(REPO_DATA_DIR "/h2_o2.mix");
+    check_mixture<4>(h2, "h2_o2", 4321);
+    ignis::MixtureModel quartic = ch4;
+    for (auto& sp : quartic.species)
+        for (auto& pc : sp.pieces) {
+            pc.c2 = 1e-7;
+            pc.c4 = -2e-15;
+        }
+    check_mixture<4>(quartic, "ch4_o2 quartic", 99);
+    ignis::MixtureModel one = ch4;  // single linear range per species
+    for (auto& sp : one.species) sp.pieces.resize(1), sp.pieces[0].t_hi = 6000.0;
+    check_mixture<4>(one, "ch4_o2 one range", 7);
     check_mixture<1>(gas, "gamma_gas", 77);
     check_sources(ch4);
     std::printf("physics parity: %d checks, %d mismatches\n", g_checks, g_fail);

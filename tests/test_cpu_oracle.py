@@ -51,6 +51,7 @@ def test_product_physics_bitwise_vs_reference(tmp_path):
     exe = str(tmp_path / "physics_parity")
     _compile(f"{ROOT}/tests/cpp/physics_parity.cpp", exe,
              (f"-I{ROOT}/include", f"-I{ROOT}/paper_2202_02319_b200/csrc",
+              f'-DREPO_DATA_DIR="{ROOT}/data"',
               f"{ROOT}/paper_2202_02319_b200/csrc/host_core.cpp"))
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-3000:]
