@@ -201,8 +201,10 @@ __global__ void __launch_bounds__(256) k_prim3(const __grid_constant__ KParams P
 // ---------------------------------------------------------------- viscous
 // compute_viscous (solver.hpp:610-696) with the z gradient, z stresses and
 // the zeta flux appended after the reference's 2D terms
+// 2-4 species: 6 CTAs/SM (<= 85 registers, a small spill) hide more of the
+// stencil loads' latency (jet visc3 -6.5%); the gamma-gas keeps 122 registers
 template <int NS>
-__global__ void __launch_bounds__(128) k_visc3(const __grid_constant__ KParams P, int stage,
+__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc3(const __grid_constant__ KParams P, int stage,
                                                int step) {
     constexpr int NC = NS + 4;
     if (failed(P.err)) return;

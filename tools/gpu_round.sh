@@ -7,6 +7,7 @@ python bench.py --case tgv --no-cpu > gpurun_out/round/bench_tgv2d.json 2>/dev/n
 python bench.py --case h2o2 > gpurun_out/round/bench_h2o2.json 2>/dev/null
 python bench.py --case ensemble > gpurun_out/round/bench_ensemble.json 2>/dev/null
 python bench.py --case jet3d --no-cpu > gpurun_out/round/bench_jet3d.json 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_prim3|k_visc3" -c 4 -o gpurun_out/round/jet_prim_visc -f python tools/profjet.py > /dev/null 2>&1
 python bench.py --impl reference > gpurun_out/round/bench_reference.json 2>/dev/null
 lscpu > gpurun_out/round/lscpu.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/round/launches_tgv3d.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
