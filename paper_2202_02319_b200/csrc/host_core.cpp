@@ -309,10 +309,11 @@ DMix build_mix(const ign_mixture& mx) {
     }
     m.all_simple = 1;
     m.all_lin2 = 1;
-    m._pad = 0;
+    m.w_pos_ok = 1;
     for (int s = 0; s < mx.ns; ++s) {
         m.all_simple &= m.sp[s].simple;
         m.all_lin2 &= m.sp[s].lin2;
+        m.w_pos_ok &= (m.sp[s].unit_W || fdiv_pos_divisor_ok(m.sp[s].W)) ? 1 : 0;
     }
     if (m.all_simple) m.all_lin2 = 0;
     // W-only factors of Wilke's rule (thermo.hpp:249-251), same glibc calls
