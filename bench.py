@@ -85,18 +85,52 @@ def env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every
+    5 ms from a thread (so a 100 ms region still gets samples), else the
+    nvidia-smi loop (200 ms period)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.sm, self.mx, self.reasons = [], None, set()
 
     def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            idx = self.device
+            try:  # CUDA ordinal -> NVML index (CUDA_VISIBLE_DEVICES aware)
+                import torch
+                idx = torch.cuda._get_nvml_device_index(self.device)
+            except Exception:
+                pass
+            h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": N.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksThrottleReasonSwPowerCap}
+            self.nvml, self.stop = N, threading.Event()
+
+            def poll():
+                while True:
+                    self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.reasons.update(k for k, b in bits.items() if r & b)
+                    if self.stop.wait(0.005):
+                        return
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
@@ -113,6 +147,9 @@ class ClockSampler:
             self.lines.append(ln.strip())
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:
@@ -121,8 +158,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = list(self.sm), self.mx, set(self.reasons)
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 9:
@@ -132,11 +168,12 @@ class ClockSampler:
                 mx = float(p[2])
             except ValueError:
                 continue
-            for k, v in zip(names, p[5:9]):
+            for k, v in zip(self.NAMES, p[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(k)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def make_case(args, nslabs: int = 1):

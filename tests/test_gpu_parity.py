@@ -19,8 +19,24 @@ pytestmark = pytest.mark.gpu
 RHS_TOL = 1e-13
 STEP_TOL = 1e-10
 
+
+
+def _ch4_quartic(n):
+    """CH4/O2 with quadratic and quartic cp terms added: keeps the general
+    (indexed-range, quartic Horner) thermo path covered on the device — the
+    linear tables in data/ all take DSpecies::lin2."""
+    case = configs.reacting_ch4(n)
+    mix = case.cfg.mix
+    for s in range(mix.ns):
+        for k in range(mix.species[s].npieces):
+            mix.species[s].pieces[k].c2 = 1e-7
+            mix.species[s].pieces[k].c4 = -2e-15
+    return case
+
+
 # name -> (builder, exact, nsteps)
 CASES = {
+    "ch4_quartic_thermo": (lambda: _ch4_quartic(24), False, 10),
     "tgv_char_teno6_visc": (lambda: configs.tgv2d(48), True, 20),
     "tgv_comp_teno6_inviscid": (lambda: configs.tgv2d(48, split="comp", viscous=False), False, 20),
     "tgv_char_weno3z_visc": (lambda: configs.tgv2d(40, scheme="weno3z"), True, 20),
