@@ -169,8 +169,9 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
 // ---------------------------------------------------------------- primitives
 // refresh_primitives (solver.hpp:148-177) over the padded box; the cached T
 // is the Newton guess (thermo.hpp:196).
+// 2-4 species: 4 CTAs/SM (64 registers, small spill): jet primitives -10%
 template <int NS, bool WX>
-__global__ void __launch_bounds__(256) k_prim(const __grid_constant__ KParams P,
+__global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim(const __grid_constant__ KParams P,
                                               const double* __restrict__ Ut, int stage,
                                               int step) {
     if (failed(P.err)) return;
