@@ -361,8 +361,10 @@ static __device__ __noinline__ double laser_cold2(double x, double y, double t, 
 // EDGE = false: every padded node except, when LODI is on, the right-edge
 // column; EDGE = true: that column alone (grid over j), with the LODI x-flux
 // difference — the LODI code never enters the bulk update.
+// 2-4 species: 4 CTAs/SM (64 registers): H2/O2 update -10% (the 3D update
+// loses 7% this way and keeps its default)
 template <int NS, int MODE, bool EDGE>
-__global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ KParams P,
+__global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_assemble(const __grid_constant__ KParams P,
                                                   const double* __restrict__ U0,
                                                   const double* __restrict__ Ucur,
                                                   double* __restrict__ Uout, double dt,
