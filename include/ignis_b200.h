@@ -71,7 +71,7 @@ typedef struct {
     ign_species species[IGN_MAX_SPECIES];
 } ign_mixture;
 
-/* reconstruction.hpp:202-230 SchemeConfig.
+/* reconstruction.hpp:12-40 SchemeConfig.
  * scheme: 0 = WENO3Z, 1 = TENO6; split: 0 = Componentwise, 1 = Characteristic;
  * metrics: 0 = Scheme, 1 = AnalyticSkew, 2 = Central2 */
 typedef struct {
@@ -112,7 +112,7 @@ typedef struct {
     double nu[IGN_MAX_SPECIES];
 } ign_mechanism;
 
-/* laser.hpp:99-127 LaserParams + ShapedProfile (present = 0 means nullopt).
+/* laser.hpp:18-46 LaserParams + ShapedProfile (present = 0 means nullopt).
  * kernel: 0 = Gaussian, 1 = Shaped */
 typedef struct {
     int32_t present;
@@ -203,7 +203,7 @@ int ign_dims(const ign_context* ctx, int32_t* nx, int32_t* ny, int32_t* g,
 int ign_dims3(const ign_context* ctx, int32_t* nz, int32_t* k0, int32_t* nz_glob);
 
 /* ---- setup / host mirrors --------------------------------------------- */
-/* mesh.x/mesh.y padded arrays (mesh.hpp:295-296) */
+/* mesh.x/mesh.y padded arrays (mesh.hpp:33-34) */
 int ign_get_mesh(const ign_context* ctx, double* x, double* y);
 /* which 0: met (solver.hpp:56), 1: met_v (solver.hpp:57); out = 5 padded
  * fields [jac, m_xi_x, m_xi_y, m_eta_x, m_eta_y] (metrics.hpp:28-35) */

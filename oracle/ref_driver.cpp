@@ -381,9 +381,15 @@ int ignref_rk3_steps(ref_ctx* ctx, double dt, int64_t n) {
 
 int ignref_advance(ref_ctx* ctx, ign_step_hook hook, void* user) {
     return guarded(&ctx->err, [&] {
-        if (hook)
-            ctx->sim.advance([&](Simulation&) { hook(ctx, user); });
-        else
+        if (hook) {
+            // the ABI hook returns nonzero to stop; the reference's void hook
+            // (solver.hpp:336-348) is stopped through its public loop bound
+            const auto max_iter = ctx->sim.integ.max_iter;
+            ctx->sim.advance([&](Simulation& s) {
+                if (hook(ctx, user) != 0) s.integ.max_iter = s.iter;
+            });
+            ctx->sim.integ.max_iter = max_iter;
+        } else
             ctx->sim.advance();
     });
 }

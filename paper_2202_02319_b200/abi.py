@@ -26,7 +26,7 @@ IGN_USAGE_ERROR = 6
 IGN_CUDA_ERROR = 7
 IGN_INTERNAL_ERROR = 8
 
-# enums (reconstruction.hpp:202-208, boundary.hpp:16-22, metrics.hpp:404, laser.hpp:93)
+# enums (reconstruction.hpp:12-18, boundary.hpp:16-22, metrics.hpp:21, laser.hpp:12)
 WENO3Z, TENO6 = 0, 1
 COMPONENTWISE, CHARACTERISTIC = 0, 1
 METRICS_SCHEME, METRICS_ANALYTIC_SKEW, METRICS_CENTRAL2 = 0, 1, 2

@@ -148,7 +148,7 @@ def base_config(nx: int, ny: int, lx: float, ly: float, *, center=(0.0, 0.0),
     cfg.center_x, cfg.center_y = center
     cfg.periodic_x, cfg.periodic_y = int(periodic[0]), int(periodic[1])
     cfg.metric_mode = abi.MM_AUTO
-    # SchemeConfig defaults (reconstruction.hpp:210-216)
+    # SchemeConfig defaults (reconstruction.hpp:20-26)
     cfg.scheme.scheme = abi.TENO6
     cfg.scheme.split = abi.CHARACTERISTIC
     cfg.scheme.teno_ct = 1e-5
@@ -346,6 +346,105 @@ def h2o2_counterflow(n: int = 512, *, scheme: str = "teno6", split: str = "char"
     return Case(f"h2o2_{nx}x{ny}", cfg, ic, min(0.15 * dx / 400.0, la.sigma_t / 6.0))
 
 
+def _lin_species(name, W, mu_ref, n_exp, c0, c1, h_form_over_R, c0_hi=None, c1_hi=None):
+    """A compact surrogate in the h2_o2.mix form: two linear cp/R ranges meeting
+    at 1000 K with h continuous there and h(298.15 K)/R = h_form_over_R."""
+    c0_hi = c0 if c0_hi is None else c0_hi
+    c1_hi = c1 if c1_hi is None else c1_hi
+    b = h_form_over_R - (c0 * 298.15 + 0.5 * c1 * 298.15 ** 2)
+    b_hi = b + (c0 - c0_hi) * 1000.0 + 0.5 * (c1 - c1_hi) * 1e6
+    return SpeciesSpec(name, W, mu_ref, 273.0, n_exp,
+                       [_piece(200.0, 1000.0, c0, c1, b), _piece(1000.0, 6000.0, c0_hi, c1_hi, b_hi)])
+
+
+def eight_species() -> list:
+    """H2, O2, H2O, N2 (data/h2_o2.mix) + four inert surrogates AR, HE, CO2, CO:
+    the reference's species cap (thermo.hpp:16 kMaxSpecies = 8)."""
+    base = h2_o2_species()
+    return base + [
+        _lin_species("AR", 0.040, 2.10e-05, 0.72, 2.5, 0.0, 0.0),
+        _lin_species("HE", 0.004, 1.87e-05, 0.67, 2.5, 0.0, 0.0),
+        _lin_species("CO2", 0.044, 1.37e-05, 0.93, 3.9, 0.002, -393510.0 / R_UNIVERSAL,
+                     5.4, 0.0005),
+        _lin_species("CO", 0.028, 1.66e-05, 0.74, 3.3, 0.0004, -110530.0 / R_UNIVERSAL,
+                     3.6, 0.0001),
+    ]
+
+
+def species_box(ns: int, n: int = 24, *, scheme: str = "teno6", split: str = "char",
+                laser: str = "gaussian", viscous: bool = True) -> Case:
+    """Periodic 1 cm box with ns species (2..8) for the species-count parity
+    cases: ns = 2 is a non-reacting H2/N2 mixture; ns >= 3 takes the first ns
+    of eight_species() with the one-step 2 H2 + O2 -> 2 H2O mechanism.  A hot
+    kernel, shear and a laser (Gaussian or the shaped two-lobe kernel,
+    laser.hpp:64-85) keep transport, chemistry and the source active."""
+    if not 2 <= ns <= 8:
+        raise ValueError("species_box: 2 <= ns <= 8")
+    allsp = eight_species()
+    species = [allsp[0], allsp[3]] if ns == 2 else allsp[:ns]
+    L = 0.01
+    cfg = base_config(n, n, L, L)
+    fill_mixture(cfg.mix, species)
+    set_scheme(cfg, scheme, split)
+    cfg.viscous = int(viscous)
+    if ns >= 3:
+        m = cfg.mech
+        m.present = 1
+        m.A, m.Ta, m.a, m.b, m.T_cutoff = 1e9, 15000.0, 1.0, 1.0, 300.0
+        m.i_fuel, m.i_ox, m.i_co2, m.i_h2o = 0, 1, -1, 2
+        for q in range(ns):
+            m.nu[q] = (-2.0, -1.0, 2.0)[q] if q < 3 else 0.0
+    la = cfg.laser
+    la.present = 1
+    la.sigma_r, la.sigma_t = 8e-4, 2e-6
+    la.x0, la.y0, la.t0 = 1e-3, -5e-4, 1e-6
+    if laser == "shaped":
+        la.kernel = abi.LASER_SHAPED
+        la.energy = 1.0  # q_shaped ignores it (laser.hpp:79-85); validate() needs >= 0
+        la.edot_rate = 1e11
+        la.lobe_sep, la.width_up, la.width_down = 1e-3, 1.2e-3, 5e-4
+        la.amp_down, la.width_radial = 0.7, 4e-4
+    else:
+        la.kernel = abi.LASER_GAUSSIAN
+        la.energy = 2.0
+    Ws = np.array([sp.W for sp in species])
+    # unburnt: fuel-lean H2/O2 in N2 (ns = 2: H2/N2), traces of every inert
+    Yu = np.full(ns, 0.02)
+    Yb = np.full(ns, 0.02)
+    if ns == 2:
+        Yu[:] = (0.3, 0.7)
+        Yb[:] = (0.05, 0.95)
+    else:
+        Yu[:3] = (0.03, 0.22, 0.0)
+        Yb[:3] = (0.005, 0.1, 0.2)
+        if ns >= 4:
+            Yu[3] = Yb[3] = 0.0
+    Yu /= Yu.sum() if ns == 2 else 1.0
+    if ns >= 4:  # N2 closes the mass fractions
+        Yu[3] = 1.0 - (Yu.sum() - Yu[3])
+        Yb[3] = 1.0 - (Yb.sum() - Yb[3])
+    elif ns == 3:
+        Yu /= Yu.sum()
+        Yb /= Yb.sum()
+
+    def ic(X, Yc):
+        r2 = (X - 1e-3) ** 2 + (Yc + 1e-3) ** 2
+        f = np.exp(-r2 / (2.0 * (1.5e-3) ** 2))
+        T = 300.0 + 1500.0 * f
+        Ys = [Yu[q] * (1 - f) + Yb[q] * f for q in range(ns)]
+        tot = sum(Ys)
+        Ys = [y / tot for y in Ys]
+        rbar = R_UNIVERSAL * sum(Ys[q] / Ws[q] for q in range(ns))
+        rho = 101325.0 / (rbar * T)
+        u = 3.0 * np.sin(2 * math.pi * Yc / L)
+        v = -2.0 * np.cos(2 * math.pi * X / L)
+        return rho, u, v, T, Ys
+
+    dx = L / n
+    c_max = 1000.0 if ns == 2 else 900.0
+    return Case(f"species{ns}_{n}_{laser}", cfg, ic, 0.2 * dx / c_max)
+
+
 def wall_channel(n: int = 48, isothermal: bool = True, scheme: str = "teno6",
                  split: str = "char") -> Case:
     """No-slip walls (boundary.hpp:210-226): periodic x, isothermal bottom and
@@ -516,7 +615,7 @@ def state_3d_to_2d(Ut3: np.ndarray, ns: int, k: int) -> np.ndarray:
 
 
 def padded_coords(cfg: abi.Config):
-    """Computational node coordinates over the padded box (mesh.hpp:302-304);
+    """Computational node coordinates over the padded box (mesh.hpp:39-42);
     for unskewed meshes these are the physical coordinates."""
     g = cfg.g
     dxi, deta = cfg.lx / cfg.nx, cfg.ly / cfg.ny

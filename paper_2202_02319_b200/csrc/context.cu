@@ -51,10 +51,11 @@ int ign_last_error(const ign_context* ctx, ign_error* err) {
 }
 
 int ign_dims(const ign_context* ctx, int32_t* nx, int32_t* ny, int32_t* g, int32_t* ns) {
-    *nx = ctx->nx;
-    *ny = ctx->ny;
-    *g = ctx->g;
-    *ns = ctx->ns;
+    if (!ctx) return IGN_USAGE_ERROR;
+    if (nx) *nx = ctx->nx;
+    if (ny) *ny = ctx->ny;
+    if (g) *g = ctx->g;
+    if (ns) *ns = ctx->ns;
     return IGN_OK;
 }
 
@@ -234,16 +235,27 @@ int ign_rk3_steps(ign_context* ctx, double dt, int64_t n) {
 int ign_ensemble_rk3_steps(ign_context** members, int n, const double* dt, int64_t nsteps,
                            int* status) {
     if (!members || n <= 0 || !dt || !status) return IGN_USAGE_ERROR;
+    // a usage error is every member's outcome: no member steps
+    auto fail_all = [&](int st, const Error& e) {
+        for (int q = 0; q < n; ++q) {
+            status[q] = st;
+            if (members[q]) set_error(&members[q]->lasterr, e);
+        }
+        return st;
+    };
     for (int q = 0; q < n; ++q)
-        if (!members[q] || members[q]->nranks > 1 || members[q]->device != members[0]->device)
-            return IGN_USAGE_ERROR;
+        if (!members[q] || members[q]->nranks > 1 || members[q]->group ||
+            members[q]->device != members[0]->device)
+            return fail_all(IGN_USAGE_ERROR,
+                            usage_error("ensemble: members must be whole-domain contexts on one "
+                                        "device"));
     try {
         cuda_check(cudaSetDevice(members[0]->device), "cudaSetDevice");
         t_run_ensemble(std::vector<ign_context*>(members, members + n), dt, nsteps, status);
     } catch (const Error& e) {
-        return e.status;
+        return fail_all(e.status, e);
     } catch (const std::exception& e) {
-        return IGN_INTERNAL_ERROR;
+        return fail_all(IGN_INTERNAL_ERROR, Error(IGN_INTERNAL_ERROR, e.what()));
     }
     int worst = IGN_OK;
     for (int q = 0; q < n; ++q)

@@ -535,19 +535,8 @@ inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int st
     constexpr int NC = NS + 4;
     const size_t smem = sizeof(FaceSmem3<NS, DIR, TENO, CHAR>);
     auto kern = k_faces3d<NS, DIR, TENO, CHAR>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-        if (std::getenv("IGN_DEBUG_OCC")) {
-            int nb = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NC * 32, smem);
-            std::fprintf(stderr, "k_faces3d<NS=%d,DIR=%d>: smem %zu B, %d CTAs/SM\n", NS, DIR,
-                         smem, nb);
-        }
-        configured = true;
-    }
+    static std::atomic<unsigned long long> configured{0};  // per instantiation, per device
+    configure_kernel(kern, smem, NC, configured, "k_faces3d");
     const int NF = 32 * NC;
     dim3 grid;
     if (DIR == 0) {

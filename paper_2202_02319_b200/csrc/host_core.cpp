@@ -210,7 +210,7 @@ void validate_config(const ign_config& c, const HMesh& mesh) {
     for (int s = 0; s < c.mix.ns; ++s)
         if (c.mix.species[s].npieces < 1 || c.mix.species[s].npieces > kMaxPieces)
             throw usage_error("mixture: species needs 1..4 polynomial pieces");
-    // SchemeConfig::validate (reconstruction.hpp:218-224)
+    // SchemeConfig::validate (reconstruction.hpp:28-34)
     const ign_scheme& sc = c.scheme;
     if (!(sc.eps > 0.0)) throw config_error("scheme: eps must be positive");
     if (!(sc.teno_ct > 0.0 && sc.teno_ct < 1.0))

@@ -60,7 +60,7 @@ struct HMesh {
     double dxi() const { return lx / nx; }
     double deta() const { return ly / ny_glob; }
     double xi(int i) const { return cx - 0.5 * lx + (i + 0.5) * dxi(); }
-    // computational coordinate of GLOBAL row jg (mesh.hpp:304)
+    // computational coordinate of GLOBAL row jg (mesh.hpp:41-42)
     double eta_glob(int jg) const { return cy - 0.5 * ly + (jg + 0.5) * deta(); }
     // of LOCAL row j
     double eta(int j) const { return eta_glob(j0 + j); }

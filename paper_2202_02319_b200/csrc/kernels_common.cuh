@@ -6,6 +6,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+
 #include "physics.cuh"
 
 namespace ign {
@@ -97,6 +103,36 @@ __device__ __forceinline__ long long pidx(const KParams& P, int i, int j) {
 #define PX(P, s) ((P).prim + (6 + (P).ns + (s)) * (P).plane)
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+// Kernel attributes (>48 KB dynamic shared memory opt-in, carveout) are
+// per device: each instantiation keeps one bit per device ordinal, set after
+// both attribute calls succeeded on that device (thread-safe; racing threads
+// at worst set the same attributes twice).  Failures throw (IGN_CUDA_ERROR at
+// the ABI: runtime_error subclasses map to the context's error).
+struct KernelAttrError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+template <class Kern>
+inline void configure_kernel(Kern kern, size_t smem, int warps, std::atomic<unsigned long long>& mask,
+                             const char* name) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) throw KernelAttrError("cudaGetDevice failed");
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess)
+        throw KernelAttrError(std::string(name) + ": cudaFuncSetAttribute: " + cudaGetErrorString(e));
+    if (std::getenv("IGN_DEBUG_OCC")) {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, warps * 32, smem);
+        std::fprintf(stderr, "%s: smem %zu B, %d CTAs/SM (device %d)\n", name, smem, nb, dev);
+    }
+    mask.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 }  // namespace ign
 

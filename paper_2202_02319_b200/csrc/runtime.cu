@@ -445,6 +445,7 @@ void t_run_ensemble(const std::vector<ign_context*>& mem, const double* dt, int6
         a0[q] = mem[q]->cur;
         t[q] = mem[q]->time;
         status[q] = IGN_OK;
+        std::memset(&mem[q]->lasterr, 0, sizeof(ign_error));  // a healthy member reads no error
     }
     for (int64_t done = 0; done < n;) {
         const int64_t chunk = std::min<int64_t>(n - done, kChunk);
@@ -554,7 +555,9 @@ void t_advance(const Team& T, ign_step_hook hook, void* user) {
         t_run_steps(T, dt, 1, false);
         t_prepare_sync(T, 1);
         t_sample(T);
-        if (hook) hook(L, user);
+        // the hook returns nonzero to stop (ignis_b200.h); the reference's
+        // void step_hook (solver.hpp:347) corresponds to always returning 0
+        if (hook && hook(L, user) != 0) break;
     }
 }
 

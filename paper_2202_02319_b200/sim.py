@@ -441,8 +441,10 @@ class Ensemble:
         dts = np.ascontiguousarray(np.broadcast_to(np.asarray(dt, dtype=np.float64), (M,)))
         hs = (C.c_void_p * M)(*[m.handle.value for m in self.members])
         st = (C.c_int * M)()
-        self._api["ensemble_rk3_steps"](hs, M, _dptr(dts), n, st)
+        rc = int(self._api["ensemble_rk3_steps"](hs, M, _dptr(dts), n, st))
         status = [int(x) for x in st]
+        if rc != abi.IGN_OK and all(x == abi.IGN_OK for x in status):
+            status = [rc] * M  # defensive: a failing call always reports per member
         if all(x != abi.IGN_OK for x in status):
             self.members[0]._check(status[0])
         return status

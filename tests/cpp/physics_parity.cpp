@@ -198,7 +198,7 @@ static void check_teno_cutoff_boundary() {
         double w[6];
         const double amp = std::pow(10.0, lg(rng));  // discontinuity strength
         for (int q = 0; q < 6; ++q) w[q] = (q < 3 ? 1.0 : 0.0) + amp * u(rng);
-        // exact ratios Q_k of the reference's sequence (reconstruction.hpp:257-289)
+        // exact ratios Q_k of the reference's sequence (reconstruction.hpp:65-115)
         const double v0 = w[0] - w[2], v1 = w[1] - w[2], v3 = w[3] - w[2], v4 = w[4] - w[2],
                      v5 = w[5] - w[2];
         const double b[4] = {
@@ -302,6 +302,24 @@ static void check_sources(const ignis::MixtureModel& mix) {
     for (int trial = 0; trial < 20000; ++trial) {
         const double x = ux(rng), y = ux(rng) - 2.0, t = ut(rng);
         EXPECT_BITWISE("q_gaussian", ign::laser_power(x, y, t, dl), ignis::laser_power(x, y, t, lp));
+    }
+    // shaped two-lobe kernel (laser.hpp:64-85): the product squares with z*z
+    // where the reference calls pow(z, 2) (tests/cpp/pow2_check.c)
+    ignis::LaserParams sp = lp;
+    sp.kernel = ignis::LaserKernel::Shaped;
+    sp.edot_rate = 3.7e10;
+    sp.profile.lobe_sep = 0.35; sp.profile.width_up = 0.5; sp.profile.width_down = 0.2;
+    sp.profile.amp_down = 0.8; sp.profile.width_radial = 0.25;
+    ign_laser as = al;
+    as.kernel = 1; as.edot_rate = sp.edot_rate; as.lobe_sep = sp.profile.lobe_sep;
+    as.width_up = sp.profile.width_up; as.width_down = sp.profile.width_down;
+    as.amp_down = sp.profile.amp_down; as.width_radial = sp.profile.width_radial;
+    const ign::DLaser ds = ign::build_laser(as);
+    for (int trial = 0; trial < 200000; ++trial) {
+        const double x = ux(rng), y = ux(rng) - 2.0, t = ut(rng);
+        EXPECT_BITWISE("shaped_profile", ign::shaped_profile(x, y, ds),
+                       ignis::shaped_profile(x, y, sp));
+        EXPECT_BITWISE("q_shaped", ign::laser_power(x, y, t, ds), ignis::laser_power(x, y, t, sp));
     }
 }
 

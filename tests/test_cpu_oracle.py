@@ -97,3 +97,20 @@ def test_oracle_periodic_conservation(oracle_api):
     t1 = sim.conserved_totals()
     assert abs(t1[0] - t0[0]) <= 1e-13 * abs(t0[0])
     assert abs(t1[3] - t0[3]) <= 1e-13 * abs(t0[3])
+
+
+@pytest.mark.parametrize("src,n", [("hypot_check.c", 20000000), ("pow2_check.c", 100000000),
+                                   ("fdiv_check.cpp", 20000000)])
+def test_libm_restatements_bitwise(tmp_path, src, n):
+    """The exact rewrites DESIGN.md §3 relies on, checked against the host libm
+    / IEEE division: glibc hypot restated (ghypot), pow(z, 2) == z*z (shaped
+    laser), Markstein division (fdiv)."""
+    exe = str(tmp_path / src.split(".")[0])
+    cc = "gcc" if src.endswith(".c") else "g++"
+    cmd = [cc, "-O2", "-ffp-contract=off", f"-I{ROOT}/paper_2202_02319_b200/csrc",
+           f"-I{ROOT}/include", f"{ROOT}/tests/cpp/{src}", "-o", exe, "-lm"]
+    if cc == "g++":
+        cmd.insert(1, "-std=c++17")
+    subprocess.run(cmd, check=True, capture_output=True)
+    r = subprocess.run([exe, str(n)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-1000:]

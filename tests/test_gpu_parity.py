@@ -161,6 +161,18 @@ def test_advance_hook_called_per_step(oracle_api, cuda_device):
     assert seen == [1, 2, 3, 4]
 
 
+def test_advance_hook_nonzero_stops(oracle_api, cuda_device):
+    """ign_step_hook returns nonzero to stop (ignis_b200.h); the oracle stops
+    the reference's loop through its public integ.max_iter (solver.hpp:340)."""
+    case = configs.tgv2d(24)
+    prod, refs = make_pair(case, oracle_api)
+    for s in (prod, refs):
+        s.set_integrator(fixed_dt=case.dt, t_end=10.5 * case.dt)
+        s.advance(lambda sim: sim.iter >= 3)
+    assert prod.iter == refs.iter == 3
+    assert bitwise_equal(prod.Ut, refs.Ut)
+
+
 def test_diagnostics_bitwise(oracle_api, cuda_device):
     case = configs.reacting_ch4(24)
     prod, refs = make_pair(case, oracle_api)
