@@ -181,7 +181,7 @@ int ign_refill_ghosts(ign_context* ctx) {
     return guarded(ctx, [&] {
         const Team T = solo(ctx);
         ctx->launches += ctx->ks.bc(ctx->kp, ctx->S[ctx->cur], 0, 0, 0, ctx->stream);
-        t_exchange(T, ctx->cur);
+        t_exchange(T, ctx->cur, ctx->stream);
         ctx->launches += ctx->ks.bc(ctx->kp, ctx->S[ctx->cur], 1, 0, 0, ctx->stream);
         t_errsync(T);
         check(T);
@@ -190,7 +190,7 @@ int ign_refill_ghosts(ign_context* ctx) {
 
 int ign_refresh_primitives(ign_context* ctx, int stage) {
     return guarded(ctx, [&] {
-        ctx->launches += ctx->ks.prim(ctx->kp, ctx->S[ctx->cur], stage, 0, ctx->stream);
+        ctx->launches += ctx->ks.prim(ctx->kp, ctx->S[ctx->cur], stage, 0, ctx->stream, 0);
         t_errsync(solo(ctx));
         check(solo(ctx));
     });

@@ -90,6 +90,12 @@ struct ign_context {
     ign_integrator integ{};
     ign_error lasterr{};
     int64_t launches = 0;
+    // halo overlap (slabs): the halo leg (exchange, edge ghosts, ghost-row
+    // primitives) runs on halo_stream while the stream computes the slab's own
+    // rows; ev_halo joins it before the first kernel that reads the halo
+    cudaStream_t halo_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    bool halo_pending = false;
     // slab decomposition
     int nranks = 1, rank = 0;
     int lo_peer = -1, hi_peer = -1;  // ranks owning our ghost rows (-1: physical edge)
@@ -201,16 +207,23 @@ inline size_t halo_stride(const ign_context* c) {
 }
 inline size_t halo_count(const ign_context* c) { return c->nz > 0 ? c->nz : c->ny; }
 
-void t_exchange(const Team& T, int buf);
+void t_exchange(const Team& T, int buf, cudaStream_t s);
+bool t_has_halo(const Team& T);
+void t_join(const Team& T);
 void t_prepare(const Team& T, int buf, int stage, int step);
 void t_fluxes(const Team& T, int buf, int stage, int step);
 void t_assemble(const Team& T, int mode, int a, int cur, int out, double dt, double w, double t,
                 int stage, int step, int slot);
 void t_step(const Team& T, int a, double time, double dt, int step, bool post_prepare);
-void read_clips(const Team& T, unsigned long long red[8]);
+void read_clips(const Team& T, int64_t chunk, std::vector<unsigned long long>& red);
 double clip_of(const unsigned long long* red, int slot);
 void for_all(const Team& T, const std::function<void(ign_context*)>& f);
 constexpr int64_t kChunk = 256;  // steps between host synchronisations
+// device reduction slots: [0] lam_max bits, [1] dt_chem bits, then the clip
+// of every stage of every step of a chunk (2 + 3 step + stage - 1) — per step,
+// so a slab that runs past a peer's failure cannot overwrite clips the
+// failure's bookkeeping still needs (the error word is reduced once per chunk)
+constexpr int64_t kRedSlots = 2 + 3 * kChunk;
 void t_enqueue_chunk(const Team& T, int a0, double& t, double dt, int64_t done, int64_t chunk,
                      bool post_prepare);
 void t_finish_chunk(const Team& T, int a0, double dt, int64_t done, int64_t chunk);

@@ -90,7 +90,8 @@ template <int NS, int DIR, bool TENO, bool CHAR>
 #define IGN_FACES_MINB 4
 #endif
 __global__ void __launch_bounds__(32 * (NS + 3), (NS == 1 ? IGN_FACES_MINB : 1))
-k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {
+k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
+         int f_lo, int f_hi) {
     using Smem = FaceSmem<NS, DIR, TENO, CHAR>;
     constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
     constexpr int NV = Smem::NV;
@@ -121,7 +122,8 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             f0 = blockIdx.x * NF;
         }
     } else {
-        f0 = blockIdx.y * NC;
+        // y faces [f_lo, f_hi) of the line (a slab splits interior and halo faces)
+        f0 = f_lo + blockIdx.y * NC;
     }
     const int i0 = blockIdx.x * 32;
     const long long win0 = DIR == 0 ? 0 : pidx(P, i0, f0 - H);
@@ -183,7 +185,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         my_col = i0 + lane;
     }
     const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < P.ny)
-                                    : (my_col < P.nx && my_f <= P.ny);
+                                    : (my_col < P.nx && my_f < f_hi);
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
     auto err_index = [&](int f, int col) -> unsigned long long {
         // global (line, face) order of inviscid_direction (solver.hpp:450-481)
@@ -465,22 +467,25 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR>
-inline void launch_faces3(const KParams& P, const double* Ut, int stage, int step,
-                          cudaStream_t s) {
+inline int launch_faces3(const KParams& P, const double* Ut, int stage, int step,
+                          cudaStream_t s, int f_lo = 0, int f_hi = -1) {
     constexpr int NC = NS + 3;
     const size_t smem = sizeof(FaceSmem<NS, DIR, TENO, CHAR>);
     auto kern = k_faces3<NS, DIR, TENO, CHAR>;
     static std::atomic<unsigned long long> configured{0};  // per instantiation, per device
     configure_kernel(kern, smem, NC, configured, "k_faces3");
     const int NF = 32 * NC;
+    if (f_hi < 0) f_hi = (DIR == 0 ? P.nx : P.ny) + 1;
+    if (f_hi <= f_lo) return 0;
     dim3 grid;
     if (DIR == 0)
         grid = P.nx + 1 >= NF  // flattened rows: (nx+1) ny faces in runs of NF
                    ? dim3((unsigned)(((long long)(P.nx + 1) * P.ny + NF - 1) / NF), 1)
                    : dim3((P.nx + 1 + NF - 1) / NF, P.ny);
     else
-        grid = dim3((P.nx + 31) / 32, (P.ny + 1 + NC - 1) / NC);
-    kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step);
+        grid = dim3((P.nx + 31) / 32, (f_hi - f_lo + NC - 1) / NC);
+    kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step, f_lo, f_hi);
+    return 1;
 }
 
 }  // namespace ign

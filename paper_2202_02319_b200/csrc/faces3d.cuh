@@ -95,7 +95,8 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
 #endif
 template <int NS, int DIR, bool TENO, bool CHAR>
 __global__ void __launch_bounds__(32 * (NS + 4), (NS == 1 && DIR == 0 && CHAR) ? IGN_X_MINB : 1)
-k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step) {
+k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
+          int f_lo, int f_hi) {
     using Smem = FaceSmem3<NS, DIR, TENO, CHAR>;
     constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
     constexpr int NV = Smem::NV;
@@ -127,7 +128,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             f0 = blockIdx.x * NF;
         }
     } else {
-        f0 = (DIR == 1 ? blockIdx.y : blockIdx.z) * NC;
+        // faces [f_lo, f_hi) along DIR (a z-slab splits interior and halo faces)
+        f0 = f_lo + (DIR == 1 ? blockIdx.y : blockIdx.z) * NC;
     }
     const int i0 = blockIdx.x * 32;
     const int jb = DIR == 2 ? blockIdx.y : 0;  // fixed j (DIR 2)
@@ -170,7 +172,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         my_col = i0 + lane;
     }
     const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < nrows)
-                                    : (my_col < P.nx && my_f <= nd);
+                                    : (my_col < P.nx && my_f < f_hi);
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;  // z faces share the y code
     auto err_index = [&](int f, int col) -> unsigned long long {
         // face f of the line through col (DIR 0: flattened row k ny + j): global
@@ -530,14 +532,16 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR>
-inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int step,
-                           cudaStream_t s) {
+inline int launch_faces3d(const KParams& P, const double* Ut, int stage, int step,
+                           cudaStream_t s, int f_lo = 0, int f_hi = -1) {
     constexpr int NC = NS + 4;
     const size_t smem = sizeof(FaceSmem3<NS, DIR, TENO, CHAR>);
     auto kern = k_faces3d<NS, DIR, TENO, CHAR>;
     static std::atomic<unsigned long long> configured{0};  // per instantiation, per device
     configure_kernel(kern, smem, NC, configured, "k_faces3d");
     const int NF = 32 * NC;
+    if (f_hi < 0) f_hi = (DIR == 0 ? P.nx : DIR == 1 ? P.ny : P.nz) + 1;
+    if (f_hi <= f_lo) return 0;
     dim3 grid;
     if (DIR == 0) {
         if (P.nx + 1 >= NF)  // flattened rows: (nx+1) ny nz faces in runs of NF
@@ -545,9 +549,10 @@ inline void launch_faces3d(const KParams& P, const double* Ut, int stage, int st
         else
             grid = dim3((P.nx + 1 + NF - 1) / NF, P.ny, P.nz);
     }
-    else if (DIR == 1) grid = dim3((P.nx + 31) / 32, (P.ny + 1 + NC - 1) / NC, P.nz);
-    else grid = dim3((P.nx + 31) / 32, P.ny, (P.nz + 1 + NC - 1) / NC);
-    kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step);
+    else if (DIR == 1) grid = dim3((P.nx + 31) / 32, (f_hi - f_lo + NC - 1) / NC, P.nz);
+    else grid = dim3((P.nx + 31) / 32, P.ny, (f_hi - f_lo + NC - 1) / NC);
+    kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step, f_lo, f_hi);
+    return 1;
 }
 
 }  // namespace ign

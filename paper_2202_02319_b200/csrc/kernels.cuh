@@ -173,10 +173,10 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
 template <int NS, bool WX>
 __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim(const __grid_constant__ KParams P,
                                               const double* __restrict__ Ut, int stage,
-                                              int step) {
+                                              int step, long long id_lo, long long id_hi) {
     if (failed(P.err)) return;
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= P.plane) return;
+    const long long id = id_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= id_hi) return;
     const double J = P.jac[id];
     double U[NS + 3];
 #pragma unroll
@@ -546,24 +546,47 @@ template <int NS> struct Launch {
         k_bc<NS><<<(2 * n + 127) / 128, 128, 0, s>>>(P, Ut, ypass, stage, step);
         return 1;
     }
-    static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        const unsigned nb = (unsigned)((P.plane + 255) / 256);
-        if (P.viscous) k_prim<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step);
-        else k_prim<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step);
+    // padded rows [r_lo, r_hi)
+    static int prim_rows(const KParams& P, const double* Ut, int stage, int step,
+                         cudaStream_t s, int r_lo, int r_hi) {
+        const long long lo = (long long)r_lo * P.sx, hi = (long long)r_hi * P.sx;
+        if (hi <= lo) return 0;
+        const unsigned nb = (unsigned)((hi - lo + 255) / 256);
+        if (P.viscous) k_prim<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+        else k_prim<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
         return 1;
     }
+    // part (KernelSet): 0 the padded box, 1 this slab's own rows, 2 its ghost rows
+    static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
+                    int part) {
+        const int g = P.g, R = P.ny + 2 * g;
+        if (part == 1) return prim_rows(P, Ut, stage, step, s, g, R - g);
+        if (part == 2)
+            return prim_rows(P, Ut, stage, step, s, 0, g) +
+                   prim_rows(P, Ut, stage, step, s, R - g, R);
+        return prim_rows(P, Ut, stage, step, s, 0, R);
+    }
+    // part: 0 every face; 1 x faces + the y faces whose stencils lie in owned
+    // rows; 2 the remaining y faces (they read the halo rows)
     template <bool TENO, bool CHAR>
-    static void faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        launch_faces3<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
-        launch_faces3<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
+    static int faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
+                       int part) {
+        constexpr int H = TENO ? 3 : 2;
+        const int lo = H < P.ny + 1 ? H : P.ny + 1;
+        const int hi = P.ny - H + 1 > lo ? P.ny - H + 1 : lo;
+        int n = 0;
+        if (part != 2) n += launch_faces3<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
+        if (part == 0) return n + launch_faces3<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
+        if (part == 1) return n + launch_faces3<NS, 1, TENO, CHAR>(P, Ut, stage, step, s, lo, hi);
+        n += launch_faces3<NS, 1, TENO, CHAR>(P, Ut, stage, step, s, 0, lo);
+        return n + launch_faces3<NS, 1, TENO, CHAR>(P, Ut, stage, step, s, hi, P.ny + 1);
     }
     static int faces(const KParams& P, int teno, int chr, const double* Ut, int stage, int step,
-                     cudaStream_t s) {
-        if (teno && chr) faces_t<true, true>(P, Ut, stage, step, s);
-        else if (teno) faces_t<true, false>(P, Ut, stage, step, s);
-        else if (chr) faces_t<false, true>(P, Ut, stage, step, s);
-        else faces_t<false, false>(P, Ut, stage, step, s);
-        return 2;
+                     cudaStream_t s, int part) {
+        if (teno && chr) return faces_t<true, true>(P, Ut, stage, step, s, part);
+        if (teno) return faces_t<true, false>(P, Ut, stage, step, s, part);
+        if (chr) return faces_t<false, true>(P, Ut, stage, step, s, part);
+        return faces_t<false, false>(P, Ut, stage, step, s, part);
     }
     static int visc(const KParams& P, int stage, int step, cudaStream_t s) {
         const long long n = (long long)(P.nx + 2) * (P.ny + 2);

@@ -165,11 +165,11 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
 template <int NS, bool WX>
 __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim3(const __grid_constant__ KParams P,
                                                const double* __restrict__ Ut, int stage,
-                                               int step) {
+                                               int step, int k_lo) {
     if (failed(P.err)) return;
     const int id2 = blockIdx.x * blockDim.x + threadIdx.x;  // (x, y) plane index
     if (id2 >= P.sxy) return;
-    const long long id = (long long)blockIdx.y * P.sxy + id2;  // blockIdx.y: padded k
+    const long long id = (long long)(blockIdx.y + k_lo) * P.sxy + id2;  // padded k
     const double J = P.jac[id2];
     double U[NS + 4];
 #pragma unroll
@@ -577,25 +577,49 @@ template <int NS> struct Launch3 {
         k_bc3<NS><<<(unsigned)((n2 + 127) / 128), 128, 0, s>>>(P, Ut, 2, stage, step);
         return 1;
     }
-    static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        const dim3 nb((unsigned)((P.sxy + 255) / 256), P.nz + 2 * P.g);
-        if (P.viscous) k_prim3<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step);
-        else k_prim3<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step);
+    // padded z planes [k_lo, k_hi)
+    static int prim_planes(const KParams& P, const double* Ut, int stage, int step,
+                           cudaStream_t s, int k_lo, int k_hi) {
+        if (k_hi <= k_lo) return 0;
+        const dim3 nb((unsigned)((P.sxy + 255) / 256), (unsigned)(k_hi - k_lo));
+        if (P.viscous) k_prim3<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+        else k_prim3<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
         return 1;
     }
+    // part (KernelSet): 0 the padded box, 1 this slab's own planes, 2 its ghost planes
+    static int prim(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
+                    int part) {
+        const int g = P.g, K = P.nz + 2 * g;
+        if (part == 1) return prim_planes(P, Ut, stage, step, s, g, K - g);
+        if (part == 2)
+            return prim_planes(P, Ut, stage, step, s, 0, g) +
+                   prim_planes(P, Ut, stage, step, s, K - g, K);
+        return prim_planes(P, Ut, stage, step, s, 0, K);
+    }
+    // part: 0 every face; 1 x, y faces + the z faces whose stencils lie in
+    // owned planes; 2 the remaining z faces (they read the halo planes)
     template <bool TENO, bool CHAR>
-    static void faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s) {
-        launch_faces3d<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
-        launch_faces3d<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
-        launch_faces3d<NS, 2, TENO, CHAR>(P, Ut, stage, step, s);
+    static int faces_t(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
+                       int part) {
+        constexpr int H = TENO ? 3 : 2;
+        const int lo = H < P.nz + 1 ? H : P.nz + 1;
+        const int hi = P.nz - H + 1 > lo ? P.nz - H + 1 : lo;
+        int n = 0;
+        if (part != 2) {
+            n += launch_faces3d<NS, 0, TENO, CHAR>(P, Ut, stage, step, s);
+            n += launch_faces3d<NS, 1, TENO, CHAR>(P, Ut, stage, step, s);
+        }
+        if (part == 0) return n + launch_faces3d<NS, 2, TENO, CHAR>(P, Ut, stage, step, s);
+        if (part == 1) return n + launch_faces3d<NS, 2, TENO, CHAR>(P, Ut, stage, step, s, lo, hi);
+        n += launch_faces3d<NS, 2, TENO, CHAR>(P, Ut, stage, step, s, 0, lo);
+        return n + launch_faces3d<NS, 2, TENO, CHAR>(P, Ut, stage, step, s, hi, P.nz + 1);
     }
     static int faces(const KParams& P, int teno, int chr, const double* Ut, int stage, int step,
-                     cudaStream_t s) {
-        if (teno && chr) faces_t<true, true>(P, Ut, stage, step, s);
-        else if (teno) faces_t<true, false>(P, Ut, stage, step, s);
-        else if (chr) faces_t<false, true>(P, Ut, stage, step, s);
-        else faces_t<false, false>(P, Ut, stage, step, s);
-        return 3;
+                     cudaStream_t s, int part) {
+        if (teno && chr) return faces_t<true, true>(P, Ut, stage, step, s, part);
+        if (teno) return faces_t<true, false>(P, Ut, stage, step, s, part);
+        if (chr) return faces_t<false, true>(P, Ut, stage, step, s, part);
+        return faces_t<false, false>(P, Ut, stage, step, s, part);
     }
     static int visc(const KParams& P, int stage, int step, cudaStream_t s) {
         const long long n = (long long)(P.nx + 2) * (P.ny + 2) * (P.nz + 2);

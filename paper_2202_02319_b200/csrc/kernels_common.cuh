@@ -153,9 +153,11 @@ namespace ign {
 // returns the number of kernels it launched.
 struct KernelSet {
     int (*bc)(const KParams&, double* Ut, int ypass, int stage, int step, cudaStream_t);
-    int (*prim)(const KParams&, const double* Ut, int stage, int step, cudaStream_t);
+    // part: 0 whole box / every face; 1 what a slab computes from its own
+    // rows (planes) while its halo is in flight; 2 what needs the halo
+    int (*prim)(const KParams&, const double* Ut, int stage, int step, cudaStream_t, int part);
     int (*faces)(const KParams&, int teno, int chr, const double* Ut, int stage, int step,
-                 cudaStream_t);
+                 cudaStream_t, int part);
     int (*visc)(const KParams&, int stage, int step, cudaStream_t);
     int (*assemble)(const KParams&, int mode, const double* U0, const double* Ucur,
                     double* Uout, double dt, double w, double t_stage, int stage, int step,

@@ -107,6 +107,7 @@ double* dalloc(size_t n) {
 // Every rank reads the same (MIN-reduced) error word: a failure in the last
 // kernels before this point (e.g. a step's final update) is seen everywhere.
 DevFail sync_and_read(const Team& T) {
+    t_join(T);
     t_errsync(T);
     cuda_check(cudaStreamSynchronize(T.stream()), "kernel execution");
     cuda_check(cudaGetLastError(), "kernel launch");
@@ -189,7 +190,7 @@ void t_errsync(const Team& T) {
 // neighbours, their rows into our ghost rows (all components; rows are
 // contiguous in the padded planes, so every transfer is one contiguous chunk).
 // 2D: y-slabs exchange g padded rows; 3D: z-slabs exchange g padded planes
-void t_exchange(const Team& T, int buf) {
+void t_exchange(const Team& T, int buf, cudaStream_t stream) {
     if (T.local()) {
         for (ign_context* c : T.m) {
             const size_t st = halo_stride(c), chunk = size_t(c->g) * st;
@@ -199,7 +200,7 @@ void t_exchange(const Team& T, int buf) {
                     cuda_check(cudaMemcpyAsync(c->S[buf] + comp * c->plane,
                                                s->S[buf] + comp * s->plane + halo_count(s) * st,
                                                chunk * sizeof(double), cudaMemcpyDeviceToDevice,
-                                               T.stream()),
+                                               stream),
                                "halo copy");
                 }
                 if (c->hi_peer >= 0) {
@@ -208,7 +209,7 @@ void t_exchange(const Team& T, int buf) {
                                                    (halo_count(c) + c->g) * st,
                                                s->S[buf] + comp * s->plane + chunk,
                                                chunk * sizeof(double), cudaMemcpyDeviceToDevice,
-                                               T.stream()),
+                                               stream),
                                "halo copy");
                 }
             }
@@ -228,51 +229,119 @@ void t_exchange(const Team& T, int buf) {
         // receives, so a two-slab periodic ring matches correctly
         if (c->hi_peer >= 0)
             nccl_check(n.Send(base + nl * st, chunk, ncclFloat64, c->hi_peer,
-                              c->comm, c->stream), "ncclSend");
+                              c->comm, stream), "ncclSend");
         if (c->lo_peer >= 0)
-            nccl_check(n.Send(base + chunk, chunk, ncclFloat64, c->lo_peer, c->comm, c->stream),
+            nccl_check(n.Send(base + chunk, chunk, ncclFloat64, c->lo_peer, c->comm, stream),
                        "ncclSend");
         if (c->lo_peer >= 0)
-            nccl_check(n.Recv(base, chunk, ncclFloat64, c->lo_peer, c->comm, c->stream),
+            nccl_check(n.Recv(base, chunk, ncclFloat64, c->lo_peer, c->comm, stream),
                        "ncclRecv");
         if (c->hi_peer >= 0)
             nccl_check(n.Recv(base + (nl + c->g) * st, chunk, ncclFloat64,
-                              c->hi_peer, c->comm, c->stream), "ncclRecv");
+                              c->hi_peer, c->comm, stream), "ncclRecv");
     }
     nccl_check(n.GroupEnd(), "ncclGroupEnd");
 }
 
+bool t_has_halo(const Team& T) {
+    for (const ign_context* c : T.m)
+        if (c->lo_peer >= 0 || c->hi_peer >= 0) return true;
+    return false;
+}
+
+// The halo overlap can be switched off (IGN_HALO_OVERLAP=0) to compare the
+// two schedules; results are bitwise identical either way.
+static bool overlap_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("IGN_HALO_OVERLAP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+static void ensure_halo_stream(ign_context* L) {
+    if (L->halo_stream) return;
+    cuda_check(cudaStreamCreateWithFlags(&L->halo_stream, cudaStreamNonBlocking), "halo stream");
+    cuda_check(cudaEventCreateWithFlags(&L->ev_ready, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&L->ev_halo, cudaEventDisableTiming), "event");
+}
+
+// Orders the team's stream after a pending halo leg.
+void t_join(const Team& T) {
+    ign_context* L = T.lead();
+    if (!L->halo_pending) return;
+    cuda_check(cudaStreamWaitEvent(T.stream(), L->ev_halo, 0), "halo join");
+    L->halo_pending = false;
+}
+
 // prepare_stage (solver.hpp:422-425): fill_ghosts (x edges, halo, y edges)
-// then refresh_primitives
+// then refresh_primitives.  A slab overlaps its halo: once the
+// x (3D: x, y) edge ghosts of its own rows exist, the halo leg — NCCL
+// send/recv of the g boundary rows (planes), the remaining edge ghosts and the
+// ghost-row primitives — runs on the halo stream while the team's stream
+// computes the primitives of the slab's own rows and, in t_fluxes, every face
+// whose stencil lies in those rows; only the halo faces, the viscous fluxes
+// and the update wait for it.  Every kernel writes disjoint data in both
+// orders, so the results are bitwise those of the serial schedule.
 void t_prepare(const Team& T, int buf, int stage, int step) {
+    t_join(T);  // the previous halo leg (a re-prepare without fluxes) is done
     for (ign_context* c : T.m)
         c->launches += timed(c, IGN_PROF_BC, [&] {
             return c->ks.bc(c->kp, c->S[buf], 0, stage, step, c->stream);
         });
-    t_exchange(T, buf);
-    for (ign_context* c : T.m)
-        c->launches += timed(c, IGN_PROF_BC, [&] {
-            return c->ks.bc(c->kp, c->S[buf], 1, stage, step, c->stream);
-        });
+    if (!t_has_halo(T) || !overlap_enabled()) {
+        t_exchange(T, buf, T.stream());
+        for (ign_context* c : T.m)
+            c->launches += timed(c, IGN_PROF_BC, [&] {
+                return c->ks.bc(c->kp, c->S[buf], 1, stage, step, c->stream);
+            });
+        for (ign_context* c : T.m)
+            c->launches += timed(c, IGN_PROF_PRIM, [&] {
+                return c->ks.prim(c->kp, c->S[buf], stage, step, c->stream, 0);
+            });
+        return;
+    }
+    ign_context* L = T.lead();
+    ensure_halo_stream(L);
+    cudaStream_t hs = L->halo_stream;
+    cuda_check(cudaEventRecord(L->ev_ready, T.stream()), "event");
+    cuda_check(cudaStreamWaitEvent(hs, L->ev_ready, 0), "halo wait");
+    t_exchange(T, buf, hs);
+    for (ign_context* c : T.m) c->launches += c->ks.bc(c->kp, c->S[buf], 1, stage, step, hs);
+    for (ign_context* c : T.m) c->launches += c->ks.prim(c->kp, c->S[buf], stage, step, hs, 2);
+    cuda_check(cudaEventRecord(L->ev_halo, hs), "event");
+    L->halo_pending = true;
     for (ign_context* c : T.m)
         c->launches += timed(c, IGN_PROF_PRIM, [&] {
-            return c->ks.prim(c->kp, c->S[buf], stage, step, c->stream);
+            return c->ks.prim(c->kp, c->S[buf], stage, step, c->stream, 1);
         });
-    t_errsync(T);
 }
 
 void t_fluxes(const Team& T, int buf, int stage, int step) {
-    for (ign_context* c : T.m) {
+    const bool split = T.lead()->halo_pending;
+    for (ign_context* c : T.m)
         c->launches += timed(c, IGN_PROF_FACES, [&] {
             return c->ks.faces(c->kp, c->cfg.scheme.scheme, c->cfg.scheme.split, c->S[buf], stage,
-                               step, c->stream);
+                               step, c->stream, split ? 1 : 0);
         });
+    if (split) {
+        t_join(T);
+        for (ign_context* c : T.m)
+            c->launches += timed(c, IGN_PROF_FACES, [&] {
+                return c->ks.faces(c->kp, c->cfg.scheme.scheme, c->cfg.scheme.split, c->S[buf],
+                                   stage, step, c->stream, 2);
+            });
+    }
+    for (ign_context* c : T.m)
         if (c->cfg.viscous)
             c->launches += timed(c, IGN_PROF_VISC,
                                  [&] { return c->ks.visc(c->kp, stage, step, c->stream); });
-    }
 }
 
+// No error-word reduction here: each slab's kernels stop on their own word,
+// and the words are MIN-reduced once per chunk (sync_and_read) — the first
+// failure of any slab carries the smallest key, because a slab fed stale halo
+// rows by a failed peer can only fail at a later (step, stage, phase).
 void t_assemble(const Team& T, int mode, int a, int cur, int out, double dt, double w, double t,
                 int stage, int step, int slot) {
     for (ign_context* c : T.m)
@@ -280,11 +349,9 @@ void t_assemble(const Team& T, int mode, int a, int cur, int out, double dt, dou
             return c->ks.assemble(c->kp, mode, c->S[a], c->S[cur], c->S[out], dt, w, t, stage,
                                   step, slot, c->stream);
         });
-    t_errsync(T);
 }
 
-// Zeroes one step's clip slots unless a failure is pending (a pending failure
-// must keep the previous step's clips for last_clip, solver.hpp:847).
+// Zeroes one step's clip slots (slot = 3 step) unless a failure is pending.
 __global__ void k_clip_reset(const ErrRec* err, unsigned long long* red, int slot) {
     if (failed(err)) return;
     red[2 + slot + threadIdx.x] = 0ull;
@@ -294,7 +361,7 @@ __global__ void k_clip_reset(const ErrRec* err, unsigned long long* red, int slo
 // post_prepare appends advance()'s prepare_stage(1) (solver.hpp:345).
 void t_step(const Team& T, int a, double time, double dt, int step, bool post_prepare) {
     const int b = (a + 1) % 3, c = (a + 2) % 3;
-    const int slot = (step & 1) * 3;
+    const int slot = step * 3;  // step < kChunk: its own three clip slots
     for (ign_context* x : T.m) {
         k_clip_reset<<<1, 3, 0, x->stream>>>(x->err, x->red, slot);
         ++x->launches;
@@ -313,20 +380,23 @@ void t_step(const Team& T, int a, double time, double dt, int step, bool post_pr
     if (post_prepare) t_prepare(T, b, 4, step);
 }
 
-// Clip slots of all slabs (MAX over slabs: the reference's clip is a max).
-void read_clips(const Team& T, unsigned long long red[8]) {
+// Clip slots of a chunk's steps over all slabs (MAX: the reference's clip is a max).
+void read_clips(const Team& T, int64_t chunk, std::vector<unsigned long long>& red) {
+    const size_t n = size_t(2 + 3 * chunk);
     ign_context* L = T.lead();
     if (!T.local() && L->comm) {
-        nccl_check(nccl().AllReduce(L->red + 2, L->red + 2, 6, ncclUint64, ncclMax, L->comm,
+        nccl_check(nccl().AllReduce(L->red + 2, L->red + 2, n - 2, ncclUint64, ncclMax, L->comm,
                                     L->stream),
                    "ncclAllReduce(clip)");
         cuda_check(cudaStreamSynchronize(L->stream), "clip reduce");
     }
-    std::memset(red, 0, 8 * sizeof(unsigned long long));
+    red.assign(n, 0ull);
+    std::vector<unsigned long long> r(n);
     for (ign_context* c : T.m) {
-        unsigned long long r[8];
-        cuda_check(cudaMemcpy(r, c->red, sizeof(r), cudaMemcpyDeviceToHost), "reductions");
-        for (int k = 2; k < 8; ++k) red[k] = std::max(red[k], r[k]);
+        cuda_check(cudaMemcpy(r.data(), c->red, n * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost),
+                   "reductions");
+        for (size_t k = 2; k < n; ++k) red[k] = std::max(red[k], r[k]);
     }
 }
 
@@ -357,11 +427,12 @@ void t_enqueue_chunk(const Team& T, int a0, double& t, double dt, int64_t done, 
 // last_clip at the point it would have thrown, then throw.
 void t_finish_chunk(const Team& T, int a0, double dt, int64_t done, int64_t chunk) {
     const DevFail f = sync_and_read(T);
-    unsigned long long red[8];
-    read_clips(T, red);
+    std::vector<unsigned long long> redv;
+    read_clips(T, chunk, redv);
+    const unsigned long long* red = redv.data();
     if (!f.any) {
         const int last = (int)(chunk - 1);
-        const int slot = (last & 1) * 3;
+        const int slot = last * 3;
         const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
                                    clip_of(red, slot + 2));
         for_all(T, [&](ign_context* c) {
@@ -378,12 +449,12 @@ void t_finish_chunk(const Team& T, int a0, double dt, int64_t done, int64_t chun
     const int64_t k = done + kk;
     double clip_prev = T.lead()->last_clip;
     if (kk > 0) {
-        const int slot = ((int)(kk - 1) & 1) * 3;
+        const int slot = (int)(kk - 1) * 3;
         clip_prev = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
                              clip_of(red, slot + 2));
     }
     const int ak = (int)((a0 + k) % 3);
-    const int slot = ((int)kk & 1) * 3;
+    const int slot = (int)kk * 3;
     const Error e = to_error(T.lead(), f);
     if (f.stage == 4) {  // advance's prepare_stage(1) after a completed step
         const double lc = std::max(std::max(clip_of(red, slot), clip_of(red, slot + 1)),
@@ -476,6 +547,7 @@ void t_run_ensemble(const std::vector<ign_context*>& mem, const double* dt, int6
 }
 
 double t_stable_dt(const Team& T) {
+    t_join(T);
     unsigned long long init[2] = {0ull, 0x7ff0000000000000ull};
     for (ign_context* c : T.m) {
         cuda_check(cudaMemcpyAsync(c->red, init, sizeof(init), cudaMemcpyHostToDevice, c->stream),

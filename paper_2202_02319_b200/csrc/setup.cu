@@ -149,6 +149,9 @@ void destroy_impl(ign_context* ctx) {
     for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
     if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
+    if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     delete ctx;
 }
 
@@ -330,9 +333,9 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     ctx->own_err = static_cast<ErrRec*>(p);
     ctx->err = ctx->own_err;
     cuda_check(cudaMemset(ctx->err, 0xff, sizeof(ErrRec)), "memset");
-    cuda_check(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc");
+    cuda_check(cudaMalloc(&p, kRedSlots * sizeof(unsigned long long)), "cudaMalloc");
     ctx->red = static_cast<unsigned long long*>(p);
-    cuda_check(cudaMemset(ctx->red, 0, 8 * sizeof(unsigned long long)), "memset");
+    cuda_check(cudaMemset(ctx->red, 0, kRedSlots * sizeof(unsigned long long)), "memset");
 
     KParams& k = ctx->kp;
     std::memset(&k, 0, sizeof(k));
