@@ -438,8 +438,10 @@ int ign_group_create(ign_context** members, int n, ign_group** out) {
             ign_context* c = members[r];
             c->group = grp;
             c->stream = members[0]->own_stream;  // lockstep on one stream
-            c->err = members[0]->own_err;        // one error word for the group
-            c->kp.err = c->err;
+            // each slab keeps its OWN error word, exactly as NCCL ranks do: a
+            // slab runs on past a peer's failure and the words are MIN-folded
+            // once per chunk (sync_and_read), so the group validates the
+            // multi-rank failure semantics on one GPU
             grp->m.push_back(c);
         }
     });

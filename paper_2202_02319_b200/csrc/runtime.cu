@@ -112,9 +112,12 @@ DevFail sync_and_read(const Team& T) {
     cuda_check(cudaStreamSynchronize(T.stream()), "kernel execution");
     cuda_check(cudaGetLastError(), "kernel launch");
     for (ign_context* c : T.m) prof_harvest(c);
-    ErrRec h;
-    ign_context* L = T.lead();
-    cuda_check(cudaMemcpy(&h, L->err, sizeof(h), cudaMemcpyDeviceToHost), "error word");
+    ErrRec h{kNoError};
+    for (ign_context* c : T.m) {  // NCCL: one (all-reduced) word; group: MIN over slabs
+        ErrRec w;
+        cuda_check(cudaMemcpy(&w, c->err, sizeof(w), cudaMemcpyDeviceToHost), "error word");
+        h.key = std::min(h.key, w.key);
+    }
     DevFail f;
     if (h.key == kNoError) return f;
     f.any = true;

@@ -131,3 +131,68 @@ def test_z_slab_initial_condition_coordinates(cuda_device):
         lo, cnt = slab_rows(18, 3, r)
         assert np.array_equal(m.mesh_z(), single.mesh_z()[lo:lo + cnt + 2 * single.g])
     grp.close()
+
+
+def _failure(fn):
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001 — the ignis exception is compared
+        return e
+    return None
+
+
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_slab_failure_semantics_match_single_domain(nslabs, cuda_device):
+    """Each slab keeps its own error word (as NCCL ranks do) and runs on past a
+    peer's failure; the words are MIN-folded once per chunk.  The first
+    failure, the restored state, iter/time and last_clip must still be the
+    undecomposed run's (solver.hpp:326-329; advance semantics of rk3_steps)."""
+    case = configs.tgv2d(24)
+    single = Simulation(case.cfg)
+    single.set_initial_condition(case.ic)
+    U0 = single.Ut
+    grp = SlabGroup(case.cfg, nslabs)
+    g = single.g
+    rows = [slab_rows(case.cfg.ny, nslabs, r) for r in range(nslabs)]
+    for r, (lo, cnt) in enumerate(rows):
+        grp.set_state(r, U0[:, lo:lo + cnt + 2 * g, :])
+    single.prepare_stage(1)
+    grp.prepare_stage(1)
+    dt = case.dt * 9.0  # marginally unstable: fails after a few steps
+    ea = _failure(lambda: single.rk3_steps(dt, 200))
+    eb = _failure(lambda: grp.rk3_steps(dt, 200))
+    if ea is None:
+        pytest.skip("no failure provoked")
+    assert type(ea) is type(eb), (ea, eb)
+    assert (getattr(ea, "stage", None), getattr(ea, "i", None), getattr(ea, "j", None)) == \
+        (getattr(eb, "stage", None), getattr(eb, "i", None), getattr(eb, "j", None))
+    Ug = single.Ut
+    for r, (lo, cnt) in enumerate(rows):
+        assert bitwise_equal(grp.Ut(r)[:, g:g + cnt], Ug[:, lo + g:lo + g + cnt]), r
+    import ctypes
+    t, it = ctypes.c_double(), ctypes.c_int64()
+    assert grp.member_call(0, "get_time", ctypes.byref(t), ctypes.byref(it)) == 0
+    assert it.value == single.iter and t.value == single.time
+    grp.close()
+
+
+def test_slab_prepare_failure_in_upper_slab(cuda_device):
+    """A bad node in the LAST slab: that slab's word alone records it; the
+    group reports the reference's StepFailure (stage, i, j) in global rows."""
+    case = configs.tgv2d(24)
+    single = Simulation(case.cfg)
+    single.set_initial_condition(case.ic)
+    U = single.Ut
+    U[0, 3 + 20, 3 + 7] = -1.0  # node (7, 20): slab 2 of 3
+    U[0, 3 + 22, 3 + 1] = -1.0
+    single.set_state(U)
+    grp = SlabGroup(case.cfg, 3)
+    g = single.g
+    rows = [slab_rows(24, 3, r) for r in range(3)]
+    for r, (lo, cnt) in enumerate(rows):
+        grp.set_state(r, U[:, lo:lo + cnt + 2 * g, :])
+    ea = _failure(lambda: single.prepare_stage(2))
+    eb = _failure(lambda: grp.prepare_stage(2))
+    assert ea is not None and type(ea) is type(eb)
+    assert (ea.stage, ea.i, ea.j) == (eb.stage, eb.i, eb.j) == (2, 7, 20)
+    grp.close()
