@@ -240,6 +240,14 @@ int ign_rk3_steps(ign_context* ctx, double dt, int64_t nsteps);
 int ign_conserved_totals(ign_context* ctx, double* tot);  /* solver.hpp:411-418 */
 int ign_product_mole_fraction(ign_context* ctx, double* out); /* :387-407 */
 int ign_last_clip(const ign_context* ctx, double* clip);  /* solver.hpp:75 */
+/* How conserved_totals / product_mole_fraction (and the trace advance()
+ * samples) reduce: IGN_DIAG_DEVICE (default) = deterministic fixed-shape tree
+ * on the device, no field download, within ~1e-15 sum|x| of the reference's
+ * serial sum; IGN_DIAG_REFERENCE = the reference's serial left fold
+ * (solver.hpp:387-418) on the host, bitwise.  Slab groups read the lead's. */
+#define IGN_DIAG_DEVICE 0
+#define IGN_DIAG_REFERENCE 1
+int ign_set_diagnostics(ign_context* ctx, int mode);
 
 /* ---- host-only helpers (no device needed; used by the CPU tests) ------- */
 /* compute_metrics over the configured mesh: which 0 = inviscid set, 1 = Central2 */

@@ -410,6 +410,13 @@ int ignref_last_clip(const ref_ctx* ctx, double* clip) {
     return IGN_OK;
 }
 
+// The reference always reduces serially (solver.hpp:387-418): any mode reads
+// the same values.
+int ignref_set_diagnostics(ref_ctx* ctx, int mode) {
+    (void)ctx;
+    return mode == IGN_DIAG_DEVICE || mode == IGN_DIAG_REFERENCE ? IGN_OK : IGN_USAGE_ERROR;
+}
+
 int ignref_host_metrics(const ign_config* cfg, int which, double* out,
                         ign_error* err) {
     return guarded(err, [&] {

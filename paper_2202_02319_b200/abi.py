@@ -34,6 +34,7 @@ PERIODIC, NOSLIP_ISOTHERMAL, NOSLIP_ADIABATIC, INFLOW, OUTFLOW = 0, 1, 2, 3, 4
 MM_AUTO, MM_CENTRAL2, MM_ORDER4, MM_ORDER6, MM_ANALYTIC_SKEW = -1, 0, 1, 2, 3
 CALORICALLY_PERFECT, MULTI_SPECIES = 0, 1
 LASER_GAUSSIAN, LASER_SHAPED = 0, 1
+DIAG_DEVICE, DIAG_REFERENCE = 0, 1  # ign_set_diagnostics
 
 
 class ThermoPiece(C.Structure):
@@ -161,6 +162,7 @@ SIGNATURES = {
     "conserved_totals": (_I, [_P, _D]),
     "product_mole_fraction": (_I, [_P, _D]),
     "last_clip": (_I, [_P, _D]),
+    "set_diagnostics": (_I, [_P, C.c_int]),
     "host_metrics": (_I, [C.POINTER(Config), _I, _D, C.POINTER(Error)]),
     "host_mesh": (_I, [C.POINTER(Config), _D, _D, C.POINTER(Error)]),
     "kernel_launches": (C.c_int64, [_P]),

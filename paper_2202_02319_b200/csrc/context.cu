@@ -348,6 +348,12 @@ int ign_product_mole_fraction(ign_context* ctx, double* out) {
     return guarded(ctx, [&] { *out = t_product_fraction(solo(ctx)); });
 }
 
+int ign_set_diagnostics(ign_context* ctx, int mode) {
+    if (!ctx || (mode != IGN_DIAG_DEVICE && mode != IGN_DIAG_REFERENCE)) return IGN_USAGE_ERROR;
+    ctx->diag_mode = mode;
+    return IGN_OK;
+}
+
 int ign_last_clip(const ign_context* ctx, double* clip) {
     *clip = ctx->last_clip;
     return IGN_OK;

@@ -96,6 +96,10 @@ struct ign_context {
     cudaStream_t halo_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     bool halo_pending = false;
+    // diagnostics (conserved_totals, product fraction): device tree (default)
+    // or the reference's serial order on the host (bitwise)
+    int diag_mode = IGN_DIAG_DEVICE;
+    double* diag_buf = nullptr;
     // slab decomposition
     int nranks = 1, rank = 0;
     int lo_peer = -1, hi_peer = -1;  // ranks owning our ghost rows (-1: physical edge)

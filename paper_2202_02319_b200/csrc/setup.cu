@@ -150,6 +150,7 @@ void destroy_impl(ign_context* ctx) {
     if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
+    if (ctx->diag_buf) cudaFree(ctx->diag_buf);
     if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     delete ctx;

@@ -215,6 +215,13 @@ class Simulation:
         self._check(self._api["conserved_totals"](self._h, _dptr(out)))
         return out
 
+    def set_diagnostics(self, mode: str = "device"):
+        """conserved_totals / product_mole_fraction / the trace: "device" =
+        deterministic tree on the GPU (default), "reference" = the reference's
+        serial order (solver.hpp:387-418) on the host, bitwise."""
+        m = {"device": abi.DIAG_DEVICE, "reference": abi.DIAG_REFERENCE}[mode]
+        self._check(self._api["set_diagnostics"](self._h, m))
+
     def product_mole_fraction(self) -> float:
         out = C.c_double()
         self._check(self._api["product_mole_fraction"](self._h, C.byref(out)))
@@ -360,6 +367,11 @@ class SlabGroup:
         dt = C.c_double()
         self._check(self._api["group_stable_dt"](self._g, C.byref(dt)))
         return dt.value
+
+    def set_diagnostics(self, mode: str = "device"):
+        m = {"device": abi.DIAG_DEVICE, "reference": abi.DIAG_REFERENCE}[mode]
+        for k in range(len(self.members)):
+            self._check(self.member_call(k, "set_diagnostics", m))
 
     def conserved_totals(self) -> np.ndarray:
         out = np.empty(self.members[0].nc)

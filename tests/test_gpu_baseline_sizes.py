@@ -49,6 +49,7 @@ def test_sod_configs0_full_run(oracle_api, cuda_device, scheme, split, dt):
 def test_tgv2d_256_200_steps_bitwise(oracle_api, cuda_device):
     case = configs.tgv2d(256)
     prod, refs = _pair(case, oracle_api)
+    prod.set_diagnostics("reference")
     for s in (prod, refs):
         s.prepare_stage(1)
         s.rk3_steps(case.dt, 200)

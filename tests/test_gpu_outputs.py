@@ -106,6 +106,7 @@ def _probe_boxes(nx, ny):
 def test_probes_and_trace_through_advance(mk, exact, oracle_api, cuda_device):
     case = mk()
     prod, refs = make_pair(case, oracle_api)
+    prod.set_diagnostics("reference")  # the trace in the reference's serial order
     for s in (prod, refs):
         for b in _probe_boxes(case.cfg.nx, case.cfg.ny):
             s.add_probe(*b)
@@ -128,6 +129,20 @@ def test_probes_and_trace_through_advance(mk, exact, oracle_api, cuda_device):
         assert np.allclose(va, vb, rtol=1e-10, atol=1e-300)
 
 
+def test_device_tree_trace_within_tolerance(oracle_api, cuda_device):
+    """Default diagnostics: the product trace reduced on the device (fixed
+    tree, no Y download) within 1e-13 of the reference's serial fold."""
+    case = configs.reacting_ch4(24)
+    prod, refs = make_pair(case, oracle_api)
+    for s in (prod, refs):
+        s.set_sampling(0, 1)
+        s.set_integrator(fixed_dt=case.dt, t_end=4.5 * case.dt)
+        s.advance()
+    (ta, va), (tb, vb) = prod.trace(), refs.trace()
+    assert np.array_equal(ta, tb) and len(ta) == 6
+    assert np.all(np.abs(va - vb) <= 1e-13 * np.abs(vb)), np.abs(va - vb).max()
+
+
 def test_probe_box_validation(oracle_api, cuda_device):
     case = configs.tgv2d(16)
     prod, refs = make_pair(case, oracle_api)
@@ -146,6 +161,8 @@ def test_slab_outputs_match_single_domain(nslabs, tmp_path, cuda_device):
     single = Simulation(clone_cfg(case.cfg))
     single.set_initial_condition(case.ic)
     grp = SlabGroup(case.cfg, nslabs)
+    single.set_diagnostics("reference")  # serial folds: decomposition-invariant bits
+    grp.set_diagnostics("reference")
     U0 = single.Ut
     g = single.g
     from tests.test_gpu_slabs import slab_rows

@@ -174,12 +174,33 @@ def test_advance_hook_nonzero_stops(oracle_api, cuda_device):
 
 
 def test_diagnostics_bitwise(oracle_api, cuda_device):
+    """IGN_DIAG_REFERENCE: the reference's serial folds, bitwise."""
     case = configs.reacting_ch4(24)
     prod, refs = make_pair(case, oracle_api)
+    prod.set_diagnostics("reference")
     for s in (prod, refs):
         s.prepare_stage(1)
     assert bitwise_equal(prod.conserved_totals(), refs.conserved_totals())
     assert prod.product_mole_fraction() == refs.product_mole_fraction()
+
+
+@pytest.mark.parametrize("mk", [lambda: configs.reacting_ch4(40), lambda: configs.tgv2d(64),
+                                lambda: configs.h2o2_counterflow(48)], ids=["ch4", "tgv", "h2o2"])
+def test_diagnostics_device_tree(mk, oracle_api, cuda_device):
+    """Default IGN_DIAG_DEVICE: deterministic device tree sums within
+    1e-12 sum|x| (totals) / 1e-13 (product fraction) of the serial fold."""
+    case = mk()
+    prod, refs = make_pair(case, oracle_api)
+    for s in (prod, refs):
+        s.prepare_stage(1)
+        s.rk3_steps(case.dt, 3)
+    ta, tb = prod.conserved_totals(), refs.conserved_totals()
+    U = refs.Ut[:, 3:-3, 3:-3]
+    bound = 1e-12 * np.abs(U).reshape(U.shape[0], -1).sum(axis=1)
+    assert np.all(np.abs(ta - tb) <= bound), (ta - tb, bound)
+    assert bitwise_equal(ta, prod.conserved_totals())  # deterministic
+    pa, pb = prod.product_mole_fraction(), refs.product_mole_fraction()
+    assert abs(pa - pb) <= 1e-13 * abs(pb) + 1e-300
 
 
 def _raises_same(fa, fb):
