@@ -63,16 +63,24 @@ UNIT = "cell-updates/s"
 # (3 face directions, nc 5); the inviscid share scaled from the 2D count by
 # the ratio of FP64 instructions the 3D and 2D face kernels execute per cell
 # and stage (ncu, profiles/r1_fp64_inst_ratio.txt).
-OPS = {  # case -> (inviscid ops per cell-stage, whole-step ops per cell)
-    "tgv": (4274, 14333),
+OPS = {  # case -> (inviscid face ops per cell-stage, whole-step ops per cell)
+    # counted on the reference's own code (tools/opcount/count_ref.cpp ->
+    # profiles/r2_opcount_ref2d.json): TGV 2D at 256^2, H2/O2 at 512^2
+    "tgv": (4269.3, 14064.3),
     "tgv3d": (None, 25800),
-    "h2o2": (7515, 29738),      # inviscid: 4274 x 1.758 (4-species faces / gamma-gas
-                                # faces FP64 instructions per cell-stage, ncu, 512^2)
-    "jet3d": (None, None),      # 4 species, 3D, WENO3Z componentwise: not counted yet
+    "h2o2": (7904.9, 28111.7),
+    "jet3d": (None, None),      # 4 species, 3D, WENO3Z componentwise: not counted
 }
 INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
 INVISCID_OPS_PER_CELL_STAGE = 4274
 TRAFFIC = {("tgv3d", 256): (1.789594 + 1.821264 + 2.173752 + 0.652562 + 0.656228 + 0.661791) * 1e9}
+TRAFFIC_SOURCE = {("tgv3d", 256): "ncu --set full capture of the three k_faces3d launches of one "
+                                   "stage at 256^3 (profiles/r1_ncu_faces3d_256.txt), not this run"}
+OPS_SOURCE = {
+    "tgv": "reference's own code, counted-double run at 256^2 (profiles/r2_opcount_ref2d.json)",
+    "tgv3d": "2D reference count x measured 3D/2D FP64 instruction ratio (r1)",
+    "h2o2": "reference's own code, counted-double run at 512^2 (profiles/r2_opcount_ref2d.json)",
+}
 STEP_OPS_PER_CELL = 14333
 BYTES_PER_CELL_STEP = lambda nc: 8 * (8 * nc + 6)  # noqa: E731  SURVEY §8d B_alg
 
@@ -377,6 +385,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cases", action="store_true",
+                    help="tgv3d only: skip the H2/O2 512^2 case of the headline metric")
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the NCCL slab path even with one rank (plumbing check)")
     args = ap.parse_args()
@@ -399,15 +409,74 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
-    from paper_2202_02319_b200 import Simulation, native
     if args.case == "ensemble":
         run_ensemble(args, rank, world, local, dist)
         return
 
     slabs = world > 1 or args.force_slabs
     case, workload = make_case(args, world)
+    peaks = load_peaks()
+    with ClockSampler(local) as clk:
+        res = measure_case(args, case, workload, rank, world, local, dist, slabs, peaks)
+        cases = {}
+        if args.case == "tgv3d" and not args.no_cases:
+            # the headline metric names TGV 256^3 AND the H2/O2 flame: configs[2]
+            # 512^2 per GPU (y-slabs under torchrun), its own value and roofline
+            sub = argparse.Namespace(**vars(args))
+            sub.case, sub.n = "h2o2", 512
+            c2, w2 = make_case(sub, world)
+            cases["h2o2_512"] = measure_case(sub, c2, w2, rank, world, local, dist, slabs, peaks)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            rate, k, el = cpu_reference_rate(512, args.cpu_seconds, threads, args.case)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": (f"512x512 {'2D analogue (no 3D reference path)' if args.case == 'tgv3d' else 'sub-problem'}"
+                              f" of the same workload, {k} RK3 steps in {el:.1f} s, unmodified "
+                              f"reference via oracle/_ref, {threads} threads")}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic initial condition)",
+            "config": res["config"],
+            "e2e": res["e2e"],
+            "gpu_launches": res["gpu_launches"] + sum(c["gpu_launches"] for c in cases.values()),
+            "roofline": res["roofline"],
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        if cases:
+            out["cases"] = cases
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def load_peaks():
+    """MEASURED_PEAKS.json (driver-written); else B200_PROFILING.md's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "hbm_source": "of measured (MEASURED_PEAKS.json)"}
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "hbm_source": "of fallback (B200_PROFILING.md)"}
+
+
+def measure_case(args, case, workload, rank, world, local, dist, slabs, peaks):
+    """One workload: K timed steps resident in HBM (CUDA events on the
+    library's stream, max over ranks), the e2e pass through the C ABI with
+    pinned host buffers, and the roofline of the dominant kernel class."""
+    import torch
+    from paper_2202_02319_b200 import Simulation, native
     case.cfg.device = local
-    if slabs:  # one y-slab per rank, halo rows over NCCL
+    if slabs:  # one slab per rank (2D: y rows, 3D: z planes), halo over NCCL (SURVEY §8e)
         case.cfg.slab_count, case.cfg.slab_rank = world, rank
     sim = Simulation(case.cfg)
     if slabs:
@@ -432,16 +501,15 @@ def main():
     sim.profile_enable(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        sim.rk3_steps(case.dt, args.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    sim.rk3_steps(case.dt, args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     ms = ev0.elapsed_time(ev1)
     prof = sim.profile_read()
     sim.profile_enable(False)
@@ -480,28 +548,31 @@ def main():
     peak = ctypes.c_double()
     native.api()["probe_fp64_peak"](local, ctypes.byref(peak))
     total_prof = sum(v[0] for v in prof.values())
-    dom = max(prof, key=lambda k: prof[k][0])
-    f_ms, f_n = prof["faces"]
+    f_ms = prof["faces"][0]
+    n_stage = prof["assemble"][1]  # one timed assemble per stage
     inv_ops, step_ops = OPS[args.case]
     if inv_ops is None and args.case == "tgv3d":
         inv_ops = INVISCID_OPS_PER_CELL_STAGE * INVISCID_3D_OVER_2D
-    # per timed faces region = one stage, all directions
+    # per stage (all face directions) = one "launch" of the faces class
     face_ops = cells * inv_ops if inv_ops else None
-    achieved = face_ops / (f_ms / f_n / 1e3) / 1e12 if (f_n and face_ops) else None
+    stage_ms = f_ms / n_stage if n_stage else None
+    achieved = face_ops / (stage_ms / 1e3) / 1e12 if (stage_ms and face_ops) else None
+    hbm = peaks["hbm_gbs"]
     roofline = {
         "bound": "fp64",
         "kernel": ("k_faces3d<x,y,z>" if args.case in ("tgv3d", "jet3d") else "k_faces3<x>+k_faces3<y>")
                   + " (inviscid face fluxes, one stage)",
         "ops_per_cell_stage": inv_ops,
+        "ops_source": OPS_SOURCE.get(args.case),
         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
         "frac": achieved / peak.value if achieved and peak.value else None,
-        # dram read+write of the three k_faces3d launches of one stage, one
-        # ncu --set full capture at 256^3 (profiles/r1_ncu_faces3d_256.txt);
-        # algorithmic: 13 fields read + 5 face planes written per direction
+        # dram read+write of the face kernels of one stage from an ncu --set
+        # full capture (not measured in this run; see traffic_source)
         "traffic": TRAFFIC.get((args.case, args.n)),
         "traffic_unit": "bytes per faces region (one stage)",
+        "traffic_source": TRAFFIC_SOURCE.get((args.case, args.n)),
         "traffic_algorithmic": (3 * (13 + 5) * cells * 8) if args.case == "tgv3d" else None,
-        "ops_per_launch": face_ops, "avg_launch_ms": f_ms / f_n if f_n else None,
+        "ops_per_launch": face_ops, "avg_launch_ms": stage_ms,
         "share_of_step": f_ms / total_prof if total_prof else None,
         "peak_source": "live DFMA-chain microbenchmark (ign_probe_fp64_peak), 2 flop/FMA",
         # bitwise parity forbids contracting the reference's a*b+c into FMAs
@@ -516,49 +587,31 @@ def main():
             "fp64_frac": (value / world * step_ops / 1e12 / peak.value
                           if step_ops and peak.value else None),
             "hbm_gbs": value / world * BYTES_PER_CELL_STEP(nc) / 1e9,
-            "hbm_frac": value / world * BYTES_PER_CELL_STEP(nc) / 1e9 / 6451.8,
+            "hbm_peak_gbs": hbm,
+            "hbm_frac": value / world * BYTES_PER_CELL_STEP(nc) / 1e9 / hbm,
+            "hbm_peak_source": peaks["hbm_source"],
         },
         "kernel_ms": {k: round(v[0], 3) for k, v in prof.items() if v[1]},
         "kernel_launches": {k: v[1] for k, v in prof.items() if v[1]},
     }
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            threads = os.cpu_count() or 1
-            rate, k, el = cpu_reference_rate(512, args.cpu_seconds, threads, args.case)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": (f"512x512 {'2D analogue (no 3D reference path)' if args.case == 'tgv3d' else 'sub-problem'}"
-                              f" of the same workload, {k} RK3 steps in {el:.1f} s, unmodified "
-                              f"reference via oracle/_ref, {threads} threads")}
-        except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
-
-    if rank == 0:
-        out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (analytic TGV initial condition)",
-            "config": {"workload": workload, "global_batch": world * cells,
-                       "cells_per_gpu": cells,
-                       "parallelism": f"y-slabs x{world}, NCCL halo rows" if slabs else "single",
-                       "l2": f"state {nc} x {sim.plane * 8 / 1e6:.0f} MB per buffer >> 126 MB L2, "
-                             "no flush needed",
-                       "dt": case.dt},
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
-                    "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
-            "gpu_launches": launches,
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(out), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
-
+    res = {
+        "value": value, "ms_per_step": ms_max / args.steps, "gpu_launches": launches,
+        "config": {"workload": workload, "global_batch": world * cells,
+                   "cells_per_gpu": cells,
+                   "parallelism": (f"{'z' if sim.nz else 'y'}-slabs x{world}, NCCL halo "
+                                   "overlapped with interior" if slabs else "single"),
+                   "l2": (f"state {nc} x {sim.plane * 8 / 1e6:.0f} MB per buffer; "
+                          + ("> 126 MB L2, no flush needed" if sim.plane * 8 * nc > 126e6 else
+                             "every stage streams 3 state buffers + cache + face planes "
+                             f"({(3 * nc + 12 + 3 * nc) * sim.plane * 8 / 1e6:.0f} MB) > 126 MB "
+                             "L2, no flush needed")),
+                   "dt": case.dt},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
+                "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
+        "roofline": roofline,
+    }
+    sim.close()
+    return res
 
 if __name__ == "__main__":
     main()
