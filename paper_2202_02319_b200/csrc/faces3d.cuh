@@ -90,11 +90,14 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
     return (g + k) * 32 + lane;
 }
 
-#ifndef IGN_X_MINB
-#define IGN_X_MINB 1
+// Registers: a 5-warp CTA needs <= 128 per thread for 3 CTAs/SM (4 warps per
+// SM sub-partition: 4 x 32 x 128 = 16384, the sub-partition's file); at 130
+// the z kernel drops to 2 CTAs/SM and runs ~30% slower.  __maxnreg__ pins it.
+#ifndef IGN_F3_MINB
+#define IGN_F3_MINB 3
 #endif
 template <int NS, int DIR, bool TENO, bool CHAR>
-__global__ void __launch_bounds__(32 * (NS + 4), (NS == 1 && DIR == 0 && CHAR) ? IGN_X_MINB : 1)
+__global__ void __launch_bounds__(32 * (NS + 4), (NS == 1 && DIR == 2) ? IGN_F3_MINB : 1)
 k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
           int f_lo, int f_hi) {
     using Smem = FaceSmem3<NS, DIR, TENO, CHAR>;
