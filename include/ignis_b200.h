@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define IGN_ABI_VERSION 1
+#define IGN_ABI_VERSION 2
 #define IGN_MAX_SPECIES 8   /* thermo.hpp:16 kMaxSpecies */
 #define IGN_MAX_COMP 11     /* flux.hpp:14 kMaxComp */
 #define IGN_MAX_PIECES 4    /* polynomial ranges per species */
@@ -119,6 +119,14 @@ typedef struct {
     int32_t kernel;
     double energy, sigma_r, sigma_t, x0, y0, t0, edot_rate;
     double lobe_sep, width_up, width_down, amp_down, width_radial;
+    /* 3D extension (no reference path): zmode 0 = the reference's 2D kernel
+     * on every z plane (a line source along z; the z-extrusion check),
+     * 1 = a point kernel at (x0, y0, z0): Gaussian with r^2 over (x, y, z) and
+     * the 3D normalisation E / ((2 pi)^2 sigma_r^3 sigma_t), so E is the
+     * deposited energy; shaped with the radial factor over (y, z). */
+    double z0;
+    int32_t zmode;
+    int32_t _pad;
 } ign_laser;
 
 /* solver.hpp:29-35 IntegratorConfig */
@@ -165,6 +173,15 @@ typedef struct {
     int32_t periodic_z;
     int32_t _pad;
     double lz, center_z;
+    /* A hand-built ignis::Mesh (mesh.hpp:23-42): its padded node coordinates
+     * mesh.x, mesh.y ((nx+2g)(ny+2g) doubles each, field.hpp layout, GLOBAL
+     * rows for slabs), read during ign_create only.  NULL = build_uniform
+     * (mesh.hpp:48-77) [+ apply_skew].  lx, ly, center_* and the periodic
+     * flags stay the Mesh's own fields (inflow profiles and the laser use the
+     * computational coordinates xi, eta, as the reference does); the metrics are
+     * compute_metrics of these coordinates (metrics.hpp:73-118). */
+    const double* mesh_x;
+    const double* mesh_y;
 } ign_config;
 
 /* errors.hpp:29-35 StepFailure payload + message; k is the z plane of a 3D

@@ -130,6 +130,11 @@ EdgeSpec to_edge(const ign_edge& e) {
 Mesh make_mesh(const ign_config& c) {
     Mesh m = build_uniform(c.nx, c.ny, c.lx, c.ly, {c.center_x, c.center_y},
                            c.periodic_x != 0, c.periodic_y != 0, c.g);
+    if (c.mesh_x && c.mesh_y) {  // a hand-built Mesh: the caller's coordinates
+        std::memcpy(m.x.raw().data(), c.mesh_x, m.x.raw().size() * sizeof(double));
+        std::memcpy(m.y.raw().data(), c.mesh_y, m.y.raw().size() * sizeof(double));
+        return m;
+    }
     if (c.apply_skew) m = apply_skew(m, c.skew_beta);
     return m;
 }

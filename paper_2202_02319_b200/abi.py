@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-IGN_ABI_VERSION = 1
+IGN_ABI_VERSION = 2
 IGN_MAX_SPECIES = 8
 IGN_MAX_COMP = 11
 IGN_MAX_PIECES = 4
@@ -90,7 +90,8 @@ class Laser(C.Structure):
     _fields_ = [("present", C.c_int32), ("kernel", C.c_int32)] + \
                [(n, C.c_double) for n in
                 ("energy", "sigma_r", "sigma_t", "x0", "y0", "t0", "edot_rate",
-                 "lobe_sep", "width_up", "width_down", "amp_down", "width_radial")]
+                 "lobe_sep", "width_up", "width_down", "amp_down", "width_radial")] + \
+               [("z0", C.c_double), ("zmode", C.c_int32), ("_pad", C.c_int32)]
 
 
 class Integrator(C.Structure):
@@ -113,7 +114,8 @@ class Config(C.Structure):
                 ("integ", Integrator),
                 ("device", C.c_int32), ("slab_count", C.c_int32),
                 ("slab_rank", C.c_int32), ("nz", C.c_int32), ("periodic_z", C.c_int32),
-                ("_pad", C.c_int32), ("lz", C.c_double), ("center_z", C.c_double)]
+                ("_pad", C.c_int32), ("lz", C.c_double), ("center_z", C.c_double),
+                ("mesh_x", C.POINTER(C.c_double)), ("mesh_y", C.POINTER(C.c_double))]
 
 
 class Error(C.Structure):

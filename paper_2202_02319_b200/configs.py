@@ -527,7 +527,8 @@ def jet3d(nx: int = 512, ny: int = 256, nz: int = 32, *, scheme: str = "weno3z",
     into air coflow (5 m/s) through a 4 cm x 2 cm channel — left inflow, right
     outflow with LODI toward 1 atm, no-slip adiabatic walls at the y edges, z
     periodic with dz = dx — one-step H2/O2 chemistry, the shaped laser kernel
-    focused in the shear layer; WENO3Z componentwise.  Weak
+    focused in the shear layer as a 3D point kernel (ign_laser.zmode 1);
+    WENO3Z componentwise.  Weak
     scaling stacks z: 512 x 256 x 32 per GPU, 512 x 256 x 256 on 8 GPUs."""
     Lx, Ly = 0.04, 0.02
     dx = Lx / nx
@@ -565,6 +566,13 @@ def jet3d(nx: int = 512, ny: int = 256, nz: int = 32, *, scheme: str = "weno3z",
     la.kernel = abi.LASER_SHAPED
     la.energy, la.sigma_r, la.sigma_t = energy, 5e-4, 1e-6
     la.x0, la.y0, la.t0 = 0.01, d, 3e-6
+    # the shaped two-lobe kernel (laser.hpp:64-85) focused on the shear layer:
+    # a point kernel in 3D (ign_laser.zmode 1) with its radial factor over
+    # (y, z), ~2.5e5 J/m^3 deposited at the focus (about the gas's own e)
+    la.edot_rate = 1e11
+    la.lobe_sep, la.width_up, la.width_down = 1e-3, 1.2e-3, 5e-4
+    la.amp_down, la.width_radial = 0.7, 4e-4
+    la.zmode, la.z0 = 1, 0.0
 
     def ic(X, Y, Z):
         f = 0.5 * (np.tanh((Y + d) / 2e-4) - np.tanh((Y - d) / 2e-4))  # 1 in the jet

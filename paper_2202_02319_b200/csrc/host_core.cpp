@@ -72,6 +72,12 @@ void slab_rows(int ny_glob, int nranks, int rank, int& lo, int& count) {
 }
 
 void HMesh::coords(int i, int jg, double& X, double& Y) const {
+    if (gx) {  // the caller's Mesh (mesh.hpp:33-34)
+        const size_t k = size_t(jg + g) * (nx + 2 * g) + (i + g);
+        X = (*gx)[k];
+        Y = (*gy)[k];
+        return;
+    }
     const double xc = xi(i), yc = eta_glob(jg);  // build_uniform (mesh.hpp:70-75)
     if (!skew) {
         X = xc;
@@ -106,6 +112,12 @@ HMesh build_mesh(const ign_config& c, int nranks, int rank) {
     m.periodic_y = c.periodic_y != 0;
     m.skew = c.apply_skew != 0;
     m.beta = c.skew_beta;
+    if (c.mesh_x && c.mesh_y) {  // hand-built Mesh: its coordinates, no apply_skew
+        const size_t n = size_t(m.nx + 2 * m.g) * (m.ny_glob + 2 * m.g);
+        m.gx = std::make_shared<const std::vector<double>>(c.mesh_x, c.mesh_x + n);
+        m.gy = std::make_shared<const std::vector<double>>(c.mesh_y, c.mesh_y + n);
+        m.skew = false;
+    }
     if (m.skew) {
         // apply_skew (mesh.hpp:92-105) validation, over this slab's interior rows
         if (std::abs(m.lx - m.ly) > 1e-14 * m.lx || m.cx != 0.0 || m.cy != 0.0)
@@ -359,6 +371,9 @@ DLaser build_laser(const ign_laser& l) {
     d.amp_down = l.amp_down;
     d.width_radial = l.width_radial;
     d.pow2pi15 = std::pow(2.0 * M_PI, 1.5);
+    d.zmode = l.zmode;
+    d.z0 = l.z0;
+    d.pow2pi2 = (2.0 * M_PI) * (2.0 * M_PI);
     return d;
 }
 

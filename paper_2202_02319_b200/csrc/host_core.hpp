@@ -7,6 +7,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "ignis_b200.h"
@@ -57,6 +58,9 @@ struct HMesh {
     bool skew = false;
     double beta = 0.0;
     HField x, y;  // local padded box
+    // a hand-built mesh (ign_config.mesh_x/mesh_y): the GLOBAL padded
+    // coordinate arrays, which coords() then reads instead of the formulas
+    std::shared_ptr<const std::vector<double>> gx, gy;
     double dxi() const { return lx / nx; }
     double deta() const { return ly / ny_glob; }
     double xi(int i) const { return cx - 0.5 * lx + (i + 0.5) * dxi(); }

@@ -371,8 +371,9 @@ __device__ void lodi_dfx3(const KParams& P, int j, int kz, double* dF) {
 
 // ---------------------------------------------------------------- assemble + update
 // laser_power out of line: the common (laser-free) update stays small
-static __device__ __noinline__ double laser_cold(double x, double y, double t, const DLaser& p) {
-    return laser_power(x, y, t, p);
+static __device__ __noinline__ double laser_cold(double x, double y, double z, double t,
+                                                 const DLaser& p) {
+    return laser_power3(x, y, z, t, p);
 }
 
 // EDGE = false: every padded node except, when LODI is on, the right-edge
@@ -453,11 +454,14 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
 #pragma unroll
                 for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
             }
-            // laser_power (laser.hpp:88-91) of the node's (x, y): the
-            // reference's 2D kernel, uniform along z
+            // laser_power (laser.hpp:88-91) of the node's (x, y) — the
+            // reference's 2D kernel on every plane — or the 3D point kernel
+            // (laser_power3, zmode 1) at the node's z
             if (P.laser.on) {
                 const int q = (j + P.g) * P.sx + (i + P.g);
-                r[NS + 3] += laser_cold(ldg(P.xc + q), ldg(P.yc + q), t_stage, P.laser) * invJ;
+                const double z = P.zc0 + ((k + P.j0) + 0.5) * P.dz;
+                r[NS + 3] +=
+                    laser_cold(ldg(P.xc + q), ldg(P.yc + q), z, t_stage, P.laser) * invJ;
             }
             const unsigned long long cell =
                 ((unsigned long long)(k + P.j0) * P.ny + j) * P.nx + i;

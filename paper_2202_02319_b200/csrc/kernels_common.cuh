@@ -64,6 +64,7 @@ struct KParams {
     double T_wall[4];
     double sigma_out_right, p_target_right;
     double lx, ly, cx, cy;
+    double zc0, dz;  // 3D: z of global plane k = zc0 + (k + 0.5) dz (sim.py mesh_z)
     ReconParams rp;  // ct, eps and the TENO cutoff decision band
     int32_t chem_dt_limit, lodi;
     double chem_dt_factor;

@@ -363,6 +363,10 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     k.ly = cfg->ly;
     k.cx = cfg->center_x;
     k.cy = cfg->center_y;
+    if (cfg->nz > 0) {
+        k.zc0 = cfg->center_z - 0.5 * cfg->lz;
+        k.dz = cfg->lz / cfg->nz;  // nz is the GLOBAL plane count in the config
+    }
     k.rp = make_recon_params(cfg->scheme.teno_ct, cfg->scheme.eps);
     k.chem_dt_limit = cfg->integ.chem_dt_limit;
     k.chem_dt_factor = cfg->integ.chem_dt_factor;

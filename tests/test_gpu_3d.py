@@ -362,3 +362,58 @@ def test_3d_probes_match_2d_oracle_on_one_plane(oracle_api, cuda_device):
     (ta, ra), (tb, rb) = single.probe(0), grp.probe(0)
     assert np.array_equal(ta, tb) and np.array_equal(ra.view(np.uint64), rb.view(np.uint64))
     grp.close()
+
+
+# ----------------------------------------------------------------- 3D laser
+def _quiescent_laser_box(n, kernel, zmode):
+    case = configs.tgv3d(n, viscous=False)
+    la = case.cfg.laser
+    la.present, la.kernel, la.zmode = 1, kernel, zmode
+    la.energy, la.sigma_t, la.t0 = 3.0, 1e-3, 0.5
+    la.sigma_r = 2.0 * (2.0 * np.pi / n)  # 2 cells: the domain spans +-6 sigma_r
+    la.x0 = la.y0 = la.z0 = 0.0
+    la.edot_rate = 7.0
+    la.lobe_sep, la.width_up, la.width_down, la.amp_down = 0.5, 0.6, 0.25, 0.7
+    la.width_radial = 0.4
+    p0 = case.notes["p0"]
+
+    def ic(X, Y, Z):
+        one = np.ones_like(X)
+        z = np.zeros_like(X)
+        return one, z, z.copy(), z.copy(), p0 * one, [one]
+    sim = Simulation(case.cfg)
+    sim.set_initial_condition(ic)
+    sim.prepare_stage(1)
+    return case, sim
+
+
+def test_laser3d_point_kernel_deposits_E(cuda_device):
+    """zmode 1 Gaussian (laser_power3): at t0 the RHS of E integrates to
+    E / (sqrt(2 pi) sigma_t) over the box (the 3D normalisation), the
+    space-time integral of q_L being E (laser.hpp:53-61 with r^2 over x,y,z)."""
+    case, sim = _quiescent_laser_box(24, abi.LASER_GAUSSIAN, 1)
+    la = case.cfg.laser
+    rhs = sim.compute_rhs(la.t0, 1)
+    g = sim.g
+    dE = rhs[-1][g:-g, g:-g, g:-g]
+    want = la.energy / (np.sqrt(2.0 * np.pi) * la.sigma_t)
+    assert abs(dE.sum() - want) <= 1e-9 * want, (dE.sum(), want)
+    # symmetric about the focus in every direction (node-centred grid about 0)
+    assert np.allclose(dE, dE[::-1, :, :], rtol=1e-12, atol=1e-12 * dE.max())
+    assert np.allclose(dE, np.swapaxes(dE, 0, 2), rtol=1e-12, atol=1e-12 * dE.max())
+
+
+def test_laser3d_zmode0_is_the_2d_kernel_on_every_plane(cuda_device):
+    """zmode 0 (default): the reference's 2D kernel, z-uniform; shaped kernel
+    with zmode 1 decays in z about z0 with its radial width."""
+    case, sim = _quiescent_laser_box(16, abi.LASER_SHAPED, 0)
+    la = case.cfg.laser
+    g = sim.g
+    dE = sim.compute_rhs(la.t0, 1)[-1][g:-g, g:-g, g:-g]
+    assert dE.max() > 0.0
+    assert np.all(dE == dE[0][None])  # identical z planes
+    case1, sim1 = _quiescent_laser_box(16, abi.LASER_SHAPED, 1)
+    dE1 = sim1.compute_rhs(la.t0, 1)[-1][g:-g, g:-g, g:-g]
+    kz = np.argmax(dE1.max(axis=(1, 2)))
+    prof = dE1.max(axis=(1, 2))
+    assert prof[kz] > 10.0 * prof[0] and np.allclose(prof, prof[::-1], rtol=1e-12)
