@@ -26,3 +26,17 @@ g++ -std=c++20 -O2 -ffp-contract=off -DNDEBUG -pthread -fPIC -shared \
     "$here/ref_driver.cpp" -o "$out/libignis_ref.so.tmp"
 mv "$out/libignis_ref.so.tmp" "$out/libignis_ref.so"
 echo "built $out/libignis_ref.so"
+# Test programs that need the reference headers, built here so they travel to
+# the GPU box (where /root/reference does not exist): the reference-typed
+# drop-in checked against ignis::Simulation, and the POD facade example.
+lib="$repo/paper_2202_02319_b200/_lib"
+if [ -f "$lib/libignis_b200.so" ]; then
+    g++ -std=c++20 -O2 -ffp-contract=off -DNDEBUG -pthread \
+        -I"$ref_inc" -I"$repo/include" -DREPO_DATA_DIR="\"$repo/data\"" \
+        "$repo/tests/cpp/drop_in_parity.cpp" -o "$out/drop_in_parity" \
+        -L"$lib" -lignis_b200 -Wl,-rpath,'$ORIGIN/../../paper_2202_02319_b200/_lib'
+    g++ -std=c++17 -O2 -I"$repo/include" "$repo/tests/cpp/facade_example.cpp" \
+        -o "$out/facade_example" -L"$lib" -lignis_b200 \
+        -Wl,-rpath,'$ORIGIN/../../paper_2202_02319_b200/_lib'
+    echo "built $out/drop_in_parity $out/facade_example"
+fi

@@ -127,3 +127,24 @@ def test_cpp_facade_example_compiles_and_links(tmp_path):
                     f"-L{lib}", "-lignis_b200", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode in (0, 2), r.stdout + r.stderr
+
+
+def test_drop_in_compiles_against_reference_headers(tmp_path):
+    """include/ignis_b200/drop_in.hpp: the reference-typed drop-in for
+    ignis::Simulation builds against the UNMODIFIED reference headers and links
+    the library (tests/cpp/drop_in_parity.cpp; run on the GPU by
+    tests/test_gpu_boundary.py)."""
+    import subprocess
+    from tests.conftest import REFERENCE_INCLUDE, has_reference_sources
+    if not has_reference_sources():
+        pytest.skip("reference headers absent")
+    root = os.path.dirname(HEADER)
+    lib = os.path.dirname(native.LIB)
+    exe = str(tmp_path / "drop_in_parity")
+    repo = os.path.dirname(root)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-pthread",
+                    f"-I{REFERENCE_INCLUDE}", f"-I{root}",
+                    f'-DREPO_DATA_DIR="{repo}/data"',
+                    os.path.join(repo, "tests", "cpp", "drop_in_parity.cpp"),
+                    f"-L{lib}", "-lignis_b200", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    assert os.path.exists(exe)

@@ -397,7 +397,8 @@ def test_laser3d_point_kernel_deposits_E(cuda_device):
     g = sim.g
     dE = rhs[-1][g:-g, g:-g, g:-g]
     want = la.energy / (np.sqrt(2.0 * np.pi) * la.sigma_t)
-    assert abs(dE.sum() - want) <= 1e-9 * want, (dE.sum(), want)
+    # the +-6 sigma_r box truncates ~2 Phi(-6) of the Gaussian per axis (~6e-9)
+    assert abs(dE.sum() - want) <= 1e-7 * want, (dE.sum(), want)
     # symmetric about the focus in every direction (node-centred grid about 0)
     assert np.allclose(dE, dE[::-1, :, :], rtol=1e-12, atol=1e-12 * dE.max())
     assert np.allclose(dE, np.swapaxes(dE, 0, 2), rtol=1e-12, atol=1e-12 * dE.max())
