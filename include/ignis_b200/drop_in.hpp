@@ -229,16 +229,23 @@ private:
         ensure();
         push();
         const int st = f();
+        ign_error e{};
+        if (st != IGN_OK && ctx_) ign_last_error(ctx_, &e);  // before pull() clears it
         if (st == IGN_OK || st == IGN_STEP_FAILURE) {  // a StepFailure restored U0: mirror it
             if (mirror && mutates) pull();
         }
-        check(st);
+        raise(st, e);
     }
 
     void check(int st) {
         if (st == IGN_OK) return;
         ign_error e{};
         if (ctx_) ign_last_error(ctx_, &e);
+        raise(st, e);
+    }
+
+    static void raise(int st, const ign_error& e) {
+        if (st == IGN_OK) return;
         const std::string m = e.msg;
         switch (st) {
         case IGN_CONFIG_ERROR: throw ignis::ConfigError(m);

@@ -170,8 +170,14 @@ int main() {
             ref.prepare_stage(1);
             gpu.prepare_stage(1);
             int sa = -1, sb = -2, ia = 0, ib = 1, ja = 0, jb = 1;
-            try { ref.rk3_step(50.0); } catch (const StepFailure& e) { sa = e.stage; ia = e.i; ja = e.j; }
-            try { gpu.rk3_step(50.0); } catch (const StepFailure& e) { sb = e.stage; ib = e.i; jb = e.j; }
+            std::string wa, wb;
+            try { ref.rk3_step(50.0); } catch (const StepFailure& e) { sa = e.stage; ia = e.i; ja = e.j; wa = e.what(); }
+            catch (const std::exception& e) { wa = std::string("other: ") + e.what(); }
+            try { gpu.rk3_step(50.0); } catch (const StepFailure& e) { sb = e.stage; ib = e.i; jb = e.j; wb = e.what(); }
+            catch (const std::exception& e) { wb = std::string("other: ") + e.what(); }
+            if (!(sa == sb && ia == ib && ja == jb && sa > 0))
+                std::printf("reference: %d (%d,%d) %s\nb200: %d (%d,%d) %s\n", sa, ia, ja, wa.c_str(),
+                            sb, ib, jb, wb.c_str());
             CHECK(sa == sb && ia == ib && ja == jb && sa > 0, "StepFailure payload");
             CHECK(bitwise(gpu.Ut, ref.Ut), "StepFailure restores U0");
         }
