@@ -56,3 +56,23 @@ def simulation(cfg: abi.Config, partitions: int = 1) -> Simulation:
 
 def set_partitions(sim: Simulation, n: int):
     lib().ignref_set_partitions(sim.handle, n)
+
+
+def inviscid_rhs3(cfg: abi.Config, Ut, prim):
+    """The 3D extension's inviscid RHS from oracle/ref3d_faces.hpp (the
+    reference's per-face algorithm restated with the z terms) for a padded 3D
+    state and the product's primitive cache; interior of the returned planes
+    written, ghosts 0."""
+    import numpy as np
+    f = lib().ignref3d_inviscid_rhs
+    f.argtypes = [C.POINTER(abi.Config), C.c_void_p, C.c_void_p, C.c_void_p,
+                  C.POINTER(abi.Error)]
+    f.restype = C.c_int
+    Ut = np.ascontiguousarray(Ut, dtype=np.float64)
+    prim = np.ascontiguousarray(prim, dtype=np.float64)
+    out = np.zeros_like(Ut)
+    err = abi.Error()
+    st = f(C.byref(cfg), Ut.ctypes.data, prim.ctypes.data, out.ctypes.data, C.byref(err))
+    if st != abi.IGN_OK:
+        raise RuntimeError(f"ref3d: status {st}: {err.msg.decode()}")
+    return out

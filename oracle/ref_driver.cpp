@@ -20,6 +20,8 @@
 #include "ignis/solver.hpp"
 #include "ignis_b200.h"
 
+#include "ref3d_faces.hpp"
+
 using namespace ignis;
 
 struct ref_ctx {
@@ -420,6 +422,26 @@ int ignref_last_clip(const ref_ctx* ctx, double* clip) {
 int ignref_set_diagnostics(ref_ctx* ctx, int mode) {
     (void)ctx;
     return mode == IGN_DIAG_DEVICE || mode == IGN_DIAG_REFERENCE ? IGN_OK : IGN_USAGE_ERROR;
+}
+
+// 3D extension checker (ref3d_faces.hpp): the inviscid RHS of a padded 3D
+// state Ut given the product's primitive cache (rho, u, v, w, p, T, c, Y_s);
+// rhs = nc padded planes, interior written.  Returns IGN_OK or the error.
+int ignref3d_inviscid_rhs(const ign_config* cfg, const double* Ut, const double* prim,
+                          double* rhs, ign_error* err) {
+    return guarded(err, [&] {
+        if (cfg->nz <= 0) throw UsageError("ref3d: nz must be > 0");
+        const Mesh mesh = make_mesh(*cfg);
+        const SchemeConfig sc = to_scheme(cfg->scheme);
+        const MetricField met = compute_metrics(mesh, inviscid_mode(*cfg, sc), cfg->skew_beta);
+        const ref3d::Met3 M = ref3d::extrude(met, cfg->lz / cfg->nz);
+        const MixtureModel mix = to_mix(cfg->mix);
+        ref3d::Grid G{cfg->nx, cfg->ny, cfg->nz, cfg->g, mix.ns(), 0, 0, 0};
+        G.sx = cfg->nx + 2 * cfg->g;
+        G.sxy = G.sx * (cfg->ny + 2 * cfg->g);
+        G.plane = G.sxy * (cfg->nz + 2 * cfg->g);
+        ref3d::inviscid_rhs(G, M, mix, sc, Ut, prim, rhs);
+    });
 }
 
 int ignref_host_metrics(const ign_config* cfg, int which, double* out,
