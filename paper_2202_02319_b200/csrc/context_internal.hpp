@@ -17,6 +17,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool
+
 #include "host_core.hpp"
 #include "ignis_b200.h"
 #include "io.hpp"
@@ -174,7 +176,20 @@ template <class F> int guarded(ign_context* ctx, F&& f) {
     });
 }
 
+// NVTX range over a host scope (stage, kernel class, halo leg): visible in
+// nsys / ncu --nvtx timelines, free when no tool is attached
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 template <class F> int timed(ign_context* ctx, int cat, F&& f) {
+    static const char* const kNames[IGN_PROF_CLASSES] = {"ghost fill", "primitives", "faces",
+                                                         "viscous", "assemble", "stable_dt",
+                                                         "other", "other"};
+    NvtxRange r(kNames[cat]);
     if (!ctx->prof_on) return f();
     cudaEvent_t a = prof_event(ctx), b = prof_event(ctx);
     cuda_check(cudaEventRecord(a, ctx->stream), "event");

@@ -307,6 +307,7 @@ void t_prepare(const Team& T, int buf, int stage, int step) {
     ign_context* L = T.lead();
     ensure_halo_stream(L);
     cudaStream_t hs = L->halo_stream;
+    NvtxRange nv("halo leg");
     cuda_check(cudaEventRecord(L->ev_ready, T.stream()), "event");
     cuda_check(cudaStreamWaitEvent(hs, L->ev_ready, 0), "halo wait");
     t_exchange(T, buf, hs);
@@ -369,18 +370,25 @@ void t_step(const Team& T, int a, double time, double dt, int step, bool post_pr
         k_clip_reset<<<1, 3, 0, x->stream>>>(x->err, x->red, slot);
         ++x->launches;
     }
-    // Stage 1: U <- U0 + dt L(U0)   (ghosts/cache already fresh)
-    t_fluxes(T, a, 1, step);
-    t_assemble(T, 1, a, a, b, dt, 0.0, time, 1, step, slot + 0);
-    t_prepare(T, b, 2, step);
-    // Stage 2: U <- U0 + 1/4 [(U1 - U0) + dt L(U1)]
-    t_fluxes(T, b, 2, step);
-    t_assemble(T, 2, a, b, c, dt, 0.25, time + dt, 2, step, slot + 1);
-    t_prepare(T, c, 3, step);
-    // Stage 3: U <- U0 + 2/3 [(U2 - U0) + dt L(U2)]
-    t_fluxes(T, c, 3, step);
-    t_assemble(T, 2, a, c, b, dt, 2.0 / 3.0, time + 0.5 * dt, 3, step, slot + 2);
-    if (post_prepare) t_prepare(T, b, 4, step);
+    NvtxRange nv("rk3_step");
+    {  // Stage 1: U <- U0 + dt L(U0)   (ghosts/cache already fresh)
+        NvtxRange s("stage 1");
+        t_fluxes(T, a, 1, step);
+        t_assemble(T, 1, a, a, b, dt, 0.0, time, 1, step, slot + 0);
+        t_prepare(T, b, 2, step);
+    }
+    {  // Stage 2: U <- U0 + 1/4 [(U1 - U0) + dt L(U1)]
+        NvtxRange s("stage 2");
+        t_fluxes(T, b, 2, step);
+        t_assemble(T, 2, a, b, c, dt, 0.25, time + dt, 2, step, slot + 1);
+        t_prepare(T, c, 3, step);
+    }
+    {  // Stage 3: U <- U0 + 2/3 [(U2 - U0) + dt L(U2)]
+        NvtxRange s("stage 3");
+        t_fluxes(T, c, 3, step);
+        t_assemble(T, 2, a, c, b, dt, 2.0 / 3.0, time + 0.5 * dt, 3, step, slot + 2);
+        if (post_prepare) t_prepare(T, b, 4, step);
+    }
 }
 
 // Clip slots of a chunk's steps over all slabs (MAX: the reference's clip is a max).
