@@ -67,18 +67,20 @@ OPS = {  # case -> (inviscid face ops per cell-stage, whole-step ops per cell)
     # counted on the reference's own code (tools/opcount/count_ref.cpp ->
     # profiles/r2_opcount_ref2d.json): TGV 2D at 256^2, H2/O2 at 512^2
     "tgv": (4269.3, 14064.3),
-    "tgv3d": (None, 25800),
+    "tgv3d": (7626.3, 25800),    # faces: tools/opcount/count_3d.cpp at 256^3 on the
+                                 # 3D restatement (profiles/r2_opcount_ref3d.json);
+                                 # whole step: SURVEY §8d's derived figure
     "h2o2": (7904.9, 28111.7),
     "jet3d": (None, None),      # 4 species, 3D, WENO3Z componentwise: not counted
 }
-INVISCID_3D_OVER_2D = 1.8987  # profiles/r1_fp64_inst_ratio.txt
-INVISCID_OPS_PER_CELL_STAGE = 4274
 TRAFFIC = {("tgv3d", 256): (1.789594 + 1.821264 + 2.173752 + 0.652562 + 0.656228 + 0.661791) * 1e9}
 TRAFFIC_SOURCE = {("tgv3d", 256): "ncu --set full capture of the three k_faces3d launches of one "
                                    "stage at 256^3 (profiles/r1_ncu_faces3d_256.txt), not this run"}
 OPS_SOURCE = {
     "tgv": "reference's own code, counted-double run at 256^2 (profiles/r2_opcount_ref2d.json)",
-    "tgv3d": "2D reference count x measured 3D/2D FP64 instruction ratio (r1)",
+    "tgv3d": ("counted-double run of oracle/ref3d_faces.hpp (the reference's per-face "
+              "algorithm with z terms, bitwise equal to the kernels) at 256^3 "
+              "(profiles/r2_opcount_ref3d.json)"),
     "h2o2": "reference's own code, counted-double run at 512^2 (profiles/r2_opcount_ref2d.json)",
 }
 STEP_OPS_PER_CELL = 14333
@@ -551,8 +553,6 @@ def measure_case(args, case, workload, rank, world, local, dist, slabs, peaks):
     f_ms = prof["faces"][0]
     n_stage = prof["assemble"][1]  # one timed assemble per stage
     inv_ops, step_ops = OPS[args.case]
-    if inv_ops is None and args.case == "tgv3d":
-        inv_ops = INVISCID_OPS_PER_CELL_STAGE * INVISCID_3D_OVER_2D
     # per stage (all face directions) = one "launch" of the faces class
     face_ops = cells * inv_ops if inv_ops else None
     stage_ms = f_ms / n_stage if n_stage else None
