@@ -238,7 +238,8 @@ class SampleResult:
     outdir: str = ""
 
 
-BatchRunner = Callable[[List[RunSpec]], List[Tuple[bool, Optional[float]]]]
+# per spec: (ignited, t_ign), or the member's exception (its failure is its result)
+BatchRunner = Callable[[List[RunSpec]], List]
 
 
 def run_batch(specs: Sequence[RunSpec], pools: PoolConfig, hf_runner: BatchRunner,
@@ -267,8 +268,11 @@ def run_batch(specs: Sequence[RunSpec], pools: PoolConfig, hf_runner: BatchRunne
             group = hf[k:k + pools.hf_workers]
             t0 = time.perf_counter()
             try:
-                outs = hf_runner(group)
-                errs = [""] * len(group)
+                raw = hf_runner(group)
+                # a batch runner reports a member's own failure as an exception
+                # instance in its slot
+                outs = [(None, None) if isinstance(o, Exception) else o for o in raw]
+                errs = [str(o) if isinstance(o, Exception) else "" for o in raw]
             except Exception as exc:  # noqa: BLE001 — recorded per sample
                 outs = [(None, None)] * len(group)
                 errs = [str(exc)] * len(group)
@@ -381,30 +385,41 @@ class CounterflowRunner:
             nsteps = int(math.ceil(self.t_end / dt))
             times = [[] for _ in cases]
             vals = [[] for _ in cases]
-            live = [True] * len(cases)
+            errs: List[Optional[Exception]] = [None] * len(cases)
             done = 0
             while done < nsteps:
+                live = [q for q in range(len(cases)) if errs[q] is None]
+                if not live:
+                    break
                 k = min(self.trace_every, nsteps - done)
-                st = ens.rk3_steps(dt, k)
+                try:
+                    st = ens.rk3_steps(dt, k, only=live)
+                except Exception:  # noqa: BLE001 — every live member failed
+                    st = [1 if q in live else 0 for q in range(len(cases))]
                 done += k
-                for q, m in enumerate(ens.members):
-                    if st[q] != 0:
-                        live[q] = False
-                    if live[q]:
-                        times[q].append(m.time)
-                        vals[q].append(m.product_mole_fraction())
-            out = []
+                for q in live:
+                    if st[q] != 0:  # a failed member stops; its error is its result
+                        errs[q] = ens.error(q) or UsageError(f"member {q} failed")
+                        continue
+                    m = ens.members[q]
+                    times[q].append(m.time)
+                    vals[q].append(m.product_mole_fraction())
+            out: List = []
             for q in range(len(cases)):
-                if not live[q]:
-                    raise ens.error(q) or UsageError(f"member {q} failed")
-                out.append(detect_ignition(times[q], vals[q], self.t0, self.window, self.y_max,
-                                           self.theta))
+                if errs[q] is not None:
+                    out.append(errs[q])
+                else:
+                    out.append(detect_ignition(times[q], vals[q], self.t0, self.window,
+                                               self.y_max, self.theta))
             return out
         finally:
             ens.close()
 
     def __call__(self, energy: float) -> Tuple[bool, Optional[float]]:
-        return self.batch([energy])[0]
+        r = self.batch([energy])[0]
+        if isinstance(r, Exception):
+            raise r
+        return r
 
     def hf_runner(self) -> BatchRunner:
         return lambda specs: self.batch([s.energy for s in specs])

@@ -445,10 +445,24 @@ class Ensemble:
     def __len__(self):
         return len(self.members)
 
-    def rk3_steps(self, dt, n: int):
+    def rk3_steps(self, dt, n: int, only=None):
         """n steps per member with dt (scalar or per member).  Returns the
         per-member status list; raises the first failure's exception only when
-        every member failed (a failed member stops, the others continue)."""
+        every member failed (a failed member stops, the others continue).
+        ``only``: indices of the members to advance (the others are left as
+        they are; their status reads 0)."""
+        idx = list(range(len(self.members))) if only is None else list(only)
+        if not idx:
+            return [0] * len(self.members)
+        if only is not None:
+            full = [0] * len(self.members)
+            sub = Ensemble.__new__(Ensemble)
+            sub._api, sub.members = self._api, [self.members[k] for k in idx]
+            dts = np.broadcast_to(np.asarray(dt, dtype=np.float64), (len(self.members),))
+            st = sub.rk3_steps([dts[k] for k in idx], n) if len(idx) else []
+            for k, v in zip(idx, st):
+                full[k] = v
+            return full
         M = len(self.members)
         dts = np.ascontiguousarray(np.broadcast_to(np.asarray(dt, dtype=np.float64), (M,)))
         hs = (C.c_void_p * M)(*[m.handle.value for m in self.members])
