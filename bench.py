@@ -196,7 +196,7 @@ def make_case(args, nslabs: int = 1):
                 f"TGV 3D {n}^3 per GPU (BASELINE configs[1]), viscous Re 1600, Ma 0.1, TENO6 "
                 "characteristic, gamma-gas, fixed dt; 3D extension (the reference is 2D-only)")
     if args.case == "jet3d":
-        nz = args.n // 16
+        nz = args.nz if args.nz else args.n // 16
         return (configs.jet3d(args.n, args.n // 2, nz * nslabs),
                 f"3D H2 jet (configs[3] form): {args.n}x{args.n // 2}x{nz} per GPU, inflow / "
                 "LODI outflow / walls, one-step chemistry, shaped laser, WENO3Z comp; z-slabs")
@@ -384,6 +384,9 @@ def main():
     ap.add_argument("--case", default="tgv3d",
                     choices=["tgv3d", "tgv", "h2o2", "ensemble", "jet3d"])
     ap.add_argument("--members", type=int, default=8, help="ensemble members per GPU")
+    ap.add_argument("--nz", type=int, default=None,
+                    help="jet3d: z planes per GPU (default size/16; 256 = the full "
+                         "512x256x256 configs[3] domain on one GPU)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
