@@ -85,7 +85,7 @@ __device__ __forceinline__ int tile_node(int g, int lane, int k, int L0) {
     return (g + k) * 32 + lane;
 }
 
-template <int NS, int DIR, bool TENO, bool CHAR>
+template <int NS, int DIR, bool TENO, bool CHAR, int TM>
 #ifndef IGN_FACES_MINB
 #define IGN_FACES_MINB 4
 #endif
@@ -212,11 +212,11 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 Yr[s] = ldg(PY(P, s) + ir);
             }
             double Ta, ua, va;
-            roe_average<NS>(ldg(PRHO(P) + il), Yl, ldg(PT(P) + il), ldg(PU(P) + il),
+            roe_average<NS, TM>(ldg(PRHO(P) + il), Yl, ldg(PT(P) + il), ldg(PU(P) + il),
                             ldg(PV(P) + il), ldg(PRHO(P) + ir), Yr, ldg(PT(P) + ir),
                             ldg(PU(P) + ir), ldg(PV(P) + ir), P.mix, Ya, Ta, ua, va);
             Eigen<NS> es;
-            const int est = eigen_at_state<NS>(Ya, Ta, ua, va, m1f, m2f, P.mix, es);
+            const int est = eigen_at_state<NS, TM>(Ya, Ta, ua, va, m1f, m2f, P.mix, es);
             if (est) {
                 report(P.err, stage, phase, err_index(my_f, my_col), 1 + est, step);
                 bad = 1;
@@ -466,12 +466,12 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     }
 }
 
-template <int NS, int DIR, bool TENO, bool CHAR>
-inline int launch_faces3(const KParams& P, const double* Ut, int stage, int step,
+template <int NS, int DIR, bool TENO, bool CHAR, int TM>
+inline int launch_faces3_tm(const KParams& P, const double* Ut, int stage, int step,
                           cudaStream_t s, int f_lo = 0, int f_hi = -1) {
     constexpr int NC = NS + 3;
     const size_t smem = sizeof(FaceSmem<NS, DIR, TENO, CHAR>);
-    auto kern = k_faces3<NS, DIR, TENO, CHAR>;
+    auto kern = k_faces3<NS, DIR, TENO, CHAR, TM>;
     static std::atomic<unsigned long long> configured{0};  // per instantiation, per device
     configure_kernel(kern, smem, NC, configured, "k_faces3");
     const int NF = 32 * NC;
@@ -486,6 +486,19 @@ inline int launch_faces3(const KParams& P, const double* Ut, int stage, int step
         grid = dim3((P.nx + 31) / 32, (f_hi - f_lo + NC - 1) / NC);
     kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step, f_lo, f_hi);
     return 1;
+}
+
+// thermo mode of the Roe/eigen thermo (physics.cuh sp_h_R): a calorically
+// perfect single-species mixture (the gamma-gas) takes the instantiation with
+// only those forms compiled in
+template <int NS, int DIR, bool TENO, bool CHAR>
+inline int launch_faces3(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
+                          int f_lo = 0, int f_hi = -1) {
+    if constexpr (NS == 1) {
+        if (P.mix.all_simple)
+            return launch_faces3_tm<NS, DIR, TENO, CHAR, 1>(P, Ut, stage, step, s, f_lo, f_hi);
+    }
+    return launch_faces3_tm<NS, DIR, TENO, CHAR, 0>(P, Ut, stage, step, s, f_lo, f_hi);
 }
 
 }  // namespace ign

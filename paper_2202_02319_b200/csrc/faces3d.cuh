@@ -96,7 +96,7 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
 #ifndef IGN_F3_MINB
 #define IGN_F3_MINB 3
 #endif
-template <int NS, int DIR, bool TENO, bool CHAR>
+template <int NS, int DIR, bool TENO, bool CHAR, int TM>
 __global__ void __launch_bounds__(32 * (NS + 4), (NS == 1 && DIR == 2) ? IGN_F3_MINB : 1)
 k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
           int f_lo, int f_hi) {
@@ -263,10 +263,10 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         if (my_active) {
             double Ya[NS];
             double Ta, ua, va, wa;
-            roe_average3<NS>(pl[0], Yl, pl[1], pl[2], pl[3], pl[4], pr[0], Yr, pr[1], pr[2],
+            roe_average3<NS, TM>(pl[0], Yl, pl[1], pl[2], pl[3], pl[4], pr[0], Yr, pr[1], pr[2],
                              pr[3], pr[4], P.mix, Ya, Ta, ua, va, wa);
             Eigen3<NS> es;
-            const int est = eigen_at_state3<NS, DIR == 2 ? 2 : 0>(Ya, Ta, ua, va, wa, m1f, m2f,
+            const int est = eigen_at_state3<NS, DIR == 2 ? 2 : 0, TM>(Ya, Ta, ua, va, wa, m1f, m2f,
                                                                   P.mix, es);
             if (est) {
                 report(P.err, stage, phase, err_index(my_f, my_col), 1 + est, step);
@@ -534,12 +534,12 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     }
 }
 
-template <int NS, int DIR, bool TENO, bool CHAR>
-inline int launch_faces3d(const KParams& P, const double* Ut, int stage, int step,
+template <int NS, int DIR, bool TENO, bool CHAR, int TM>
+inline int launch_faces3d_tm(const KParams& P, const double* Ut, int stage, int step,
                            cudaStream_t s, int f_lo = 0, int f_hi = -1) {
     constexpr int NC = NS + 4;
     const size_t smem = sizeof(FaceSmem3<NS, DIR, TENO, CHAR>);
-    auto kern = k_faces3d<NS, DIR, TENO, CHAR>;
+    auto kern = k_faces3d<NS, DIR, TENO, CHAR, TM>;
     static std::atomic<unsigned long long> configured{0};  // per instantiation, per device
     configure_kernel(kern, smem, NC, configured, "k_faces3d");
     const int NF = 32 * NC;
@@ -556,6 +556,19 @@ inline int launch_faces3d(const KParams& P, const double* Ut, int stage, int ste
     else grid = dim3((P.nx + 31) / 32, P.ny, (f_hi - f_lo + NC - 1) / NC);
     kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step, f_lo, f_hi);
     return 1;
+}
+
+// thermo mode of the Roe/eigen thermo (physics.cuh sp_h_R): a calorically
+// perfect single-species mixture (the gamma-gas) takes the instantiation with
+// only those forms compiled in
+template <int NS, int DIR, bool TENO, bool CHAR>
+inline int launch_faces3d(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
+                          int f_lo = 0, int f_hi = -1) {
+    if constexpr (NS == 1) {
+        if (P.mix.all_simple)
+            return launch_faces3d_tm<NS, DIR, TENO, CHAR, 1>(P, Ut, stage, step, s, f_lo, f_hi);
+    }
+    return launch_faces3d_tm<NS, DIR, TENO, CHAR, 0>(P, Ut, stage, step, s, f_lo, f_hi);
 }
 
 }  // namespace ign

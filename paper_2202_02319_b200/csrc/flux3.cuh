@@ -83,7 +83,7 @@ IGN_HD void mapped_flux3(const double* U, double p, double u, double v, double w
 }
 
 // roe_average (flux.hpp:157-186) + w
-template <int NS>
+template <int NS, int TM = 0>
 IGN_HD void roe_average3(double rho_l, const double* Yl, double Tl, double ul, double vl,
                          double wl_, double rho_r, const double* Yr, double Tr, double ur,
                          double vr, double wr_, const DMix& m, double* Y, double& T, double& u,
@@ -96,14 +96,14 @@ IGN_HD void roe_average3(double rho_l, const double* Yl, double Tl, double ul, d
     w = (wl * wl_ + wr * wr_) * inv;
 #pragma unroll
     for (int s = 0; s < NS; ++s) Y[s] = (wl * Yl[s] + wr * Yr[s]) * inv;
-    const double Hl = h_mass<NS>(Tl, Yl, m) + 0.5 * ((ul * ul + vl * vl) + wl_ * wl_);
-    const double Hr = h_mass<NS>(Tr, Yr, m) + 0.5 * ((ur * ur + vr * vr) + wr_ * wr_);
+    const double Hl = h_mass<NS, false, TM>(Tl, Yl, m) + 0.5 * ((ul * ul + vl * vl) + wl_ * wl_);
+    const double Hr = h_mass<NS, false, TM>(Tr, Yr, m) + 0.5 * ((ur * ur + vr * vr) + wr_ * wr_);
     const double H = (wl * Hl + wr * Hr) * inv;
     const double h = H - 0.5 * ((u * u + v * v) + w * w);
     double Tt = 0.5 * (Tl + Tr);
     for (int it = 0; it < 50; ++it) {
-        const double r = h_mass<NS>(Tt, Y, m) - h;
-        const double cp = cp_mass<NS>(Tt, Y, m);
+        const double r = h_mass<NS, false, TM>(Tt, Y, m) - h;
+        const double cp = cp_mass<NS, false, TM>(Tt, Y, m);
         const double Tn = Tt - r / cp;
         if (fabs(Tn - Tt) <= 1e-14 * Tt) {
             Tt = Tn;
@@ -122,7 +122,7 @@ template <int NS> struct Eigen3 {
 };
 
 // EigenSystem::at_state (flux.hpp:72-104); DIR < 2: m = (m1, m2, 0), DIR 2: (0, 0, m1)
-template <int NS, int DIR>
+template <int NS, int DIR, int TM = 0>
 IGN_HD int eigen_at_state3(const double* Y, double T, double uu, double vv, double ww,
                            double m1, double m2, const DMix& m, Eigen3<NS>& e) {
     if (DIR < 2) {
@@ -151,14 +151,14 @@ IGN_HD int eigen_at_state3(const double* Y, double T, double uu, double vv, doub
 #pragma unroll
     for (int s = 0; s < NS; ++s) e.Y[s] = Y[s];
     const double rbar = r_specific<NS>(Y, m);
-    const double cv = cp_mass<NS>(T, Y, m) - rbar;
+    const double cv = cp_mass<NS, false, TM>(T, Y, m) - rbar;
     e.kappa = rbar / cv;
-    const double h = h_mass<NS>(T, Y, m);
+    const double h = h_mass<NS, false, TM>(T, Y, m);
     double c2 = e.kappa * h;
 #pragma unroll
     for (int sp = 0; sp < NS; ++sp) {
         const double rs = divW(m.sp[sp], m.R);
-        const double es = h_species(T, m.sp[sp], m.R) - rs * T;
+        const double es = h_species<TM>(T, m.sp[sp], m.R) - rs * T;
         const double chi = rs * T - e.kappa * es;
         e.Theta[sp] = chi + e.kappa * e.k;
         c2 += Y[sp] * chi;
