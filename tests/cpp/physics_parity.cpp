@@ -186,11 +186,12 @@ static void check_mixture(const ignis::MixtureModel& mix, const char* name, unsi
 
 // TENO6's cutoff filter (physics.cuh teno_cutoff_filter) at the decision
 // boundary: for random stencils, ct is placed ON one candidate's exact ratio
-// g_k/gsum (times 1 + O(1e-6) jitter, inside and outside the filter band), so
+// g_k/gsum (times 1 + O(1e-7 .. 1e-3) jitter, inside and outside the filter
+// band), so
 // every branch of the filter and its exact fallback is exercised.
 static void check_teno_cutoff_boundary() {
     std::mt19937 rng(4242);
-    std::uniform_real_distribution<double> u(-2.0, 2.0), jit(-3e-7, 3e-7);
+    std::uniform_real_distribution<double> u(-2.0, 2.0), jit(-3e-7, 3e-7), wide(-1.5e-3, 1.5e-3);
     std::uniform_int_distribution<int> pick(0, 3);
     std::uniform_real_distribution<double> lg(-12.0, 0.0);
     int filtered = 0, exact = 0;
@@ -225,9 +226,12 @@ static void check_teno_cutoff_boundary() {
         }
         gsum = g[0] + g[1] + g[2] + g[3];
         const double Q = g[pick(rng)] / gsum;
-        // ct on the exact ratio, or 1 + O(1e-7) away from it on either side
-        const int mode = trial % 4;
-        double ct = mode == 0 ? Q : Q * (1.0 + (mode == 1 ? 1.0 : 10.0) * jit(rng));
+        // ct on the exact ratio, 1 + O(1e-7 .. 1e-6) away from it, or up to
+        // 1.5e-3 away — across the filter's 2e-4 band edges on both sides
+        const int mode = trial % 5;
+        double ct = mode == 0 ? Q
+                    : mode == 4 ? Q * (1.0 + wide(rng))
+                                : Q * (1.0 + (mode == 1 ? 1.0 : 10.0) * jit(rng));
         if (!(ct > 0.0 && ct < 1.0)) continue;
         const ign::ReconParams rp = ign::make_recon_params(ct, 1e-40);
         const double B[4] = {b[0] + 1e-40, b[1] + 1e-40, b[2] + 1e-40, b[3] + 1e-40};
