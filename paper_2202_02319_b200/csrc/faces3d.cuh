@@ -96,8 +96,14 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
 #ifndef IGN_F3_MINB
 #define IGN_F3_MINB 3
 #endif
+// xi faces (55 KB shared): 4 CTAs/SM at <= 96 registers beat 3 CTAs without
+// the small spill (-1.2% faces, 256^3); eta/zeta (67-71 KB) stay at 3
+#ifndef IGN_F3X_MINB
+#define IGN_F3X_MINB 4
+#endif
 template <int NS, int DIR, bool TENO, bool CHAR, int TM>
-__global__ void __launch_bounds__(32 * (NS + 4), (NS == 1 && DIR == 2) ? IGN_F3_MINB : 1)
+__global__ void __launch_bounds__(32 * (NS + 4),
+                                  NS != 1 ? 1 : DIR == 2 ? IGN_F3_MINB : DIR == 0 ? IGN_F3X_MINB : 1)
 k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
           int f_lo, int f_hi) {
     using Smem = FaceSmem3<NS, DIR, TENO, CHAR>;
