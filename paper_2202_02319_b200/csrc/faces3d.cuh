@@ -589,7 +589,8 @@ inline int launch_faces3d_tm(const KParams& P, const double* Ut, int stage, int 
 }
 
 // thermo mode of the Roe/eigen thermo (physics.cuh sp_h_R): a calorically
-// perfect single-species mixture (the gamma-gas) takes the instantiation with
+// perfect single-species mixture (the gamma-gas) or an all-lin2 mixture (every
+// table in data/ and the reference's ch4_o2.mix) takes the instantiation with
 // only those forms compiled in
 template <int NS, int DIR, bool TENO, bool CHAR>
 inline int launch_faces3d(const KParams& P, const double* Ut, int stage, int step, cudaStream_t s,
@@ -597,6 +598,9 @@ inline int launch_faces3d(const KParams& P, const double* Ut, int stage, int ste
     if constexpr (NS == 1) {
         if (P.mix.all_simple)
             return launch_faces3d_tm<NS, DIR, TENO, CHAR, 1>(P, Ut, stage, step, s, f_lo, f_hi);
+    } else {
+        if (P.mix.all_lin2)
+            return launch_faces3d_tm<NS, DIR, TENO, CHAR, 2>(P, Ut, stage, step, s, f_lo, f_hi);
     }
     return launch_faces3d_tm<NS, DIR, TENO, CHAR, 0>(P, Ut, stage, step, s, f_lo, f_hi);
 }
