@@ -138,66 +138,106 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         }
     };
 
-    // ---------------- phase 1a: node window -> shared memory.  Each thread
-    // stages NIT nodes (NIT = ceil(NT / NF)); every node's loads are issued
-    // before any is consumed, so their latencies overlap
-    constexpr int NIT = (NT + NF - 1) / NF;
-    double raw[NIT][NC + 7];
-    int slot_t[NIT];
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int t = threadIdx.x + it * NF;
-        long long id = 0;
-        bool ok = t < NT;
-        if (DIR == 0) {
-            const int n0 = L0 + W - 1;  // window slots of the first segment
-            int a, row;
-            if (t < n0) {
-                a = f0 - H + t;
-                row = r0;
+    // ---------------- phase 1a: node window -> shared memory
+    if constexpr (CHAR) {
+        // ---------------- phase 1a: node window -> shared memory.  Each thread
+        // stages NIT nodes (NIT = ceil(NT / NF)); every node's loads are issued
+        // before any is consumed, so their latencies overlap
+        constexpr int NIT = (NT + NF - 1) / NF;
+        double raw[NIT][NC + 7];
+        int slot_t[NIT];
+    #pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int t = threadIdx.x + it * NF;
+            long long id = 0;
+            bool ok = t < NT;
+            if (DIR == 0) {
+                const int n0 = L0 + W - 1;  // window slots of the first segment
+                int a, row;
+                if (t < n0) {
+                    a = f0 - H + t;
+                    row = r0;
+                } else {
+                    a = -H + (t - n0);
+                    row = r0 + 1;
+                }
+                id = pidx(P, a, row);
+                ok = ok && a < P.nx + P.g && row < P.ny && (t < n0 || t - n0 < NF - L0 + W - 1);
             } else {
-                a = -H + (t - n0);
-                row = r0 + 1;
+                const int r = t / 32, l = t % 32;
+                id = win0 + (long long)r * P.sx + l;
+                ok = ok && i0 + l < P.nx && f0 - H + r < P.ny + P.g;
             }
-            id = pidx(P, a, row);
-            ok = ok && a < P.nx + P.g && row < P.ny && (t < n0 || t - n0 < NF - L0 + W - 1);
-        } else {
-            const int r = t / 32, l = t % 32;
-            id = win0 + (long long)r * P.sx + l;
-            ok = ok && i0 + l < P.nx && f0 - H + r < P.ny + P.g;
+            slot_t[it] = ok ? t : -1;
+            if (!ok) continue;
+            double* q = raw[it];
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) q[c] = ldg(Ut + c * P.plane + id);
+            q[NC] = ldg(P.jac + id);
+            q[NC + 1] = ldg(PU(P) + id);
+            q[NC + 2] = ldg(PV(P) + id);
+            q[NC + 3] = ldg(PP(P) + id);
+            q[NC + 4] = ldg(m1a + id);
+            q[NC + 5] = ldg(m2a + id);
+            q[NC + 6] = ldg(PC(P) + id);
         }
-        slot_t[it] = ok ? t : -1;
-        if (!ok) continue;
-        double* q = raw[it];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) q[c] = ldg(Ut + c * P.plane + id);
-        q[NC] = ldg(P.jac + id);
-        q[NC + 1] = ldg(PU(P) + id);
-        q[NC + 2] = ldg(PV(P) + id);
-        q[NC + 3] = ldg(PP(P) + id);
-        q[NC + 4] = ldg(m1a + id);
-        q[NC + 5] = ldg(m2a + id);
-        q[NC + 6] = ldg(PC(P) + id);
-    }
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int t = slot_t[it];
-        if (t < 0) continue;
-        const double* q = raw[it];
-        const double J = q[NC];
-        double Uk[NC], Fk[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) Uk[c] = q[c] * J;
-        const double nu = q[NC + 1], nv = q[NC + 2];
-        mapped_flux_uv<NS>(Uk, q[NC + 3], nu, nv, q[NC + 4], q[NC + 5], Fk);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            S.U[c][t] = Uk[c];
-            S.F[c][t] = Fk[c];
+    #pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int t = slot_t[it];
+            if (t < 0) continue;
+            const double* q = raw[it];
+            const double J = q[NC];
+            double Uk[NC], Fk[NC];
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) Uk[c] = q[c] * J;
+            const double nu = q[NC + 1], nv = q[NC + 2];
+            mapped_flux_uv<NS>(Uk, q[NC + 3], nu, nv, q[NC + 4], q[NC + 5], Fk);
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                S.U[c][t] = Uk[c];
+                S.F[c][t] = Fk[c];
+            }
+            S.u[t] = nu;
+            S.v[t] = nv;
+            S.c[t] = q[NC + 6];
         }
-        S.u[t] = nu;
-        S.v[t] = nv;
-        S.c[t] = q[NC + 6];
+    } else {  // componentwise: the plain loop (hoisting costs it occupancy)
+        for (int t = threadIdx.x; t < NT; t += blockDim.x) {
+            long long id;
+            bool ok;
+            if (DIR == 0) {
+                const int n0 = L0 + W - 1;  // window slots of the first segment
+                int a, row;
+                if (t < n0) {
+                    a = f0 - H + t;
+                    row = r0;
+                } else {
+                    a = -H + (t - n0);
+                    row = r0 + 1;
+                }
+                id = pidx(P, a, row);
+                ok = a < P.nx + P.g && row < P.ny && (t < n0 || t - n0 < NF - L0 + W - 1);
+            } else {
+                const int r = t / 32, l = t % 32;
+                id = win0 + (long long)r * P.sx + l;
+                ok = i0 + l < P.nx && f0 - H + r < P.ny + P.g;
+            }
+            if (!ok) continue;
+            const double J = ldg(P.jac + id);
+            double Uk[NC], Fk[NC];
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
+            const double nu = ldg(PU(P) + id), nv = ldg(PV(P) + id);
+            mapped_flux_uv<NS>(Uk, ldg(PP(P) + id), nu, nv, ldg(m1a + id), ldg(m2a + id), Fk);
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                S.U[c][t] = Uk[c];
+                S.F[c][t] = Fk[c];
+            }
+            S.u[t] = nu;
+            S.v[t] = nv;
+            S.c[t] = ldg(PC(P) + id);
+        }
     }
 
     // this thread's face in phase 1b: group = warp, lane

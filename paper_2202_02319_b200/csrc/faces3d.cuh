@@ -221,71 +221,116 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         }
     }
 
-    // ---------------- phase 1a: node window -> shared memory.  Each thread
-    // stages NIT nodes (NIT = ceil(NT / NF), 2 here); every node's 13 loads are
-    // issued before any is consumed, so the latencies overlap
-    constexpr int NIT = (NT + NF - 1) / NF;
-    double raw[NIT][NC + 8];
-    int slot_t[NIT];
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int t = threadIdx.x + it * NF;
-        int a = 0, col = 0;
-        bool ok = t < NT;
-        if (DIR == 0) {
-            const int n0 = L0 + W - 1;  // window slots of the first segment
-            if (t < n0) {
-                a = f0 - H + t;
-                col = r0;
+    // ---------------- phase 1a: node window -> shared memory
+    if constexpr (CHAR) {
+        // ---------------- phase 1a: node window -> shared memory.  Each thread
+        // stages NIT nodes (NIT = ceil(NT / NF), 2 here); every node's 13 loads are
+        // issued before any is consumed, so the latencies overlap
+        constexpr int NIT = (NT + NF - 1) / NF;
+        double raw[NIT][NC + 8];
+        int slot_t[NIT];
+    #pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int t = threadIdx.x + it * NF;
+            int a = 0, col = 0;
+            bool ok = t < NT;
+            if (DIR == 0) {
+                const int n0 = L0 + W - 1;  // window slots of the first segment
+                if (t < n0) {
+                    a = f0 - H + t;
+                    col = r0;
+                } else {
+                    a = -H + (t - n0);
+                    col = r0 + 1;
+                }
+                ok = ok && a < P.nx + P.g && col < nrows && (t < n0 || t - n0 < NF - L0 + W - 1);
             } else {
-                a = -H + (t - n0);
-                col = r0 + 1;
+                a = f0 - H + t / 32;
+                col = i0 + t % 32;
+                ok = ok && col < P.nx && a < nd + P.g;
             }
-            ok = ok && a < P.nx + P.g && col < nrows && (t < n0 || t - n0 < NF - L0 + W - 1);
-        } else {
-            a = f0 - H + t / 32;
-            col = i0 + t % 32;
-            ok = ok && col < P.nx && a < nd + P.g;
+            slot_t[it] = ok ? t : -1;
+            if (!ok) continue;
+            const long long id = node(a, col);
+            const int id2 = node2(a, col);
+            double* r = raw[it];
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) r[c] = ldg(Ut + c * P.plane + id);
+            r[NC] = ldg(P.jac + id2);
+            r[NC + 1] = ldg(PU3(P) + id);
+            r[NC + 2] = ldg(PV3(P) + id);
+            r[NC + 3] = ldg(PW3(P) + id);
+            r[NC + 4] = ldg(PP3(P) + id);
+            r[NC + 5] = ldg(m1a + id2);
+            r[NC + 6] = ldg(m2a + id2);
+            r[NC + 7] = ldg(PC3(P) + id);
         }
-        slot_t[it] = ok ? t : -1;
-        if (!ok) continue;
-        const long long id = node(a, col);
-        const int id2 = node2(a, col);
-        double* r = raw[it];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) r[c] = ldg(Ut + c * P.plane + id);
-        r[NC] = ldg(P.jac + id2);
-        r[NC + 1] = ldg(PU3(P) + id);
-        r[NC + 2] = ldg(PV3(P) + id);
-        r[NC + 3] = ldg(PW3(P) + id);
-        r[NC + 4] = ldg(PP3(P) + id);
-        r[NC + 5] = ldg(m1a + id2);
-        r[NC + 6] = ldg(m2a + id2);
-        r[NC + 7] = ldg(PC3(P) + id);
-    }
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int t = slot_t[it];
-        if (t < 0) continue;
-        const double* r = raw[it];
-        const double J = r[NC];
-        double Uk[NC], Fk[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) Uk[c] = r[c] * J;
-        const double nu = r[NC + 1], nv = r[NC + 2], nw = r[NC + 3];
-        mapped_flux3<NS, DIR>(Uk, r[NC + 4], nu, nv, nw, r[NC + 5], r[NC + 6], Fk);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            S.U[c][t] = Uk[c];
-            S.F[c][t] = Fk[c];
+    #pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int t = slot_t[it];
+            if (t < 0) continue;
+            const double* r = raw[it];
+            const double J = r[NC];
+            double Uk[NC], Fk[NC];
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) Uk[c] = r[c] * J;
+            const double nu = r[NC + 1], nv = r[NC + 2], nw = r[NC + 3];
+            mapped_flux3<NS, DIR>(Uk, r[NC + 4], nu, nv, nw, r[NC + 5], r[NC + 6], Fk);
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                S.U[c][t] = Uk[c];
+                S.F[c][t] = Fk[c];
+            }
+            if (DIR < 2) {
+                S.vel[0][t] = nu;
+                S.vel[DIR < 2 ? 1 : 0][t] = nv;
+            } else {
+                S.vel[0][t] = nw;
+            }
+            S.c[t] = r[NC + 7];
         }
-        if (DIR < 2) {
-            S.vel[0][t] = nu;
-            S.vel[DIR < 2 ? 1 : 0][t] = nv;
-        } else {
-            S.vel[0][t] = nw;
+    } else {  // componentwise: the plain loop (hoisting costs it occupancy)
+        for (int t = threadIdx.x; t < NT; t += blockDim.x) {
+            int a, col;
+            bool ok;
+            if (DIR == 0) {
+                const int n0 = L0 + W - 1;  // window slots of the first segment
+                if (t < n0) {
+                    a = f0 - H + t;
+                    col = r0;
+                } else {
+                    a = -H + (t - n0);
+                    col = r0 + 1;
+                }
+                ok = a < P.nx + P.g && col < nrows && (t < n0 || t - n0 < NF - L0 + W - 1);
+            } else {
+                a = f0 - H + t / 32;
+                col = i0 + t % 32;
+                ok = col < P.nx && a < nd + P.g;
+            }
+            if (!ok) continue;
+            const long long id = node(a, col);
+            const int id2 = node2(a, col);
+            const double J = ldg(P.jac + id2);
+            double Uk[NC], Fk[NC];
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) Uk[c] = ldg(Ut + c * P.plane + id) * J;
+            const double nu = ldg(PU3(P) + id), nv = ldg(PV3(P) + id), nw = ldg(PW3(P) + id);
+            mapped_flux3<NS, DIR>(Uk, ldg(PP3(P) + id), nu, nv, nw, ldg(m1a + id2), ldg(m2a + id2),
+                                  Fk);
+    #pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                S.U[c][t] = Uk[c];
+                S.F[c][t] = Fk[c];
+            }
+            if (DIR < 2) {
+                S.vel[0][t] = nu;
+                S.vel[DIR < 2 ? 1 : 0][t] = nv;
+            } else {
+                S.vel[0][t] = nw;
+            }
+            S.c[t] = ldg(PC3(P) + id);
         }
-        S.c[t] = r[NC + 7];
     }
 
     if (CHAR) {

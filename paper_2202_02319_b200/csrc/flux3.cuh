@@ -23,7 +23,7 @@ template <int NS> struct Prim3 {
 };
 
 // conservative_from_primitives (state.hpp:47-57) + w
-template <int NS>
+template <int NS, int TM = 0>
 IGN_HD void conservative_from_primitives3(const Prim3<NS>& pt, const DMix& m, double* U) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) U[s] = pt.rho * pt.Y[s];
@@ -31,12 +31,12 @@ IGN_HD void conservative_from_primitives3(const Prim3<NS>& pt, const DMix& m, do
     U[NS + 1] = pt.rho * pt.v;
     U[NS + 2] = pt.rho * pt.w;
     const double rs = r_specific<NS>(pt.Y, m);
-    const double e = e_mass_rs<NS>(pt.T, pt.Y, rs, m);
+    const double e = e_mass_rs<NS, false, TM>(pt.T, pt.Y, rs, m);
     U[NS + 3] = pt.rho * (e + 0.5 * ((pt.u * pt.u + pt.v * pt.v) + pt.w * pt.w));
 }
 
 // primitives_from_conservative (state.hpp:26-44) + w
-template <int NS, bool BF = false>
+template <int NS, bool BF = false, int TM = 0>
 IGN_HD int primitives_from_conservative3(const double* U, const DMix& m, double T_guess,
                                          Prim3<NS>& pt, double* rs_out) {
     double rho = 0.0;
@@ -54,7 +54,7 @@ IGN_HD int primitives_from_conservative3(const double* U, const DMix& m, double 
         fdiv(U[NS + 3], rho, yr) - 0.5 * ((pt.u * pt.u + pt.v * pt.v) + pt.w * pt.w);
     const double rs = r_specific<NS>(pt.Y, m);
     int st;
-    pt.T = temperature_from_energy<NS, BF>(e, pt.Y, rs, m, T_guess, &st);
+    pt.T = temperature_from_energy<NS, BF, TM>(e, pt.Y, rs, m, T_guess, &st);
     if (st != T_OK) return st;
     pt.p = pt.rho * rs * pt.T;
     *rs_out = rs;

@@ -30,7 +30,7 @@ namespace ign {
 // fill_ghosts (boundary.hpp:136-258).  One thread per (edge, t) runs the
 // reference's k = 1..g loop.  x edges cover rows 0..ny-1 (launch 1), y edges
 // the full padded range -g..nx+g-1 (launch 2), so corners take the y rule.
-template <int NS>
+template <int NS, int TM>
 __device__ int bc_prim_at(const KParams& P, const double* Ut, int i, int j, Prim<NS>& pt,
                           double& rs) {
     const long long id = pidx(P, i, j);
@@ -38,13 +38,13 @@ __device__ int bc_prim_at(const KParams& P, const double* Ut, int i, int j, Prim
     double U[NS + 3];
 #pragma unroll
     for (int c = 0; c < NS + 3; ++c) U[c] = Ut[c * P.plane + id] * J;
-    return primitives_from_conservative<NS, true>(U, P.mix, 300.0, pt, &rs);
+    return primitives_from_conservative<NS, true, TM>(U, P.mix, 300.0, pt, &rs);
 }
 
-template <int NS>
+template <int NS, int TM>
 __device__ void bc_store(const KParams& P, double* Ut, const Prim<NS>& pt, int i, int j) {
     double U[NS + 3];
-    conservative_from_primitives<NS>(pt, P.mix, U);
+    conservative_from_primitives<NS, TM>(pt, P.mix, U);
     const long long id = pidx(P, i, j);
     const double invJ = 1.0 / P.jac[id];
 #pragma unroll
@@ -59,7 +59,7 @@ __device__ void bc_copy_scaled(const KParams& P, double* Ut, int is, int js, int
     for (int c = 0; c < NS + 3; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
 }
 
-template <int NS>
+template <int NS, int TM>
 __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, double* Ut,
                                             int ypass, int stage, int step) {
     if (failed(P.err)) return;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
             Prim<NS> pt;
             double rs;
-            const int st = bc_prim_at<NS>(P, Ut, mi, mj, pt, rs);
+            const int st = bc_prim_at<NS, TM>(P, Ut, mi, mj, pt, rs);
             if (st) {
                 report(P.err, stage, PH_BC, ekey + k, st, step);
                 return;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
                 pt.T = smax(tg, 0.05 * P.T_wall[edge]);
             }
             pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
-            bc_store<NS>(P, Ut, pt, gi, gj);
+            bc_store<NS, TM>(P, Ut, pt, gi, gj);
         }
         break;
     }
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
         ij(side == 0 ? 0 : n - 1, ii, ji);
         Prim<NS> inner;
         double rs;
-        const int st = bc_prim_at<NS>(P, Ut, ii, ji, inner, rs);
+        const int st = bc_prim_at<NS, TM>(P, Ut, ii, ji, inner, rs);
         if (st) {
             report(P.err, stage, PH_BC, ekey, st, step);
             return;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
             for (int s = 0; s < NS; ++s) pt.Y[s] = q[3 + s];
             pt.p = inner.p;
             pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
-            bc_store<NS>(P, Ut, pt, gi, gj);
+            bc_store<NS, TM>(P, Ut, pt, gi, gj);
         }
         break;
     }
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
 // refresh_primitives (solver.hpp:148-177) over the padded box; the cached T
 // is the Newton guess (thermo.hpp:196).
 // 2-4 species: 4 CTAs/SM (64 registers, small spill): jet primitives -10%
-template <int NS, bool WX>
-__global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim(const __grid_constant__ KParams P,
+template <int NS, bool WX, int TM>
+__global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim(const __grid_constant__ KParams P,
                                               const double* __restrict__ Ut, int stage,
                                               int step, long long id_lo, long long id_hi) {
     if (failed(P.err)) return;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim(const
     for (int c = 0; c < NS + 3; ++c) U[c] = Ut[c * P.plane + id] * J;
     Prim<NS> pt;
     double rs;
-    const int st = primitives_from_conservative<NS, true>(U, P.mix, PT(P)[id], pt, &rs);
+    const int st = primitives_from_conservative<NS, true, TM>(U, P.mix, PT(P)[id], pt, &rs);
     if (st) {
         report(P.err, stage, PH_PRIM, (unsigned long long)(id + (long long)P.j0 * P.sx), st,
                step);
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim(const
     PV(P)[id] = pt.v;
     PP(P)[id] = pt.p;
     PT(P)[id] = pt.T;
-    PC(P)[id] = sound_speed_rs<NS, true>(pt.T, pt.Y, rs, P.mix);
+    PC(P)[id] = sound_speed_rs<NS, true, TM>(pt.T, pt.Y, rs, P.mix);
 #pragma unroll
     for (int s = 0; s < NS; ++s) PY(P, s)[id] = pt.Y[s];
     if (WX) {
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim(const
 // ---------------------------------------------------------------- viscous
 // compute_viscous node fluxes over ring 1 (solver.hpp:610-696).
 // 2-4 species: 6 CTAs/SM (a small spill) hide more load latency (H2/O2 -14%)
-template <int NS>
+template <int NS, int TM>
 __global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc(const __grid_constant__ KParams P, int stage,
                                               int step) {
     constexpr int NC = NS + 3;
@@ -241,10 +241,10 @@ __global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc(const
         X[s] = ldg(PX(P, s) + id);
         gx[s] = gradx(PX(P, s));
         gy[s] = grady(PX(P, s));
-        hs[s] = h_species(T, P.mix.sp[s], P.mix.R);
+        hs[s] = h_species<TM>(T, P.mix.sp[s], P.mix.R);
     }
     double mu, lambda, D, cp;
-    transport<NS>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
+    transport<NS, TM>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
     const double div = ux + vy;
     const double txx = mu * (2.0 * ux - (2.0 / 3.0) * div);
     const double tyy = mu * (2.0 * vy - (2.0 / 3.0) * div);
@@ -543,7 +543,12 @@ template <int NS> struct Launch {
     // the full padded width (ypass 1) — boundary.hpp:254-257
     static int bc(const KParams& P, double* Ut, int ypass, int stage, int step, cudaStream_t s) {
         const int n = ypass ? P.nx + 2 * P.g : P.ny;
-        k_bc<NS><<<(2 * n + 127) / 128, 128, 0, s>>>(P, Ut, ypass, stage, step);
+        const unsigned nb = (2 * n + 127) / 128;
+        switch (thermo_mode<NS>(P.mix)) {
+        case 1: k_bc<NS, 1><<<nb, 128, 0, s>>>(P, Ut, ypass, stage, step); break;
+        case 2: k_bc<NS, 2><<<nb, 128, 0, s>>>(P, Ut, ypass, stage, step); break;
+        default: k_bc<NS, 0><<<nb, 128, 0, s>>>(P, Ut, ypass, stage, step); break;
+        }
         return 1;
     }
     // padded rows [r_lo, r_hi)
@@ -552,8 +557,16 @@ template <int NS> struct Launch {
         const long long lo = (long long)r_lo * P.sx, hi = (long long)r_hi * P.sx;
         if (hi <= lo) return 0;
         const unsigned nb = (unsigned)((hi - lo + 255) / 256);
-        if (P.viscous) k_prim<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
-        else k_prim<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+        const int tm = thermo_mode<NS>(P.mix);
+        if (P.viscous) {
+            if (tm == 1) k_prim<NS, true, 1><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+            else if (tm == 2) k_prim<NS, true, 2><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+            else k_prim<NS, true, 0><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+        } else {
+            if (tm == 1) k_prim<NS, false, 1><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+            else if (tm == 2) k_prim<NS, false, 2><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+            else k_prim<NS, false, 0><<<nb, 256, 0, s>>>(P, Ut, stage, step, lo, hi);
+        }
         return 1;
     }
     // part (KernelSet): 0 the padded box, 1 this slab's own rows, 2 its ghost rows
@@ -590,7 +603,12 @@ template <int NS> struct Launch {
     }
     static int visc(const KParams& P, int stage, int step, cudaStream_t s) {
         const long long n = (long long)(P.nx + 2) * (P.ny + 2);
-        k_visc<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, stage, step);
+        const unsigned nb = (unsigned)((n + 127) / 128);
+        switch (thermo_mode<NS>(P.mix)) {
+        case 1: k_visc<NS, 1><<<nb, 128, 0, s>>>(P, stage, step); break;
+        case 2: k_visc<NS, 2><<<nb, 128, 0, s>>>(P, stage, step); break;
+        default: k_visc<NS, 0><<<nb, 128, 0, s>>>(P, stage, step); break;
+        }
         return 1;
     }
     template <bool EDGE>

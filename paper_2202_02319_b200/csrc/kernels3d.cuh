@@ -18,7 +18,7 @@ namespace ign {
 // the reference's 2D edge rules extended by w (walls mirror it, inflow sets
 // w = 0); then z (periodic) over whole (x, y) planes unless the z ghost planes
 // come from the neighbouring z-slabs.
-template <int NS>
+template <int NS, int TM>
 __device__ int bc3_prim_at(const KParams& P, const double* Ut, int i, int j, int k,
                            Prim3<NS>& pt, double& rs) {
     const long long id = pidx3(P, i, j, k);
@@ -26,13 +26,13 @@ __device__ int bc3_prim_at(const KParams& P, const double* Ut, int i, int j, int
     double U[NS + 4];
 #pragma unroll
     for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
-    return primitives_from_conservative3<NS, true>(U, P.mix, 300.0, pt, &rs);
+    return primitives_from_conservative3<NS, true, TM>(U, P.mix, 300.0, pt, &rs);
 }
 
-template <int NS>
+template <int NS, int TM>
 __device__ void bc3_store(const KParams& P, double* Ut, const Prim3<NS>& pt, int i, int j, int k) {
     double U[NS + 4];
-    conservative_from_primitives3<NS>(pt, P.mix, U);
+    conservative_from_primitives3<NS, TM>(pt, P.mix, U);
     const long long id = pidx3(P, i, j, k);
     const double invJ = 1.0 / P.jac[(j + P.g) * P.sx + (i + P.g)];
 #pragma unroll
@@ -49,7 +49,7 @@ __device__ void bc3_copy_scaled(const KParams& P, double* Ut, int is, int js, in
     for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
 }
 
-template <int NS>
+template <int NS, int TM>
 __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, double* Ut,
                                              int pass, int stage, int step) {
     if (failed(P.err)) return;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
             Prim3<NS> pt;
             double rs;
-            const int st = bc3_prim_at<NS>(P, Ut, mi, mj, kz, pt, rs);
+            const int st = bc3_prim_at<NS, TM>(P, Ut, mi, mj, kz, pt, rs);
             if (st) {
                 report(P.err, stage, PH_BC, ekey + k, st, step);
                 return;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
                 pt.T = smax(tg, 0.05 * P.T_wall[edge]);
             }
             pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
-            bc3_store<NS>(P, Ut, pt, gi, gj, kz);
+            bc3_store<NS, TM>(P, Ut, pt, gi, gj, kz);
         }
         break;
     }
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
         ij(side == 0 ? 0 : n - 1, ii, ji);
         Prim3<NS> inner;
         double rs;
-        const int st = bc3_prim_at<NS>(P, Ut, ii, ji, kz, inner, rs);
+        const int st = bc3_prim_at<NS, TM>(P, Ut, ii, ji, kz, inner, rs);
         if (st) {
             report(P.err, stage, PH_BC, ekey, st, step);
             return;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
             for (int s = 0; s < NS; ++s) pt.Y[s] = q[3 + s];
             pt.p = inner.p;
             pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
-            bc3_store<NS>(P, Ut, pt, gi, gj, kz);
+            bc3_store<NS, TM>(P, Ut, pt, gi, gj, kz);
         }
         break;
     }
@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
 
 // ---------------------------------------------------------------- primitives
 // 2-4 species: 4 CTAs/SM (64 registers, small spill): jet primitives -10%
-template <int NS, bool WX>
-__global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim3(const __grid_constant__ KParams P,
+template <int NS, bool WX, int TM>
+__global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim3(const __grid_constant__ KParams P,
                                                const double* __restrict__ Ut, int stage,
                                                int step, int k_lo) {
     if (failed(P.err)) return;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim3(cons
     for (int c = 0; c < NS + 4; ++c) U[c] = Ut[c * P.plane + id] * J;
     Prim3<NS> pt;
     double rs;
-    const int st = primitives_from_conservative3<NS, true>(U, P.mix, PT3(P)[id], pt, &rs);
+    const int st = primitives_from_conservative3<NS, true, TM>(U, P.mix, PT3(P)[id], pt, &rs);
     if (st) {
         report(P.err, stage, PH_PRIM, (unsigned long long)(id + (long long)P.j0 * P.sxy), st,
                step);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim3(cons
     PW3(P)[id] = pt.w;
     PP3(P)[id] = pt.p;
     PT3(P)[id] = pt.T;
-    PC3(P)[id] = sound_speed_rs<NS, true>(pt.T, pt.Y, rs, P.mix);
+    PC3(P)[id] = sound_speed_rs<NS, true, TM>(pt.T, pt.Y, rs, P.mix);
 #pragma unroll
     for (int s = 0; s < NS; ++s) PY3(P, s)[id] = pt.Y[s];
     if (WX) {
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_prim3(cons
 // the zeta flux appended after the reference's 2D terms
 // 2-4 species: 6 CTAs/SM (<= 85 registers, a small spill) hide more of the
 // stencil loads' latency (jet visc3 -6.5%); the gamma-gas keeps 122 registers
-template <int NS>
+template <int NS, int TM>
 __global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc3(const __grid_constant__ KParams P, int stage,
                                                int step) {
     constexpr int NC = NS + 4;
@@ -241,10 +241,10 @@ __global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc3(cons
         gx[s] = gradx(PX3(P, s));
         gy[s] = grady(PX3(P, s));
         gz[s] = gradz(PX3(P, s));
-        hs[s] = h_species(T, P.mix.sp[s], P.mix.R);
+        hs[s] = h_species<TM>(T, P.mix.sp[s], P.mix.R);
     }
     double mu, lambda, D, cp;
-    transport<NS>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
+    transport<NS, TM>(rho, T, Y, X, P.mix, mu, lambda, D, cp);
     const double div = (ux + vy) + wz;
     const double txx = mu * (2.0 * ux - (2.0 / 3.0) * div);
     const double tyy = mu * (2.0 * vy - (2.0 / 3.0) * div);
@@ -564,6 +564,14 @@ __global__ void __launch_bounds__(256) k_dt3(const __grid_constant__ KParams P) 
 }
 
 template <int NS> struct Launch3 {
+    static void bc3_launch(const KParams& P, double* Ut, int pass, int stage, int step,
+                           unsigned nb, cudaStream_t s) {
+        switch (thermo_mode<NS>(P.mix)) {
+        case 1: k_bc3<NS, 1><<<nb, 128, 0, s>>>(P, Ut, pass, stage, step); break;
+        case 2: k_bc3<NS, 2><<<nb, 128, 0, s>>>(P, Ut, pass, stage, step); break;
+        default: k_bc3<NS, 0><<<nb, 128, 0, s>>>(P, Ut, pass, stage, step); break;
+        }
+    }
     // ypass 0 (before the halo exchange): x then y periodic copies, so the
     // exchanged z planes carry their x/y ghosts; ypass 1: z copies (single
     // domain) — with z-slabs the z ghost planes came from the peers instead
@@ -571,14 +579,14 @@ template <int NS> struct Launch3 {
         const int g = P.g;
         if (ypass == 0) {
             const int n0 = 2 * P.ny * P.nz;
-            k_bc3<NS><<<(unsigned)((n0 + 127) / 128), 128, 0, s>>>(P, Ut, 0, stage, step);
+            bc3_launch(P, Ut, 0, stage, step, (unsigned)((n0 + 127) / 128), s);
             const int n1 = 2 * (P.nx + 2 * g) * P.nz;
-            k_bc3<NS><<<(unsigned)((n1 + 127) / 128), 128, 0, s>>>(P, Ut, 1, stage, step);
+            bc3_launch(P, Ut, 1, stage, step, (unsigned)((n1 + 127) / 128), s);
             return 2;
         }
         if (P.zhalo) return 0;
         const int n2 = 2 * (P.nx + 2 * g) * (P.ny + 2 * g);
-        k_bc3<NS><<<(unsigned)((n2 + 127) / 128), 128, 0, s>>>(P, Ut, 2, stage, step);
+        bc3_launch(P, Ut, 2, stage, step, (unsigned)((n2 + 127) / 128), s);
         return 1;
     }
     // padded z planes [k_lo, k_hi)
@@ -586,8 +594,16 @@ template <int NS> struct Launch3 {
                            cudaStream_t s, int k_lo, int k_hi) {
         if (k_hi <= k_lo) return 0;
         const dim3 nb((unsigned)((P.sxy + 255) / 256), (unsigned)(k_hi - k_lo));
-        if (P.viscous) k_prim3<NS, true><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
-        else k_prim3<NS, false><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+        const int tm = thermo_mode<NS>(P.mix);
+        if (P.viscous) {
+            if (tm == 1) k_prim3<NS, true, 1><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+            else if (tm == 2) k_prim3<NS, true, 2><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+            else k_prim3<NS, true, 0><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+        } else {
+            if (tm == 1) k_prim3<NS, false, 1><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+            else if (tm == 2) k_prim3<NS, false, 2><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+            else k_prim3<NS, false, 0><<<nb, 256, 0, s>>>(P, Ut, stage, step, k_lo);
+        }
         return 1;
     }
     // part (KernelSet): 0 the padded box, 1 this slab's own planes, 2 its ghost planes
@@ -627,7 +643,12 @@ template <int NS> struct Launch3 {
     }
     static int visc(const KParams& P, int stage, int step, cudaStream_t s) {
         const long long n = (long long)(P.nx + 2) * (P.ny + 2) * (P.nz + 2);
-        k_visc3<NS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, stage, step);
+        const unsigned nb = (unsigned)((n + 127) / 128);
+        switch (thermo_mode<NS>(P.mix)) {
+        case 1: k_visc3<NS, 1><<<nb, 128, 0, s>>>(P, stage, step); break;
+        case 2: k_visc3<NS, 2><<<nb, 128, 0, s>>>(P, stage, step); break;
+        default: k_visc3<NS, 0><<<nb, 128, 0, s>>>(P, stage, step); break;
+        }
         return 1;
     }
     template <bool EDGE>

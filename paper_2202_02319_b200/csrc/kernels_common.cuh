@@ -150,6 +150,15 @@ namespace ign {
 #define PY3(P, s) ((P).prim + (7 + (s)) * (P).plane)
 #define PX3(P, s) ((P).prim + (7 + (P).ns + (s)) * (P).plane)
 
+// Compile-time thermo mode of a kernel launch (physics.cuh sp_h_R): 1 = the
+// calorically perfect single-species gas, 2 = every species lin2 (multi-species
+// tables), 0 = the general piece code.  Instantiations for modes a species
+// count cannot take are never launched (NS == 1: 0/1; NS > 1: 0/2).
+template <int NS> inline int thermo_mode(const DMix& m) {
+    if (NS == 1) return m.all_simple ? 1 : 0;
+    return m.all_lin2 ? 2 : 0;
+}
+
 // Launcher table of one (species count, dimension) instantiation; every entry
 // returns the number of kernels it launched.
 struct KernelSet {
