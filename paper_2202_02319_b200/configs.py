@@ -505,8 +505,9 @@ def tgv3d(n: int = 256, *, viscous: bool = True, scheme: str = "teno6",
     p0 = 1.0 / (gamma * mach * mach)
     c0 = math.sqrt(gamma * p0)
     dx = L / n
-    # fixed step at CFL 0.5 on the inviscid 3D bound (|u|+|v|+|w| + sqrt3 c0 <= 3 + 1.74 c0)
-    dt = 0.5 * dx / (3.0 + math.sqrt(3.0) * c0)
+    # fixed step at CFL <= 0.5 in the reference's stable_dt form (solver.hpp:256-259,
+    # summed over the three directions): (|u| + |v| + |w| + 3 c) / dx <= (3 + 3 c0) / dx
+    dt = 0.5 * dx / (3.0 + 3.0 * c0)
 
     def ic(X, Y, Z):
         u = np.sin(X) * np.cos(Y) * np.cos(Z)

@@ -553,9 +553,23 @@ __global__ void __launch_bounds__(256) k_dt3(const __grid_constant__ KParams P) 
             }
         }
     }
-    if (lam_loc > 0.0) atomicMax(&s_lam, (unsigned long long)__double_as_longlong(lam_loc));
-    if (chem_loc < __longlong_as_double(0x7ff0000000000000ll))
-        atomicMin(&s_chem, (unsigned long long)__double_as_longlong(chem_loc));
+    // warp max / min first (on the bit patterns: lam > 0 and chem > 0, where
+    // the unsigned order is the numeric one; NaN lam is skipped as the
+    // reference's std::max skips it), then one shared atomic per warp
+    unsigned long long lb = lam_loc > 0.0 ? (unsigned long long)__double_as_longlong(lam_loc) : 0ull;
+    unsigned long long cb = chem_loc < __longlong_as_double(0x7ff0000000000000ll)
+                                ? (unsigned long long)__double_as_longlong(chem_loc)
+                                : 0x7ff0000000000000ull;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long lo = __shfl_xor_sync(0xffffffffu, lb, o);
+        const unsigned long long co = __shfl_xor_sync(0xffffffffu, cb, o);
+        lb = lo > lb ? lo : lb;
+        cb = co < cb ? co : cb;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lb) atomicMax(&s_lam, lb);
+        if (cb != 0x7ff0000000000000ull) atomicMin(&s_chem, cb);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_lam) atomicMax(&P.red[0], s_lam);
