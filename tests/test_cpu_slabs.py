@@ -129,3 +129,68 @@ def test_bench_reference_arm_under_torchrun_gloo():
         assert k in d, k
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "reference"
+
+
+def _halo_ring(rank, world, port, periodic, q):
+    """The halo protocol of runtime.cu t_exchange, restated over gloo: per
+    component, send our top g rows to hi_peer and our bottom g rows to lo_peer,
+    receive lo_peer's into the bottom ghosts and hi_peer's into the top ghosts,
+    in the [top, bottom] send / [lo, hi] receive order that makes a two-slab
+    periodic ring (lo_peer == hi_peer) match.  Peers as setup.cu assigns them."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ny, nx, g, nc = 4 * world + 3, 5, 3, 2
+    glob = torch.arange(nc * ny * nx, dtype=torch.float64).reshape(nc, ny, nx)
+    lo, cnt = slab_rows(ny, world, rank)
+    lo_peer = rank - 1 if rank > 0 else (world - 1 if periodic else -1)
+    hi_peer = rank + 1 if rank < world - 1 else (0 if periodic else -1)
+    loc = torch.full((nc, cnt + 2 * g, nx), -1.0, dtype=torch.float64)
+    loc[:, g:g + cnt] = glob[:, lo:lo + cnt]
+    for c in range(nc):
+        ops = []
+        if hi_peer >= 0:
+            ops.append(dist.P2POp(dist.isend, loc[c, cnt:cnt + g].contiguous(), hi_peer))
+        if lo_peer >= 0:
+            ops.append(dist.P2POp(dist.isend, loc[c, g:2 * g].contiguous(), lo_peer))
+        rb = torch.empty((g, nx), dtype=torch.float64)
+        rt = torch.empty((g, nx), dtype=torch.float64)
+        if lo_peer >= 0:
+            ops.append(dist.P2POp(dist.irecv, rb, lo_peer))
+        if hi_peer >= 0:
+            ops.append(dist.P2POp(dist.irecv, rt, hi_peer))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        if lo_peer >= 0:
+            loc[c, :g] = rb
+        if hi_peer >= 0:
+            loc[c, cnt + g:] = rt
+    ok = True
+    for j in range(-g, cnt + g):
+        jg = lo + j
+        if not (0 <= jg < ny):
+            if not periodic:
+                continue  # physical edge: the ghost-fill kernels own it
+            jg %= ny
+        ok &= bool(torch.equal(loc[:, g + j], glob[:, jg]))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,periodic", [(2, True), (2, False), (3, True)])
+def test_halo_protocol_gloo(world, periodic):
+    """World-size-2/3 run of the slab halo protocol (send/recv pairing, ring
+    wrap, physical edges) on CPU: every ghost row equals the global row."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_halo_ring, args=(r, world, port, periodic, q))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert [ok for _, ok in res] == [True] * world, res
