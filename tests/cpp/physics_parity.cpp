@@ -244,6 +244,32 @@ static void check_teno_cutoff_boundary() {
                 exact);
 }
 
+// TENO6's keep-all shortcut (ReconParams::keep_r): for cutoffs across the
+// whole range, random smooth / kinked / flat / step stencils, bitwise
+static void check_teno_keep_all() {
+    std::mt19937 rng(7);
+    std::uniform_real_distribution<double> u(-1.0, 1.0), lg(-15.0, 3.0);
+    const double cts[] = {1e-300, 1e-12, 1e-5, 1e-3, 0.02, 0.1, 0.2, 0.6};
+    for (const double ct : cts) {
+        const ign::ReconParams rp = ign::make_recon_params(ct, 1e-40);
+        for (int trial = 0; trial < 40000; ++trial) {
+            double w[6];
+            const double a = std::pow(10.0, lg(rng)), c = u(rng);
+            for (int q = 0; q < 6; ++q) {
+                switch (trial % 4) {
+                case 0: w[q] = c + a * std::sin(0.4 * q + u(rng) * 0.01); break;  // smooth
+                case 1: w[q] = c + a * std::abs(q - 2.5 + 0.3 * u(rng)); break;    // kink
+                case 2: w[q] = c; break;                                          // flat
+                default: w[q] = c + (q < 3 ? 0.0 : a) + 1e-3 * a * u(rng); break; // step
+                }
+            }
+            EXPECT_BITWISE("teno6_plus keep-all", 
+                           ign::teno6_plus(w[0], w[1], w[2], w[3], w[4], w[5], rp),
+                           ignis::recon::teno6_plus(w + 2, ct, 1e-40));
+        }
+    }
+}
+
 static void check_recon() {
     const ign::ReconParams rp = ign::make_recon_params(1e-5, 1e-40);
     std::mt19937 rng(42);
@@ -333,6 +359,7 @@ int main() {
     ignis::MixtureModel gas = ignis::MixtureModel::calorically_perfect(1.4, 1.0, 6.25e-4);
     gas.species[0].pieces[0].t_hi = 1e6;
     check_recon();
+    check_teno_keep_all();
     check_teno_cutoff_boundary();
     check_mixture<4>(ch4, "ch4_o2", 1234);  // two linear-cp ranges: DSpecies::lin2 path
     // the repo's H2/O2 table (one linear range and two), and a quartic variant
