@@ -211,7 +211,10 @@ __global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim(const __grid_cons
 // compute_viscous node fluxes over ring 1 (solver.hpp:610-696).
 // 2-4 species: 6 CTAs/SM (a small spill) hide more load latency (H2/O2 -14%)
 template <int NS, int TM>
-__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc(const __grid_constant__ KParams P, int stage,
+#ifndef IGN_VISC1_MINB
+#define IGN_VISC1_MINB 8  // one species: 8 CTAs/SM (64 registers, small spill) -4% viscous
+#endif
+__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : NS == 1 ? IGN_VISC1_MINB : 1) k_visc(const __grid_constant__ KParams P, int stage,
                                               int step) {
     constexpr int NC = NS + 3;
     if (failed(P.err)) return;

@@ -205,7 +205,10 @@ __global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim3(const __grid_con
 // 2-4 species: 6 CTAs/SM (<= 85 registers, a small spill) hide more of the
 // stencil loads' latency (jet visc3 -6.5%); the gamma-gas keeps 122 registers
 template <int NS, int TM>
-__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : 1) k_visc3(const __grid_constant__ KParams P, int stage,
+#ifndef IGN_VISC1_MINB
+#define IGN_VISC1_MINB 8  // one species: 8 CTAs/SM (64 registers, small spill) -4% viscous
+#endif
+__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : NS == 1 ? IGN_VISC1_MINB : 1) k_visc3(const __grid_constant__ KParams P, int stage,
                                                int step) {
     constexpr int NC = NS + 4;
     if (failed(P.err)) return;
