@@ -600,7 +600,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 for (int sp = 0; sp < NS; ++sp) {
                     const double th = S.E[F3Y0 + NS + sp][face];
                     en += S.amp[1 + sp][face] *
-                          (2.0 * kk - (NS > 1 ? fdiv(th, kappa, ykappa) : th / kappa));
+                          (2.0 * kk - fdiv(th, kappa, ykappa));
                 }
                 r = en;
             }

@@ -101,10 +101,15 @@ IGN_HD void roe_average3(double rho_l, const double* Yl, double Tl, double ul, d
     const double H = (wl * Hl + wr * Hr) * inv;
     const double h = H - 0.5 * ((u * u + v * v) + w * w);
     double Tt = 0.5 * (Tl + Tr);
+    // calorically perfect (TM 1): cp does not depend on T, so its reciprocal
+    // is formed once and every iteration's r / cp is a Markstein quotient
+    // (correctly rounded, IEEE fallback) instead of an IEEE division
+    const double cp1 = TM == 1 ? cp_mass<NS, false, TM>(Tt, Y, m) : 0.0;
+    const double ycp1 = TM == 1 ? 1.0 / cp1 : 0.0;
     for (int it = 0; it < 50; ++it) {
         const double r = h_mass<NS, false, TM>(Tt, Y, m) - h;
-        const double cp = cp_mass<NS, false, TM>(Tt, Y, m);
-        const double Tn = Tt - r / cp;
+        const double cp = TM == 1 ? cp1 : cp_mass<NS, false, TM>(Tt, Y, m);
+        const double Tn = Tt - (TM == 1 ? fdiv(r, cp, ycp1) : r / cp);
         if (fabs(Tn - Tt) <= 1e-14 * Tt) {
             Tt = Tn;
             break;
@@ -128,8 +133,10 @@ IGN_HD int eigen_at_state3(const double* Y, double T, double uu, double vv, doub
     if (DIR < 2) {
         e.s = sqrt(m1 * m1 + m2 * m2);
         if (!(e.s > 0.0)) return E_ZERO_METRIC;
-        e.n1 = m1 / e.s;
-        e.n2 = m2 / e.s;
+        // two quotients over one divisor: Markstein with the shared RN(1/s)
+        const double ys = 1.0 / e.s;
+        e.n1 = fdiv(m1, e.s, ys);
+        e.n2 = fdiv(m2, e.s, ys);
         e.n3 = 0.0;
         e.un = e.n1 * uu + e.n2 * vv;
         e.ut1 = -e.n2 * uu + e.n1 * vv;
