@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define IGN_ABI_VERSION 2
+#define IGN_ABI_VERSION 3
 #define IGN_MAX_SPECIES 8   /* thermo.hpp:16 kMaxSpecies */
 #define IGN_MAX_COMP 11     /* flux.hpp:14 kMaxComp */
 #define IGN_MAX_PIECES 4    /* polynomial ranges per species */
@@ -168,7 +168,8 @@ typedef struct {
      * nz > 0 extrudes the (x, y) mesh uniformly over lz in z.  Component order
      * then [rhoY_s, rho u, rho v, rho w, E]; primitive cache rho,u,v,w,p,T,c,Y;
      * the x / y edges take the reference's rules on every z plane, z is
-     * periodic (periodic_z = 1).  With slab_count > 1, 3D contexts split z. */
+     * periodic (periodic_z = 1) or bounded by zlo / zhi below.  With
+     * slab_count > 1, 3D contexts split z. */
     int32_t nz;
     int32_t periodic_z;
     int32_t _pad;
@@ -182,6 +183,12 @@ typedef struct {
      * compute_metrics of these coordinates (metrics.hpp:73-118). */
     const double* mesh_x;
     const double* mesh_y;
+    /* 3D extension: the z edges (back = k < 0, front = k >= nz) when
+     * periodic_z = 0 — no-slip walls (isothermal / adiabatic) or outflow, the
+     * reference's y-edge rules with w the wall-normal velocity; filled after
+     * the x and y edges, over the full padded (x, y) plane.  Ignored (must be
+     * periodic) when periodic_z = 1; inflow is not supported on z edges. */
+    ign_edge zlo, zhi;
 } ign_config;
 
 /* errors.hpp:29-35 StepFailure payload + message; k is the z plane of a 3D

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-IGN_ABI_VERSION = 2
+IGN_ABI_VERSION = 3
 IGN_MAX_SPECIES = 8
 IGN_MAX_COMP = 11
 IGN_MAX_PIECES = 4
@@ -115,7 +115,8 @@ class Config(C.Structure):
                 ("device", C.c_int32), ("slab_count", C.c_int32),
                 ("slab_rank", C.c_int32), ("nz", C.c_int32), ("periodic_z", C.c_int32),
                 ("_pad", C.c_int32), ("lz", C.c_double), ("center_z", C.c_double),
-                ("mesh_x", C.POINTER(C.c_double)), ("mesh_y", C.POINTER(C.c_double))]
+                ("mesh_x", C.POINTER(C.c_double)), ("mesh_y", C.POINTER(C.c_double)),
+                ("zlo", Edge), ("zhi", Edge)]
 
 
 class Error(C.Structure):

@@ -522,7 +522,7 @@ def tgv3d(n: int = 256, *, viscous: bool = True, scheme: str = "teno6",
 
 
 def jet3d(nx: int = 512, ny: int = 256, nz: int = 32, *, scheme: str = "weno3z",
-          split: str = "comp", energy: float = 0.05) -> Case:
+          split: str = "comp", energy: float = 0.05, zwalls: bool = False) -> Case:
     """BASELINE configs[3] in the form the 3D extension runs (SURVEY §8d config
     D; no reference path): an H2/N2 jet (tanh-smoothed inflow segment, 100 m/s)
     into air coflow (5 m/s) through a 4 cm x 2 cm channel — left inflow, right
@@ -530,11 +530,14 @@ def jet3d(nx: int = 512, ny: int = 256, nz: int = 32, *, scheme: str = "weno3z",
     periodic with dz = dx — one-step H2/O2 chemistry, the shaped laser kernel
     focused in the shear layer as a 3D point kernel (ign_laser.zmode 1);
     WENO3Z componentwise.  Weak
-    scaling stacks z: 512 x 256 x 32 per GPU, 512 x 256 x 256 on 8 GPUs."""
+    scaling stacks z: 512 x 256 x 32 per GPU, 512 x 256 x 256 on 8 GPUs.
+    zwalls: no-slip adiabatic walls on the z edges too (a confined duct)."""
     Lx, Ly = 0.04, 0.02
     dx = Lx / nx
     cfg = base_config(nx, ny, Lx, Ly, center=(0.5 * Lx, 0.0), periodic=(False, False))
-    cfg.nz, cfg.periodic_z, cfg.lz, cfg.center_z = nz, 1, dx * nz, 0.0
+    cfg.nz, cfg.periodic_z, cfg.lz, cfg.center_z = nz, int(not zwalls), dx * nz, 0.0
+    if zwalls:
+        cfg.zlo.type = cfg.zhi.type = abi.NOSLIP_ADIABATIC
     species = h2_o2_species()
     fill_mixture(cfg.mix, species)
     set_scheme(cfg, scheme, split)
@@ -589,7 +592,8 @@ def jet3d(nx: int = 512, ny: int = 256, nz: int = 32, *, scheme: str = "weno3z",
         return rho, u, np.zeros_like(X), w, T, Ys
 
     c_max = 1300.0  # sound speed bound of the H2/N2 jet at 300 K
-    return Case(f"jet3d_{nx}x{ny}x{nz}", cfg, ic, 0.3 * dx / (c_max + 100.0))
+    return Case(f"jet3d_{nx}x{ny}x{nz}" + ("_zw" if zwalls else ""), cfg, ic,
+                0.3 * dx / (c_max + 100.0))
 
 
 def extrude_z(case: Case, nz: int = 7) -> Case:
@@ -606,6 +610,32 @@ def extrude_z(case: Case, nz: int = 7) -> Case:
         return rho, u, v, np.zeros_like(X), T, Ys
 
     return Case(case.name + f"_z{nz}", cfg, ic, case.dt, dict(case.notes, ic2=ic2))
+
+
+def lay_xz(case: Case, ny: int = 7) -> Case:
+    """A 2D case laid in the (x, z) plane of a 3D box: the 2D y axis becomes z
+    (its edges — periodic, walls or outflow — become the z edges), y is
+    periodic with ny cells of dy = 1 and the data constant in y, v = 0.  Checks
+    the zeta-face kernels and the z-edge rules against the 2D oracle."""
+    c2 = case.cfg
+    cfg = abi.Config()
+    ctypes.memmove(ctypes.byref(cfg), ctypes.byref(c2), ctypes.sizeof(abi.Config))
+    cfg.ny, cfg.ly, cfg.center_y = ny, float(ny), 0.0
+    cfg.nz, cfg.lz, cfg.center_z, cfg.periodic_z = c2.ny, c2.ly, c2.center_y, c2.periodic_y
+    if not c2.periodic_y:
+        if abi.INFLOW in (c2.bc.bottom.type, c2.bc.top.type):
+            raise ValueError("lay_xz: inflow is not supported on z edges")
+        ctypes.memmove(ctypes.byref(cfg.zlo), ctypes.byref(c2.bc.bottom), ctypes.sizeof(abi.Edge))
+        ctypes.memmove(ctypes.byref(cfg.zhi), ctypes.byref(c2.bc.top), ctypes.sizeof(abi.Edge))
+        cfg.periodic_y = 1
+        cfg.bc.bottom.type = cfg.bc.top.type = abi.PERIODIC
+    ic2 = case.ic
+
+    def ic(X, Y, Z):
+        rho, u, v, T, Ys = ic2(X, Z)
+        return rho, u, np.zeros_like(X), v, T, Ys
+
+    return Case(case.name + f"_xz{ny}", cfg, ic, case.dt, dict(case.notes, ic2=ic2))
 
 
 def state_2d_to_3d(Ut2: np.ndarray, ns: int, nz: int, g: int = 3) -> np.ndarray:

@@ -235,6 +235,19 @@ void validate_config(const ign_config& c, const HMesh& mesh) {
     const bool py = c.bc.bottom.type == 0;
     if (py != (c.bc.top.type == 0) || py != mesh.periodic_y)
         throw config_error("boundary: periodic y edges must be paired and match the mesh");
+    if (c.nz > 0) {
+        // 3D extension: z edges are periodic (paired) or walls / outflow
+        const bool pz = c.periodic_z != 0;
+        if (pz && (c.zlo.type != 0 || c.zhi.type != 0))
+            throw config_error("boundary: periodic z needs periodic zlo / zhi edges");
+        for (const ign_edge* e : {&c.zlo, &c.zhi}) {
+            if (pz) continue;
+            if (e->type == 0)
+                throw config_error("boundary: periodic z edges must be paired and match periodic_z");
+            if (e->type == 3) throw usage_error("boundary: inflow is not supported on z edges");
+            if (e->type < 0 || e->type > 4) throw usage_error("boundary: unknown BC type");
+        }
+    }
     auto check_inflow = [&](const ign_edge& s, bool xedge) {
         if (s.type != 3) return;
         if (s.nseg <= 0) throw config_error("boundary: inflow edge needs segments");

@@ -3,7 +3,8 @@
 // (kernels.cuh) by the z terms on EXTRUDED meshes (2D reference metrics x
 // uniform z, flux3.cuh), appended after the reference's 2D expressions so the
 // z-extrusion cross-check reproduces the 2D oracle bit for bit.  Boundary
-// conditions: periodic in x, y, z (the TGV); other BCs are 2D-only for now.
+// conditions: the reference's 2D edge rules on x / y; z periodic, no-slip
+// walls or outflow.
 #pragma once
 
 #include "faces3d.cuh"
@@ -63,14 +64,49 @@ __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, 
     const int rem = tid - side * na * nb;
     const int a = a0 + rem % na, b = b0 + rem / na;
     const int n = pass == 0 ? P.nx : pass == 1 ? P.ny : P.nz;
-    if (pass == 2) {  // periodic z: the (x, y) metrics are z-independent
-        for (int k = 1; k <= g; ++k) {
-            const long long s = pidx3(P, a, b, side == 0 ? n - k : k - 1);
-            const long long d = pidx3(P, a, b, side == 0 ? -k : n - 1 + k);
-            const int q = (b + g) * P.sx + (a + g);
+    if (pass == 2) {
+        // z edges over the whole padded (x, y) plane, after the x / y edges
+        // (the reference's corner order: the last-filled edge wins)
+        const int type = P.bc_z[side];
+        if (type == BC_HALO) return;  // the peer slab's planes
+        const int q = (b + g) * P.sx + (a + g);
+        if (type == 0 || type == 4) {
+            // periodic (boundary.hpp:203-209) or outflow (boundary.hpp:242-249):
+            // scaled copies, the ratio J/J = 1 of the z-independent (x, y) metrics
             const double ratio = P.jac[q] / P.jac[q];
+            for (int k = 1; k <= g; ++k) {
+                const int ks = type == 0 ? (side == 0 ? n - k : k - 1) : (side == 0 ? 0 : n - 1);
+                const long long s = pidx3(P, a, b, ks);
+                const long long d = pidx3(P, a, b, side == 0 ? -k : n - 1 + k);
 #pragma unroll
-            for (int c = 0; c < NS + 4; ++c) Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+                for (int c = 0; c < NS + 4; ++c)
+                    Ut[c * P.plane + d] = Ut[c * P.plane + s] * ratio;
+            }
+            return;
+        }
+        // no-slip walls (boundary.hpp:210-226) with w the wall-normal velocity;
+        // keys after every x / y edge key of the whole box, (side, y, x, k) order
+        const unsigned long long zkey =
+            (unsigned long long)P.nz_glob * 4 * (P.nx + P.ny + 4 * g) * (g + 1) +
+            (((unsigned long long)side * (P.ny + 2 * g) + (b + g)) * (P.nx + 2 * g) + (a + g)) *
+                (g + 1);
+        for (int k = 1; k <= g; ++k) {
+            Prim3<NS> pt;
+            double rs;
+            const int st = bc3_prim_at<NS, TM>(P, Ut, a, b, side == 0 ? k - 1 : n - k, pt, rs);
+            if (st) {
+                report(P.err, stage, PH_BC, zkey + k, st, step);
+                return;
+            }
+            pt.u = -pt.u;
+            pt.v = -pt.v;
+            pt.w = -pt.w;
+            if (type == 1) {
+                const double tg = 2.0 * P.T_wall_z[side] - pt.T;
+                pt.T = smax(tg, 0.05 * P.T_wall_z[side]);
+            }
+            pt.rho = pt.p / (r_specific<NS>(pt.Y, P.mix) * pt.T);
+            bc3_store<NS, TM>(P, Ut, pt, a, b, side == 0 ? -k : n - 1 + k);
         }
         return;
     }
@@ -601,7 +637,7 @@ template <int NS> struct Launch3 {
             bc3_launch(P, Ut, 1, stage, step, (unsigned)((n1 + 127) / 128), s);
             return 2;
         }
-        if (P.zhalo) return 0;
+        if (P.bc_z[0] == BC_HALO && P.bc_z[1] == BC_HALO) return 0;
         const int n2 = 2 * (P.nx + 2 * g) * (P.ny + 2 * g);
         bc3_launch(P, Ut, 2, stage, step, (unsigned)((n2 + 127) / 128), s);
         return 1;

@@ -77,7 +77,10 @@ struct KParams {
     // 3D extension (extruded mesh; nz = 0 for 2D): z cells, state plane
     // stride, zeta metric (2D planes), z face fluxes, viscous z fluxes
     int32_t nz, nz_glob;
-    int32_t zhalo, _pad3;  // 3D z-slabs: z ghost planes come from the peers
+    int32_t zhalo;  // 3D z-slabs: some z ghost planes come from the peers
+    int32_t bc_z[2];  // 3D back / front edge: 0 periodic, 1/2 walls, 4 outflow, BC_HALO
+    int32_t _pad3;
+    double T_wall_z[2];
     long long sxy;
     const double *mzz, *vmzz;
     double *Hz, *Hv;

@@ -179,8 +179,8 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     if (three_d) {
         // 3D extension: the (x, y) mesh extruded over lz (flux3.cuh)
         if (!(cfg->lz > 0.0)) throw config_error("3D: lz must be positive");
-        // x / y edges take the reference's 2D rules on every z plane; z is periodic
-        if (!cfg->periodic_z) throw usage_error("3D: z must be periodic");
+        // x / y edges take the reference's 2D rules on every z plane; z is
+        // periodic or bounded by walls / outflow (cfg->zlo / zhi)
         int k0 = 0;
         slab_rows(cfg->nz, ctx->nranks, ctx->rank, k0, nz);
         if (nz < cfg->g) throw config_error("3D: every z-slab needs >= g planes");
@@ -395,6 +395,12 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     if (three_d) {
         k.j0 = ctx->k0;  // 3D: global z offset of the slab (error keys)
         k.zhalo = ctx->lo_peer >= 0 || ctx->hi_peer >= 0;
+        const ign_edge* ze[2] = {&cfg->zlo, &cfg->zhi};
+        const bool peer[2] = {ctx->lo_peer >= 0, ctx->hi_peer >= 0};
+        for (int side = 0; side < 2; ++side) {
+            k.bc_z[side] = peer[side] ? BC_HALO : cfg->periodic_z ? 0 : ze[side]->type;
+            k.T_wall_z[side] = ze[side]->T_wall;
+        }
     }
     k.sxy = static_cast<long long>(P2);
     k.Fx = ctx->Fx;

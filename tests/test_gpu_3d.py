@@ -8,9 +8,10 @@ z-extrusion cross-check of SURVEY §8c:
     to the sign of zero) for the gamma-gas cases, within the 2D multi-species
     tolerances otherwise — and bitwise equal to the 2D B200 path in all cases.
   * (x, z) extrusion: a 2D case laid in the x-z plane (v = 0, y-constant,
-    dy = 1) exercises the zeta-face kernel; equal to the 2D oracle within a
-    tolerance (the 2D oracle's y metrics carry ulp noise the uniform z
-    metrics do not).
+    dy = 1) exercises the zeta-face kernel and, for the wall channels, the
+    z-edge rules (the 2D y walls / outflow become z walls / outflow); equal to
+    the 2D oracle within a tolerance (the 2D oracle's y metrics carry ulp
+    noise the uniform z metrics do not).
   * The non-periodic x / y edges (walls, inflow, outflow with LODI) and the
     laser run the reference's 2D rules on every z plane: the same extrusion
     check covers them (wall, counterflow, Sod/LODI cases).
@@ -160,21 +161,13 @@ def test_extrusion_stable_dt_bounded(triple):
 
 # ----------------------------------------------------------------- x-z plane
 def _xz_pair(oracle_api, case2):
-    """A 2D case laid in the (x, z) plane of a 3D box: ny = 7 cells of dy = 1."""
-    c2 = case2.cfg
-    cfg3 = clone_cfg(c2)
-    cfg3.ny, cfg3.ly, cfg3.center_y = NZ, float(NZ), 0.0
-    cfg3.nz, cfg3.lz, cfg3.center_z, cfg3.periodic_z = c2.ny, c2.ly, c2.center_y, 1
-    ic2 = case2.ic
-
-    def ic3(X, Y, Z):
-        rho, u, v, T, Ys = ic2(X, Z)
-        return rho, u, np.zeros_like(X), v, T, Ys
-
-    refs = Simulation(clone_cfg(c2), oracle_api)
-    refs.set_initial_condition(ic2)
-    p3 = Simulation(cfg3)
-    p3.set_initial_condition(ic3)
+    """A 2D case laid in the (x, z) plane of a 3D box: ny = 7 cells of dy = 1
+    (configs.lay_xz; the 2D y edges become the z edges)."""
+    refs = Simulation(clone_cfg(case2.cfg), oracle_api)
+    refs.set_initial_condition(case2.ic)
+    c3 = configs.lay_xz(case2, NZ)
+    p3 = Simulation(c3.cfg)
+    p3.set_initial_condition(c3.ic)
     return refs, p3
 
 
@@ -190,11 +183,23 @@ def _state_scale(U, ns, g=3):
     return np.array([rho] * ns + [mom, mom, np.abs(b[ns + 2]).max()])
 
 
+def _wall_outflow():
+    """wall_channel with a zero-gradient outflow top edge (boundary.hpp:242-249)."""
+    case = configs.wall_channel(20)
+    case.cfg.bc.top.type = abi.OUTFLOW
+    return case
+
+
 @pytest.mark.parametrize("mk", [
     lambda: configs.tgv2d(24),
     lambda: configs.tgv2d(20, scheme="weno3z", split="comp"),
     lambda: configs.reacting_ch4(16, laser=False),
-], ids=["tgv_char_teno6", "tgv_comp_weno3z", "ch4_char"])
+    # the 2D y walls as z walls (isothermal back, adiabatic front)
+    lambda: configs.wall_channel(20),
+    lambda: configs.wall_channel(20, isothermal=False, scheme="weno3z", split="comp"),
+    lambda: _wall_outflow(),
+], ids=["tgv_char_teno6", "tgv_comp_weno3z", "ch4_char", "zwalls_isothermal",
+        "zwalls_adiabatic_weno3z", "zwall_zoutflow"])
 def test_xz_plane_matches_oracle(mk, oracle_api, cuda_device):
     case = mk()
     refs, p3 = _xz_pair(oracle_api, case)
@@ -492,3 +497,42 @@ def test_full_3d_faces_bitwise_vs_ref3d(name, oracle_api, cuda_device):
     assert np.abs(b[-2]).max() > 0.0  # the z momentum moves
     assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), \
         np.abs(a - b).max(axis=(1, 2, 3))
+
+
+def test_z_edge_validation(cuda_device):
+    """z edges: periodic_z needs periodic zlo / zhi, a bounded z needs walls or
+    outflow on both sides (inflow is not supported on z edges)."""
+    from paper_2202_02319_b200 import errors
+    bad = []
+    c = configs.jet3d(24, 12, 8, zwalls=True)
+    c.cfg.zhi.type = abi.PERIODIC
+    bad.append((c.cfg, errors.ConfigError))
+    c = configs.jet3d(24, 12, 8)
+    c.cfg.zlo.type = abi.NOSLIP_ADIABATIC
+    bad.append((c.cfg, errors.ConfigError))
+    c = configs.jet3d(24, 12, 8, zwalls=True)
+    c.cfg.zlo.type = abi.INFLOW
+    bad.append((c.cfg, errors.UsageError))
+    for cfg, exc in bad:
+        with pytest.raises(exc):
+            Simulation(cfg)
+
+
+def test_jet3d_zwalls_no_through_flow(cuda_device):
+    """configs[3] as a confined duct: with z walls the cache's w vanishes at
+    the wall faces (ghost w mirrors the first plane's), mass stays finite."""
+    case = configs.jet3d(48, 24, 12, zwalls=True)
+    sim = Simulation(case.cfg)
+    sim.set_initial_condition(case.ic)
+    sim.rk3_steps(case.dt, 20)
+    c = sim.cache()
+    g = 3
+    w = c["w"]
+    # ghost plane -k mirrors plane k-1 (both sides), so the face average is 0
+    scale = np.abs(w).max()
+    assert scale > 0.0
+    for k in range(1, g + 1):
+        assert np.abs(w[g - k] + w[g + k - 1]).max() <= 1e-13 * scale
+        assert np.abs(w[-g - 1 + k] + w[-g - k]).max() <= 1e-13 * scale
+    T = c["T"][g:-g, g:-g, g:-g]
+    assert np.isfinite(T).all() and T.min() > 250.0

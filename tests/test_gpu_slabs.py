@@ -88,6 +88,9 @@ CASES3 = {
     "h2o2_inflow_outflow_3d": lambda: configs.extrude_z(configs.h2o2_counterflow(12), 18),
     "wall_channel_3d": lambda: configs.extrude_z(configs.wall_channel(12), 18),
     "jet3d_inflow_lodi_walls_laser": lambda: configs.jet3d(48, 24, 12),
+    # z edges: walls on the end slabs' outer sides, no periodic ring
+    "jet3d_zwalls": lambda: configs.jet3d(48, 24, 12, zwalls=True),
+    "wall_channel_xz_zwalls": lambda: configs.lay_xz(configs.wall_channel(18), 7),
 }
 
 
