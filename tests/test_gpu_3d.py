@@ -524,6 +524,7 @@ def test_jet3d_zwalls_no_through_flow(cuda_device):
     case = configs.jet3d(48, 24, 12, zwalls=True)
     sim = Simulation(case.cfg)
     sim.set_initial_condition(case.ic)
+    sim.prepare_stage(1)
     sim.rk3_steps(case.dt, 20)
     c = sim.cache()
     g = 3
