@@ -101,7 +101,8 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     // load's latency hides behind the window staging (garbage phase-1 reports
     // carry larger keys than the first one)
     __shared__ int s_dead;
-    const bool dead0 = threadIdx.x == 0 && failed(P.err);
+    const bool dead0 =
+        threadIdx.x == 0 && failed_before(P.err, step, stage, DIR == 0 ? PH_INVX : PH_INVY);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long step_n = DIR == 0 ? 1 : P.sx;

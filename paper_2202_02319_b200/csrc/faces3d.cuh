@@ -115,7 +115,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     // load's latency hides behind the window staging instead of stalling the
     // CTA start (garbage phase-1 reports carry larger keys than the first one)
     __shared__ int s_dead;
-    const bool dead0 = threadIdx.x == 0 && failed(P.err);
+    const bool dead0 =
+        threadIdx.x == 0 && failed_before(P.err, step, stage, DIR == 0 ? PH_INVX : PH_INVY);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // DIR 0: NF consecutive faces of the flattened (row, f) order, row = k ny + j,

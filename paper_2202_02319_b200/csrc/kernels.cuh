@@ -62,7 +62,7 @@ __device__ void bc_copy_scaled(const KParams& P, double* Ut, int is, int js, int
 template <int NS, int TM>
 __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, double* Ut,
                                             int ypass, int stage, int step) {
-    if (failed(P.err)) return;
+    if (failed_before(P.err, step, stage, PH_BC)) return;
     const int g = P.g, nx = P.nx, ny = P.ny;
     const int tlo = ypass ? -g : 0;
     const int ntr = ypass ? nx + 2 * g : ny;
@@ -174,7 +174,7 @@ template <int NS, bool WX, int TM>
 __global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim(const __grid_constant__ KParams P,
                                               const double* __restrict__ Ut, int stage,
                                               int step, long long id_lo, long long id_hi) {
-    if (failed(P.err)) return;
+    if (failed_before(P.err, step, stage, PH_PRIM)) return;
     const long long id = id_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= id_hi) return;
     const double J = P.jac[id];
@@ -217,7 +217,7 @@ template <int NS, int TM>
 __global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : NS == 1 ? IGN_VISC1_MINB : 1) k_visc(const __grid_constant__ KParams P, int stage,
                                               int step) {
     constexpr int NC = NS + 3;
-    if (failed(P.err)) return;
+    if (failed_before(P.err, step, stage, PH_RHS)) return;
     const int w = P.nx + 2;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)w * (P.ny + 2)) return;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256, (NS > 1 && NS <= 4) ? 4 : 1) k_assemble(c
     __shared__ unsigned long long s_clip;
     if (threadIdx.x == 0) s_clip = 0ull;
     __syncthreads();
-    const bool dead = failed(P.err);
+    const bool dead = failed_before(P.err, step, stage, PH_RHS);
     long long id;
     bool in_range;
     if (EDGE) {

@@ -53,7 +53,7 @@ __device__ void bc3_copy_scaled(const KParams& P, double* Ut, int is, int js, in
 template <int NS, int TM>
 __global__ void __launch_bounds__(128) k_bc3(const __grid_constant__ KParams P, double* Ut,
                                              int pass, int stage, int step) {
-    if (failed(P.err)) return;
+    if (failed_before(P.err, step, stage, PH_BC)) return;
     const int g = P.g;
     const int na = pass == 0 ? P.ny : P.nx + 2 * g;        // first transverse index
     const int nb = pass == 2 ? P.ny + 2 * g : P.nz;       // second
@@ -202,7 +202,7 @@ template <int NS, bool WX, int TM>
 __global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim3(const __grid_constant__ KParams P,
                                                const double* __restrict__ Ut, int stage,
                                                int step, int k_lo) {
-    if (failed(P.err)) return;
+    if (failed_before(P.err, step, stage, PH_PRIM)) return;
     const int id2 = blockIdx.x * blockDim.x + threadIdx.x;  // (x, y) plane index
     if (id2 >= P.sxy) return;
     const long long id = (long long)(blockIdx.y + k_lo) * P.sxy + id2;  // padded k
@@ -237,21 +237,13 @@ __global__ void __launch_bounds__(256, NS <= 4 ? 4 : 1) k_prim3(const __grid_con
 
 // ---------------------------------------------------------------- viscous
 // compute_viscous (solver.hpp:610-696) with the z gradient, z stresses and
-// the zeta flux appended after the reference's 2D terms
-// 2-4 species: 6 CTAs/SM (<= 85 registers, a small spill) hide more of the
-// stencil loads' latency (jet visc3 -6.5%); the gamma-gas keeps 122 registers
+// the zeta flux appended after the reference's 2D terms: the mapped node
+// fluxes (Fv, Gv, Hv) of node (i, j, k)
 template <int NS, int TM>
-#ifndef IGN_VISC1_MINB
-#define IGN_VISC1_MINB 8  // one species: 8 CTAs/SM (64 registers, small spill) -4% viscous
-#endif
-__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : NS == 1 ? IGN_VISC1_MINB : 1) k_visc3(const __grid_constant__ KParams P, int stage,
-                                               int step) {
+__device__ __forceinline__ void visc_node3(const KParams& P, int i, int j, int k,
+                                           double* __restrict__ Fo, double* __restrict__ Go,
+                                           double* __restrict__ Ho) {
     constexpr int NC = NS + 4;
-    if (failed(P.err)) return;
-    const long long wx = P.nx + 2, wy = P.ny + 2;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= wx * wy * (P.nz + 2)) return;
-    const int i = (int)(t % wx) - 1, j = (int)((t / wx) % wy) - 1, k = (int)(t / (wx * wy)) - 1;
     const long long id = pidx3(P, i, j, k), id2 = id % P.sxy;
     auto ddxi = [&](const double* f) { return 0.5 * (ldg(f + id + 1) - ldg(f + id - 1)); };
     auto ddeta = [&](const double* f) { return 0.5 * (ldg(f + id + P.sx) - ldg(f + id - P.sx)); };
@@ -330,9 +322,34 @@ __global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : NS == 1 ? IGN_V
     const double c2 = ldg(P.vmex + id2), d = ldg(P.vmey + id2), e = ldg(P.vmzz + id2);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        P.Fv[c * P.plane + id] = a * Fd[c] + b * Gd[c];
-        P.Gv[c * P.plane + id] = c2 * Fd[c] + d * Gd[c];
-        P.Hv[c * P.plane + id] = e * Hd[c];
+        Fo[c] = a * Fd[c] + b * Gd[c];
+        Go[c] = c2 * Fd[c] + d * Gd[c];
+        Ho[c] = e * Hd[c];
+    }
+}
+
+// 2-4 species: 6 CTAs/SM (<= 85 registers, a small spill) hide more of the
+// stencil loads' latency (jet visc3 -6.5%); the gamma-gas keeps 122 registers
+template <int NS, int TM>
+#ifndef IGN_VISC1_MINB
+#define IGN_VISC1_MINB 8  // one species: 8 CTAs/SM (64 registers, small spill) -4% viscous
+#endif
+__global__ void __launch_bounds__(128, (NS > 1 && NS <= 4) ? 6 : NS == 1 ? IGN_VISC1_MINB : 1) k_visc3(const __grid_constant__ KParams P, int stage,
+                                               int step) {
+    constexpr int NC = NS + 4;
+    if (failed_before(P.err, step, stage, PH_RHS)) return;
+    const long long wx = P.nx + 2, wy = P.ny + 2;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= wx * wy * (P.nz + 2)) return;
+    const int i = (int)(t % wx) - 1, j = (int)((t / wx) % wy) - 1, k = (int)(t / (wx * wy)) - 1;
+    const long long id = pidx3(P, i, j, k);
+    double F[NC], G[NC], H[NC];
+    visc_node3<NS, TM>(P, i, j, k, F, G, H);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        P.Fv[c * P.plane + id] = F[c];
+        P.Gv[c * P.plane + id] = G[c];
+        P.Hv[c * P.plane + id] = H[c];
     }
 }
 
@@ -415,6 +432,73 @@ static __device__ __noinline__ double laser_cold(double x, double y, double z, d
     return laser_power3(x, y, z, t, p);
 }
 
+// The rest of the update of interior node (i, j, k) once its flux
+// differences r are summed: compute_rhs's source terms and finite check
+// (solver.hpp:422-439), then the RK3 blend with post_stage's clip / validate
+// (solver.hpp:304-332, state.hpp:94-121) — or r itself for MODE 0.
+template <int NS, int MODE>
+__device__ __forceinline__ void finish_node3(const KParams& P, const double* __restrict__ U0,
+                                             const double* __restrict__ Ucur,
+                                             double* __restrict__ Uout, long long id, int i, int j,
+                                             int k, double (&r)[NS + 4], double dt, double w,
+                                             double t_stage, int stage, int step, double& clip) {
+    constexpr int NC = NS + 4;
+    const double J = ldg(P.jac + id % P.sxy);
+    const double invJ = 1.0 / J;
+    if (P.mech.present) {
+        double Y[NS], wdot[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) Y[s] = ldg(PY3(P, s) + id);
+        source_terms<NS>(ldg(PRHO3(P) + id), ldg(PT3(P) + id), Y, P.mix, P.mech, wdot);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
+    }
+    // laser_power (laser.hpp:88-91) of the node's (x, y) — the
+    // reference's 2D kernel on every plane — or the 3D point kernel
+    // (laser_power3, zmode 1) at the node's z
+    if (P.laser.on) {
+        const int q = (j + P.g) * P.sx + (i + P.g);
+        const double z = P.zc0 + ((k + P.j0) + 0.5) * P.dz;
+        r[NS + 3] +=
+            laser_cold(ldg(P.xc + q), ldg(P.yc + q), z, t_stage, P.laser) * invJ;
+    }
+    const unsigned long long cell =
+        ((unsigned long long)(k + P.j0) * P.ny + j) * P.nx + i;
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) bad |= !isfinite(r[c]);
+    if (bad) {
+        report(P.err, stage, PH_RHS, cell, 0, step);
+    } else if (MODE == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = r[c];
+    } else {
+        double o[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double b = U0[c * P.plane + id];
+            if (MODE == 1) o[c] = b + dt * r[c];
+            else o[c] = b + w * ((Ucur[c * P.plane + id] - b) + dt * r[c]);
+        }
+        double rsum = 0.0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (o[s] < 0.0) {
+                clip = smax(clip, -o[s] * J);
+                o[s] = 0.0;
+            }
+            rsum += o[s];
+        }
+        bool fin = true;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) fin &= isfinite(o[c]);
+        if (!(rsum > 0.0)) report(P.err, stage, PH_POST, cell * 2, 0, step);
+        else if (!fin) report(P.err, stage, PH_POST, cell * 2 + 1, 0, step);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = o[c];
+    }
+}
+
 // EDGE = false: every padded node except, when LODI is on, the right-edge
 // column; EDGE = true: that column alone (grid over its (j, k)), with the LODI
 // x-flux difference — so the LODI code never enters the bulk update.
@@ -429,7 +513,7 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
     __shared__ unsigned long long s_clip;
     if (threadIdx.x == 0) s_clip = 0ull;
     __syncthreads();
-    const bool dead = failed(P.err);
+    const bool dead = failed_before(P.err, step, stage, PH_RHS);
     long long id;
     bool in_range;
     if (EDGE) {
@@ -483,60 +567,8 @@ __global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KPara
                     r[c] += (dVx + dVy) + dVz;
                 }
             }
-            const double J = ldg(P.jac + id % P.sxy);
-            const double invJ = 1.0 / J;
-            if (P.mech.present) {
-                double Y[NS], wdot[NS];
-#pragma unroll
-                for (int s = 0; s < NS; ++s) Y[s] = ldg(PY3(P, s) + id);
-                source_terms<NS>(ldg(PRHO3(P) + id), ldg(PT3(P) + id), Y, P.mix, P.mech, wdot);
-#pragma unroll
-                for (int s = 0; s < NS; ++s) r[s] += wdot[s] * invJ;
-            }
-            // laser_power (laser.hpp:88-91) of the node's (x, y) — the
-            // reference's 2D kernel on every plane — or the 3D point kernel
-            // (laser_power3, zmode 1) at the node's z
-            if (P.laser.on) {
-                const int q = (j + P.g) * P.sx + (i + P.g);
-                const double z = P.zc0 + ((k + P.j0) + 0.5) * P.dz;
-                r[NS + 3] +=
-                    laser_cold(ldg(P.xc + q), ldg(P.yc + q), z, t_stage, P.laser) * invJ;
-            }
-            const unsigned long long cell =
-                ((unsigned long long)(k + P.j0) * P.ny + j) * P.nx + i;
-            bool bad = false;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) bad |= !isfinite(r[c]);
-            if (bad) {
-                report(P.err, stage, PH_RHS, cell, 0, step);
-            } else if (MODE == 0) {
-#pragma unroll
-                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = r[c];
-            } else {
-                double o[NC];
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const double b = U0[c * P.plane + id];
-                    if (MODE == 1) o[c] = b + dt * r[c];
-                    else o[c] = b + w * ((Ucur[c * P.plane + id] - b) + dt * r[c]);
-                }
-                double rsum = 0.0;
-#pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    if (o[s] < 0.0) {
-                        clip = smax(clip, -o[s] * J);
-                        o[s] = 0.0;
-                    }
-                    rsum += o[s];
-                }
-                bool fin = true;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) fin &= isfinite(o[c]);
-                if (!(rsum > 0.0)) report(P.err, stage, PH_POST, cell * 2, 0, step);
-                else if (!fin) report(P.err, stage, PH_POST, cell * 2 + 1, 0, step);
-#pragma unroll
-                for (int c = 0; c < NC; ++c) Uout[c * P.plane + id] = o[c];
-            }
+            finish_node3<NS, MODE>(P, U0, Ucur, Uout, id, i, j, k, r, dt, w, t_stage, stage,
+                                   step, clip);
         }
     }
     if (MODE != 0) {

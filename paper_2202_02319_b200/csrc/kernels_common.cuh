@@ -41,6 +41,18 @@ __device__ __forceinline__ bool failed(const ErrRec* e) {
     return *reinterpret_cast<const volatile unsigned long long*>(&e->key) != kNoError;
 }
 
+// A failure recorded by an EARLIER (step, stage, phase) than the caller's:
+// kernels stop on those only.  A failure of their own phase must not stop
+// them, or a CTA that starts after another CTA's report would miss a smaller
+// key (the reference's first failure in row-major order) of the same phase.
+__device__ __forceinline__ bool failed_before(const ErrRec* e, int step, int stage,
+                                              unsigned phase) {
+    const unsigned long long first = ((unsigned long long)(step & 0xFFFFF) << 44) |
+                                     ((unsigned long long)stage << 41) |
+                                     ((unsigned long long)phase << 38);
+    return *reinterpret_cast<const volatile unsigned long long*>(&e->key) < first;
+}
+
 __device__ __forceinline__ void report(ErrRec* e, unsigned stage, unsigned phase,
                                        unsigned long long idx, unsigned sub, int step) {
     const unsigned long long key = ((unsigned long long)(step & 0xFFFFF) << 44) |
@@ -119,7 +131,7 @@ struct KernelAttrError : std::runtime_error {
 
 template <class Kern>
 inline void configure_kernel(Kern kern, size_t smem, int warps, std::atomic<unsigned long long>& mask,
-                             const char* name) {
+                             const char* name, int carveout = cudaSharedmemCarveoutMaxShared) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) throw KernelAttrError("cudaGetDevice failed");
     const unsigned long long bit = 1ull << (dev & 63);
@@ -127,7 +139,7 @@ inline void configure_kernel(Kern kern, size_t smem, int warps, std::atomic<unsi
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
+                                 carveout);
     if (e != cudaSuccess)
         throw KernelAttrError(std::string(name) + ": cudaFuncSetAttribute: " + cudaGetErrorString(e));
     if (std::getenv("IGN_DEBUG_OCC")) {
