@@ -382,7 +382,9 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 const int t = tile_node<DIR, W>(g, lane, k, L0);
                 const double unk = n1 * S.u[t] + n2 * S.v[t];
                 const double ck = S.c[t];
-                const double lam = es * (kind == 0 ? unk + -1.0 * ck : kind == 2 ? unk + ck : unk);
+                // kind is warp-uniform: the selects pick one expression
+                const double lam = kind == 0 ? es * (unk + -1.0 * ck)
+                                 : kind == 2 ? es * (unk + ck) : es * unk;
                 alpha = smax(alpha, fabs(lam));
             }
             S.alpha[kind][lane] = alpha;
@@ -412,12 +414,11 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
             const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
             double lf[W], lu[W];
-            // Row fl of EigenSystem::project (flux.hpp:116-119) in ONE code path
-            // for every field kind (all NC warps of the CTA share the
-            // instructions): acoustic  w = (dp -+ c dun) / (2c^2), written as
-            // dp + s*(c dun) with s = -+1 (exact negation); species
-            // w = q_s - Y_s dp / c^2; shear w = dut.  The 2W quotients share one
-            // validity flag (one branch, exact redo on the rare failure).
+            // Row fl of EigenSystem::project (flux.hpp:116-119), one
+            // warp-uniform branch per field kind: acoustic w = (dp -+ c dun) /
+            // (2c^2), written as dp + s*(c dun) with s = -+1 (exact negation);
+            // species w = q_s - Y_s dp / c^2; shear w = dut.  The 2W quotients
+            // share one validity flag (one branch, exact redo on the rare failure).
             const bool ac = fl == 0 || fl == NC - 1, sh = fl == NC - 2;
             const int sp_i = ac || sh ? 0 : fl - 1;
             const double sgn = fl == 0 ? -1.0 : 1.0;
@@ -429,39 +430,45 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                     lf[k] = S.L[2 * k][2][lane];
                     lu[k] = S.L[2 * k + 1][2][lane];
                 }
-            } else {
+            } else if (ac) {
+                // acoustic fields: w = (dp -+ c dun) / (2c^2) as dp + s (c dun)
+                // (warp-uniform branch: no selects, no unused products)
                 unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    const int t = tile_node<DIR, W>(g, lane, k, L0);
-#pragma unroll
-                    for (int vu = 0; vu < 2; ++vu) {
-                        const int vec = 2 * k + vu;
-                        const double dp = S.L[vec][0][lane];
-                        const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                        const double fd = fdiv_pos_try(num, den, yden, bad);
-                        const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
-                        const double w = ac ? fd : qs - fd;
-                        if (vu) lu[k] = w;
-                        else lf[k] = w;
-                    }
+                for (int vec = 0; vec < NV; ++vec) {
+                    const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
+                    const double fd = fdiv_pos_try(num, den, yden, bad);
+                    if (vec & 1) lu[vec >> 1] = fd;
+                    else lf[vec >> 1] = fd;
                 }
                 if (bad) {  // exact redo (rare): plain IEEE quotients
 #pragma unroll
-                    for (int k = 0; k < W; ++k) {
-                        const int t = tile_node<DIR, W>(g, lane, k, L0);
+                    for (int vec = 0; vec < NV; ++vec) {
+                        const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
+                        const double fd = div_cold(num, den);
+                        if (vec & 1) lu[vec >> 1] = fd;
+                        else lf[vec >> 1] = fd;
+                    }
+                }
+            } else {
+                // species fields: w = q_s - Y_s dp / c^2
+                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
-                        for (int vu = 0; vu < 2; ++vu) {
-                            const int vec = 2 * k + vu;
-                            const double dp = S.L[vec][0][lane];
-                            const double num =
-                                ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                            const double fd = div_cold(num, den);
-                            const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
-                            const double w = ac ? fd : qs - fd;
-                            if (vu) lu[k] = w;
-                            else lf[k] = w;
-                        }
+                for (int vec = 0; vec < NV; ++vec) {
+                    const int t = tile_node<DIR, W>(g, lane, vec >> 1, L0);
+                    const double fd = fdiv_pos_try(Ys * S.L[vec][0][lane], den, yden, bad);
+                    const double w = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
+                    if (vec & 1) lu[vec >> 1] = w;
+                    else lf[vec >> 1] = w;
+                }
+                if (bad) {  // exact redo (rare): plain IEEE quotients
+#pragma unroll
+                    for (int vec = 0; vec < NV; ++vec) {
+                        const int t = tile_node<DIR, W>(g, lane, vec >> 1, L0);
+                        const double fd = div_cold(Ys * S.L[vec][0][lane], den);
+                        const double w = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
+                        if (vec & 1) lu[vec >> 1] = w;
+                        else lf[vec >> 1] = w;
                     }
                 }
             }

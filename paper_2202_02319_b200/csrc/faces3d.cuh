@@ -103,7 +103,7 @@ __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
 #endif
 template <int NS, int DIR, bool TENO, bool CHAR, int TM>
 __global__ void __launch_bounds__(32 * (NS + 4),
-                                  NS != 1 ? 1 : DIR == 2 ? IGN_F3_MINB : DIR == 0 ? IGN_F3X_MINB : 1)
+                                  NS != 1 ? 1 : DIR == 0 ? IGN_F3X_MINB : IGN_F3_MINB)
 k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
           int f_lo, int f_hi) {
     using Smem = FaceSmem3<NS, DIR, TENO, CHAR>;
@@ -115,8 +115,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     // load's latency hides behind the window staging instead of stalling the
     // CTA start (garbage phase-1 reports carry larger keys than the first one)
     __shared__ int s_dead;
-    const bool dead0 =
-        threadIdx.x == 0 && failed_before(P.err, step, stage, DIR == 0 ? PH_INVX : PH_INVY);
+    const unsigned long long key0 = threadIdx.x == 0 ? err_key(P.err) : kNoError;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // DIR 0: NF consecutive faces of the flattened (row, f) order, row = k ny + j,
@@ -200,12 +199,14 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         return ((long long)f * P.ny + jb) * P.nx + col;
     };
     const long long il = node(my_f - 1, my_col), ir = il + step_n;
-    double m1f = 0.0, m2f = 0.0;
+    // face metrics: the four loads are issued here, combined after the window
+    // staging (their latency hides behind it)
+    double m1l = 0.0, m1r = 0.0, m2l = 0.0, m2r = 0.0;
     if (my_active) {
         const int l2 = node2(my_f - 1, my_col);
         const int r2 = DIR == 0 ? l2 + 1 : DIR == 1 ? l2 + P.sx : l2;
-        m1f = 0.5 * (ldg(m1a + l2) + ldg(m1a + r2));
-        m2f = 0.5 * (ldg(m2a + l2) + ldg(m2a + r2));
+        m1l = ldg(m1a + l2), m1r = ldg(m1a + r2);
+        m2l = ldg(m2a + l2), m2r = ldg(m2a + r2);
     }
     // this thread's face state, loaded before the window staging so the
     // global-load latency overlaps it (phase 1 consumes it after the loop)
@@ -334,6 +335,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         }
     }
 
+    const double m1f = 0.5 * (m1l + m1r), m2f = 0.5 * (m2l + m2r);
     if (CHAR) {
         int bad = 0;
         if (my_active) {
@@ -368,7 +370,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         }
         S.bad[threadIdx.x] = my_active ? bad : 1;
     }
-    if (threadIdx.x == 0) s_dead = dead0;
+    if (threadIdx.x == 0) s_dead = key0 < err_first(step, stage, DIR == 0 ? PH_INVX : PH_INVY);
     __syncthreads();
     if (s_dead) return;
     if (!CHAR) {
@@ -450,7 +452,9 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 const double unk =
                     DIR < 2 ? n1 * S.vel[0][t] + n2 * S.vel[DIR < 2][t] : n3 * S.vel[0][t];
                 const double ck = S.c[t];
-                const double lam = es * (kind == 0 ? unk + -1.0 * ck : kind == 2 ? unk + ck : unk);
+                // kind is warp-uniform: the selects pick one expression
+                const double lam = kind == 0 ? es * (unk + -1.0 * ck)
+                                 : kind == 2 ? es * (unk + ck) : es * unk;
                 alpha = smax(alpha, fabs(lam));
             }
             S.alpha[kind][lane] = alpha;
@@ -498,39 +502,45 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                     lf[k] = S.L[2 * k][sh1 ? 2 : 3][lane];
                     lu[k] = S.L[2 * k + 1][sh1 ? 2 : 3][lane];
                 }
-            } else {
+            } else if (ac) {
+                // acoustic fields: w = (dp -+ c dun) / (2c^2) as dp + s (c dun)
+                // (warp-uniform branch: no selects, no unused products)
                 unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    const int t = tile_node3<DIR, W>(g, lane, k, L0);
-#pragma unroll
-                    for (int vu = 0; vu < 2; ++vu) {
-                        const int vec = 2 * k + vu;
-                        const double dp = S.L[vec][0][lane];
-                        const double num = ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                        const double fd = fdiv_pos_try(num, den, yden, bad);
-                        const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
-                        const double wv = ac ? fd : qs - fd;
-                        if (vu) lu[k] = wv;
-                        else lf[k] = wv;
-                    }
+                for (int vec = 0; vec < NV; ++vec) {
+                    const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
+                    const double fd = fdiv_pos_try(num, den, yden, bad);
+                    if (vec & 1) lu[vec >> 1] = fd;
+                    else lf[vec >> 1] = fd;
                 }
                 if (bad) {
 #pragma unroll
-                    for (int k = 0; k < W; ++k) {
-                        const int t = tile_node3<DIR, W>(g, lane, k, L0);
+                    for (int vec = 0; vec < NV; ++vec) {
+                        const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
+                        const double fd = div_cold(num, den);
+                        if (vec & 1) lu[vec >> 1] = fd;
+                        else lf[vec >> 1] = fd;
+                    }
+                }
+            } else {
+                // species fields: w = q_s - Y_s dp / c^2
+                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
 #pragma unroll
-                        for (int vu = 0; vu < 2; ++vu) {
-                            const int vec = 2 * k + vu;
-                            const double dp = S.L[vec][0][lane];
-                            const double num =
-                                ac ? dp + sgn * (ec * S.L[vec][1][lane]) : Ys * dp;
-                            const double fd = div_cold(num, den);
-                            const double qs = vu ? S.U[sp_i][t] : S.F[sp_i][t];
-                            const double wv = ac ? fd : qs - fd;
-                            if (vu) lu[k] = wv;
-                            else lf[k] = wv;
-                        }
+                for (int vec = 0; vec < NV; ++vec) {
+                    const int t = tile_node3<DIR, W>(g, lane, vec >> 1, L0);
+                    const double fd = fdiv_pos_try(Ys * S.L[vec][0][lane], den, yden, bad);
+                    const double wv = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
+                    if (vec & 1) lu[vec >> 1] = wv;
+                    else lf[vec >> 1] = wv;
+                }
+                if (bad) {
+#pragma unroll
+                    for (int vec = 0; vec < NV; ++vec) {
+                        const int t = tile_node3<DIR, W>(g, lane, vec >> 1, L0);
+                        const double fd = div_cold(Ys * S.L[vec][0][lane], den);
+                        const double wv = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
+                        if (vec & 1) lu[vec >> 1] = wv;
+                        else lf[vec >> 1] = wv;
                     }
                 }
             }

@@ -45,12 +45,20 @@ __device__ __forceinline__ bool failed(const ErrRec* e) {
 // kernels stop on those only.  A failure of their own phase must not stop
 // them, or a CTA that starts after another CTA's report would miss a smaller
 // key (the reference's first failure in row-major order) of the same phase.
+__device__ __forceinline__ unsigned long long err_first(int step, int stage, unsigned phase) {
+    return ((unsigned long long)(step & 0xFFFFF) << 44) | ((unsigned long long)stage << 41) |
+           ((unsigned long long)phase << 38);
+}
 __device__ __forceinline__ bool failed_before(const ErrRec* e, int step, int stage,
                                               unsigned phase) {
-    const unsigned long long first = ((unsigned long long)(step & 0xFFFFF) << 44) |
-                                     ((unsigned long long)stage << 41) |
-                                     ((unsigned long long)phase << 38);
-    return *reinterpret_cast<const volatile unsigned long long*>(&e->key) < first;
+    return *reinterpret_cast<const volatile unsigned long long*>(&e->key) <
+           err_first(step, stage, phase);
+}
+// A snapshot of the word (L2, not L1: other CTAs report into it) whose
+// comparison can be deferred past other work — the face kernels compare it
+// after their window staging, so its latency is hidden
+__device__ __forceinline__ unsigned long long err_key(const ErrRec* e) {
+    return __ldcg(&e->key);
 }
 
 __device__ __forceinline__ void report(ErrRec* e, unsigned stage, unsigned phase,
