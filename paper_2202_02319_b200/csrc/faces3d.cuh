@@ -1,6 +1,6 @@
 // faces3d.cuh — inviscid face fluxes of the 3D extension (extruded meshes,
 // flux3.cuh).  Same CTA organisation as faces.cuh: NC = ns+4 warps own
-// 32*NC faces (x: along a row; y/z: 32 columns x NC face lines), the node
+// 32*NC faces (x: along a row; y/z: 8 columns x 4NC face lines), the node
 // window lives in shared memory, warp w evaluates characteristic field w.
 #pragma once
 
@@ -18,6 +18,9 @@ __device__ __forceinline__ long long pidx3(const KParams& P, int i, int j, int k
     return (long long)(k + P.g) * P.sxy + (long long)(j + P.g) * P.sx + (i + P.g);
 }
 
+// y/z tile width (columns): see FaceSmem3::TW
+template <int DIR> __host__ __device__ constexpr int tile_w3() { return DIR == 0 ? 32 : 8; }
+
 // CHAR = false (componentwise) needs only the node window and one LLF speed
 // per face: the characteristic tables shrink to one row so more CTAs fit
 template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
@@ -25,8 +28,12 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;
+    // y/z tiles: TW columns x NF/TW face lines (a narrow tile keeps the
+    // window's halo lines few: 4 CTAs/SM fit)
+    static constexpr int TW = tile_w3<DIR>();
+    static constexpr int LINES = NF / TW;
     // x: up to two row segments of the flattened face order (see k_faces3d)
-    static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
+    static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : TW * (LINES + W - 1);
     // eigen table rows: 10 common + Y, Theta + the direction's own (n1, n2
     // for xi/eta faces; n3 for zeta faces — the others are 0 or alias u, v, w;
     // un, ut1 and k are recomputed by the eigensystem's own expressions)
@@ -42,8 +49,10 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     double vel[NVEL][NT];
     double c[NT];
     double E[NE][NF];
-    double L[NV_S][4][32];  // dp, dun, dut1, dut2
-    double amp[NA_S][NF];
+    // characteristic values of one group's stencil vectors, every field:
+    // row fl of L F and L U (EigenSystem::project, flux.hpp:107-119 + z terms)
+    double Wc[NV_S][NA_S][32];
+    double amp[NA_S][32];  // one group (phase 3 follows each group)
     double alpha[NK_S][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
     unsigned char bad[NF];
 };
@@ -79,22 +88,22 @@ template <int NS, int DIR> struct ERow {
     }
 };
 
-// window slot of stencil node k of face (g, lane); x faces past the first row
-// segment (q >= L0) sit W-1 slots further (their segment's own halo)
+// window slot of stencil node k of face slot q = 32 g + lane; x faces past the
+// first row segment (q >= L0) sit W-1 slots further (their segment's own
+// halo); y/z: slot q is column q % TW of face line q / TW, its node k lies k
+// lines further
 template <int DIR, int W>
 __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
-    if (DIR == 0) {
-        const int q = g * 32 + lane;
-        return q + k + (q >= L0 ? W - 1 : 0);
-    }
-    return (g + k) * 32 + lane;
+    const int q = g * 32 + lane;
+    if (DIR == 0) return q + k + (q >= L0 ? W - 1 : 0);
+    return q + k * tile_w3<DIR>();
 }
 
 // Registers: a 5-warp CTA needs <= 128 per thread for 3 CTAs/SM (4 warps per
 // SM sub-partition: 4 x 32 x 128 = 16384, the sub-partition's file); at 130
 // the z kernel drops to 2 CTAs/SM and runs ~30% slower.  __maxnreg__ pins it.
 #ifndef IGN_F3_MINB
-#define IGN_F3_MINB 3
+#define IGN_F3_MINB 4
 #endif
 // xi faces (55 KB shared): 4 CTAs/SM at <= 96 registers beat 3 CTAs without
 // the small spill (-1.2% faces, 256^3); eta/zeta (67-71 KB) stay at 3
@@ -120,8 +129,9 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // DIR 0: NF consecutive faces of the flattened (row, f) order, row = k ny + j,
     // f = 0..nx — at most two row segments when nx+1 >= NF (no idle lanes at row
-    // ends), else one row segment per CTA; DIR 1: 32 columns i x NC face rows
-    // along j in plane k; DIR 2: 32 columns i of row j x NC face planes along k
+    // ends), else one row segment per CTA; DIR 1: TW columns i x NF/TW face
+    // rows along j in plane k; DIR 2: TW columns i of row j x NF/TW face planes
+    // along k
     const long long step_n = DIR == 0 ? 1 : DIR == 1 ? P.sx : P.sxy;
     const int nd = DIR == 0 ? P.nx : DIR == 1 ? P.ny : P.nz;  // cells along DIR
     const int nrows = P.ny * P.nz;
@@ -138,9 +148,10 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         }
     } else {
         // faces [f_lo, f_hi) along DIR (a z-slab splits interior and halo faces)
-        f0 = f_lo + (DIR == 1 ? blockIdx.y : blockIdx.z) * NC;
+        f0 = f_lo + (DIR == 1 ? blockIdx.y : blockIdx.z) * Smem::LINES;
     }
-    const int i0 = blockIdx.x * 32;
+    constexpr int TW = Smem::TW;
+    const int i0 = blockIdx.x * TW;
     const int jb = DIR == 2 ? blockIdx.y : 0;  // fixed j (DIR 2)
     const int kb = DIR == 1 ? blockIdx.z : 0;  // fixed k (DIR 1)
     // metric planes: xi (DIR 0) / eta (DIR 1) use (m_x, m_y); zeta uses m_zz
@@ -177,8 +188,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     if (DIR == 0) {
         xface(threadIdx.x, my_col, my_f);
     } else {
-        my_f = f0 + warp;
-        my_col = i0 + lane;
+        my_f = f0 + (int)threadIdx.x / TW;
+        my_col = i0 + (int)threadIdx.x % TW;
     }
     const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < nrows)
                                     : (my_col < P.nx && my_f < f_hi);
@@ -247,8 +258,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 }
                 ok = ok && a < P.nx + P.g && col < nrows && (t < n0 || t - n0 < NF - L0 + W - 1);
             } else {
-                a = f0 - H + t / 32;
-                col = i0 + t % 32;
+                a = f0 - H + t / TW;
+                col = i0 + t % TW;
                 ok = ok && col < P.nx && a < nd + P.g;
             }
             slot_t[it] = ok ? t : -1;
@@ -306,8 +317,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 }
                 ok = a < P.nx + P.g && col < nrows && (t < n0 || t - n0 < NF - L0 + W - 1);
             } else {
-                a = f0 - H + t / 32;
-                col = i0 + t % 32;
+                a = f0 - H + t / TW;
+                col = i0 + t % TW;
                 ok = col < P.nx && a < nd + P.g;
             }
             if (!ok) continue;
@@ -402,14 +413,73 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
     const long long fplane = (long long)(P.nx + (DIR == 0)) * (P.ny + (DIR == 1)) *
                              (P.nz + (DIR == 2));
     const int fl = warp;
+    // ---------------- phase 3: component fl of R * amp of group g
+    // (flux.hpp:123-139 + z), run while the next group's vectors are built:
+    // the amplitude table holds one group
+    auto assemble_group = [&](int g) {
+        const int face = g * 32 + lane;
+        if (S.bad[face]) return;
+        int f, col;
+        if (DIR == 0) {
+            xface(face, col, f);
+        } else {
+            f = f0 + face / TW;
+            col = i0 + face % TW;
+        }
+        const long long o = out_index(f, col);
+        const double am = S.amp[0][lane];
+        const double ap = S.amp[NC - 1][lane];
+        const double at1 = S.amp[NC - 3][lane];
+        const double at2 = S.amp[NC - 2][lane];
+        const double c = S.E[F3C][face];
+        using ER = ERow<NS, DIR>;
+        const double n1 = ER::n1(S, face), n2 = ER::n2(S, face), n3 = ER::n3(S, face);
+        double r;
+        if (fl < NS) {
+            r = S.E[F3Y0 + fl][face] * (am + ap) + S.amp[1 + fl][lane];
+        } else {
+            double asum = 0.0;
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp) asum += S.amp[1 + sp][lane];
+            const double u = S.E[F3U][face], v = S.E[F3V][face], w = S.E[F3W][face];
+            if (fl == NS) {  // rho u
+                r = DIR < 2 ? (u - c * n1) * am + (u + c * n1) * ap + u * asum - n2 * at1
+                            : u * am + u * ap + u * asum + at1;
+            } else if (fl == NS + 1) {  // rho v
+                r = DIR < 2 ? (v - c * n2) * am + (v + c * n2) * ap + v * asum + n1 * at1
+                            : v * am + v * ap + v * asum + at2;
+            } else if (fl == NS + 2) {  // rho w
+                r = DIR < 2 ? w * am + w * ap + w * asum + at2
+                            : (w - c * n3) * am + (w + c * n3) * ap + w * asum;
+            } else {  // E
+                const double Hh = S.E[F3H][face], un = ER::un(S, face);
+                const double ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
+                // EigenSystem's k (eigen_at_state3), from the stored velocity
+                const double kk = 0.5 * ((u * u + v * v) + w * w);
+                const double kappa = S.E[F3KAPPA][face];
+                const double ykappa = S.E[F3YKAPPA][face];
+                double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut1 * at1;
+                en = en + ut2 * at2;
+#pragma unroll
+                for (int sp = 0; sp < NS; ++sp) {
+                    const double th = S.E[F3Y0 + NS + sp][face];
+                    en += S.amp[1 + sp][lane] *
+                          (2.0 * kk - fdiv(th, kappa, ykappa));
+                }
+                r = en;
+            }
+        }
+        out[fl * fplane + o] = r;
+    };
     for (int g = 0; g < NC; ++g) {
+        if (CHAR && g > 0) assemble_group(g - 1);
         const int face = g * 32 + lane;
         int f, col;
         if (DIR == 0) {
             xface(face, col, f);
         } else {
-            f = f0 + g;
-            col = i0 + lane;
+            f = f0 + face / TW;
+            col = i0 + face % TW;
         }
         const bool live = !S.bad[face];
         const long long o = out_index(f, col);
@@ -438,9 +508,8 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         // the three distinct LLF wave speeds of the face (solver.hpp:555-566;
         // the convective one serves every species and shear field), by the
         // warps with the fewest projection vectors
-        // work split of (a): the shear warps (no projection quotients in (b))
-        // take the extra stencil vectors, the three lightest other warps the
-        // LLF speeds — the fields then reach the group barrier together
+        // work split of (a): 2W vectors over NC warps; the warps with one
+        // vector fewer take the three LLF speeds
         const int rot = (warp + 3) % NC;
         if (rot >= NC - 3 && !S.bad[face]) {
             const int kind = NC - 1 - rot;  // 0: un - c, 1: un, 2: un + c
@@ -459,7 +528,18 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             }
             S.alpha[kind][lane] = alpha;
         }
-        for (int vec = rot; vec < NV; vec += NC) {
+        // (a) also projects: vector vec's value in every characteristic field,
+        // so every warp's (b) below is the same split + reconstruction work.
+        // acoustic w = (dp -+ c dun) / (2c^2), written as dp + s*(c dun) with
+        // s = -+1 (exact negation); species w = q_s - Y_s dp / c^2; shear
+        // w = dut1, dut2.  One validity flag per vector (exact redo if unset).
+        const double ec = S.E[F3C][face];
+        const double c2 = S.E[F3C2][face], yc2 = S.E[F3YC2][face];
+        // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
+        const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
+        const unsigned den_bad =
+            (fdiv_pos_divisor_ok(c2) && fdiv_pos_divisor_ok(c2x2)) ? 0u : 1u;
+        for (int vec = live ? rot : NV; vec < NV; vec += NC) {
             const int k = vec >> 1;
             const int t = tile_node3<DIR, W>(g, lane, k, L0);
             double q[NC];
@@ -471,78 +551,45 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             double dp = kap * q[NS + 3] - keu * q[NS] - kev * q[NS + 1] - kew * q[NS + 2];
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) dp += S.E[F3Y0 + NS + sp][face] * q[sp];
-            S.L[vec][0][lane] = dp;
+            double dun, dut1, dut2;
             if (DIR < 2) {
-                S.L[vec][1][lane] = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
-                S.L[vec][2][lane] = -n2 * q[NS] + n1 * q[NS + 1] - ut1 * drho;
-                S.L[vec][3][lane] = q[NS + 2] - ut2 * drho;
+                dun = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
+                dut1 = -n2 * q[NS] + n1 * q[NS + 1] - ut1 * drho;
+                dut2 = q[NS + 2] - ut2 * drho;
             } else {
-                S.L[vec][1][lane] = n3 * q[NS + 2] - un * drho;
-                S.L[vec][2][lane] = q[NS] - ut1 * drho;
-                S.L[vec][3][lane] = q[NS + 1] - ut2 * drho;
+                dun = n3 * q[NS + 2] - un * drho;
+                dut1 = q[NS] - ut1 * drho;
+                dut2 = q[NS + 1] - ut2 * drho;
             }
+            unsigned bad = den_bad;
+            const double cdun = ec * dun;
+            double wv[NC];
+            wv[0] = fdiv_pos_try(dp + -1.0 * cdun, c2x2, y2c2, bad);
+            wv[NC - 1] = fdiv_pos_try(dp + 1.0 * cdun, c2x2, y2c2, bad);
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp)
+                wv[1 + sp] = q[sp] - fdiv_pos_try(S.E[F3Y0 + sp][face] * dp, c2, yc2, bad);
+            if (bad) {  // exact redo (rare): plain IEEE quotients
+                wv[0] = div_cold(dp + -1.0 * cdun, c2x2);
+                wv[NC - 1] = div_cold(dp + 1.0 * cdun, c2x2);
+#pragma unroll
+                for (int sp = 0; sp < NS; ++sp)
+                    wv[1 + sp] = q[sp] - div_cold(S.E[F3Y0 + sp][face] * dp, c2);
+            }
+            wv[NC - 3] = dut1;
+            wv[NC - 2] = dut2;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) S.Wc[vec][c][lane] = wv[c];
         }
         __syncthreads();
-        // (b) row fl of L, wave speed, LLF split, reconstruction
+        // (b) field fl: wave speed, LLF split, reconstruction
         double amp = 0.0;
         if (live) {
-            const double ec = S.E[F3C][face];
-            const double c2 = S.E[F3C2][face], yc2 = S.E[F3YC2][face];
-            const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
-            const bool ac = fl == 0 || fl == NC - 1;
-            const bool sh1 = fl == NC - 3, sh2 = fl == NC - 2;
-            const int sp_i = (ac || sh1 || sh2) ? 0 : fl - 1;
-            const double sgn = fl == 0 ? -1.0 : 1.0;
-            const double Ys = S.E[F3Y0 + sp_i][face];
-            const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
             double lf[W], lu[W];
-            if (sh1 || sh2) {
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    lf[k] = S.L[2 * k][sh1 ? 2 : 3][lane];
-                    lu[k] = S.L[2 * k + 1][sh1 ? 2 : 3][lane];
-                }
-            } else if (ac) {
-                // acoustic fields: w = (dp -+ c dun) / (2c^2) as dp + s (c dun)
-                // (warp-uniform branch: no selects, no unused products)
-                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
-#pragma unroll
-                for (int vec = 0; vec < NV; ++vec) {
-                    const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
-                    const double fd = fdiv_pos_try(num, den, yden, bad);
-                    if (vec & 1) lu[vec >> 1] = fd;
-                    else lf[vec >> 1] = fd;
-                }
-                if (bad) {
-#pragma unroll
-                    for (int vec = 0; vec < NV; ++vec) {
-                        const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
-                        const double fd = div_cold(num, den);
-                        if (vec & 1) lu[vec >> 1] = fd;
-                        else lf[vec >> 1] = fd;
-                    }
-                }
-            } else {
-                // species fields: w = q_s - Y_s dp / c^2
-                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
-#pragma unroll
-                for (int vec = 0; vec < NV; ++vec) {
-                    const int t = tile_node3<DIR, W>(g, lane, vec >> 1, L0);
-                    const double fd = fdiv_pos_try(Ys * S.L[vec][0][lane], den, yden, bad);
-                    const double wv = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
-                    if (vec & 1) lu[vec >> 1] = wv;
-                    else lf[vec >> 1] = wv;
-                }
-                if (bad) {
-#pragma unroll
-                    for (int vec = 0; vec < NV; ++vec) {
-                        const int t = tile_node3<DIR, W>(g, lane, vec >> 1, L0);
-                        const double fd = div_cold(Ys * S.L[vec][0][lane], den);
-                        const double wv = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
-                        if (vec & 1) lu[vec >> 1] = wv;
-                        else lf[vec >> 1] = wv;
-                    }
-                }
+            for (int k = 0; k < W; ++k) {
+                lf[k] = S.Wc[2 * k][fl][lane];
+                lu[k] = S.Wc[2 * k + 1][fl][lane];
             }
             const double alpha = S.alpha[fl == 0 ? 0 : fl == NC - 1 ? 2 : 1][lane];
             if (!isfinite(alpha)) {
@@ -557,67 +604,10 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 amp = face_pm<TENO>(wp, wm, P.rp);
             }
         }
-        S.amp[fl][face] = amp;
+        S.amp[fl][lane] = amp;
         __syncthreads();
     }
-    if (!CHAR) return;
-
-    // ---------------- phase 3: component fl of R * amp (flux.hpp:123-139 + z)
-    for (int g = 0; g < NC; ++g) {
-        const int face = g * 32 + lane;
-        if (S.bad[face]) continue;
-        int f, col;
-        if (DIR == 0) {
-            xface(face, col, f);
-        } else {
-            f = f0 + g;
-            col = i0 + lane;
-        }
-        const long long o = out_index(f, col);
-        const double am = S.amp[0][face];
-        const double ap = S.amp[NC - 1][face];
-        const double at1 = S.amp[NC - 3][face];
-        const double at2 = S.amp[NC - 2][face];
-        const double c = S.E[F3C][face];
-        using ER = ERow<NS, DIR>;
-        const double n1 = ER::n1(S, face), n2 = ER::n2(S, face), n3 = ER::n3(S, face);
-        double r;
-        if (fl < NS) {
-            r = S.E[F3Y0 + fl][face] * (am + ap) + S.amp[1 + fl][face];
-        } else {
-            double asum = 0.0;
-#pragma unroll
-            for (int sp = 0; sp < NS; ++sp) asum += S.amp[1 + sp][face];
-            const double u = S.E[F3U][face], v = S.E[F3V][face], w = S.E[F3W][face];
-            if (fl == NS) {  // rho u
-                r = DIR < 2 ? (u - c * n1) * am + (u + c * n1) * ap + u * asum - n2 * at1
-                            : u * am + u * ap + u * asum + at1;
-            } else if (fl == NS + 1) {  // rho v
-                r = DIR < 2 ? (v - c * n2) * am + (v + c * n2) * ap + v * asum + n1 * at1
-                            : v * am + v * ap + v * asum + at2;
-            } else if (fl == NS + 2) {  // rho w
-                r = DIR < 2 ? w * am + w * ap + w * asum + at2
-                            : (w - c * n3) * am + (w + c * n3) * ap + w * asum;
-            } else {  // E
-                const double Hh = S.E[F3H][face], un = ER::un(S, face);
-                const double ut1 = ER::ut1(S, face), ut2 = ER::ut2(S, face);
-                // EigenSystem's k (eigen_at_state3), from the stored velocity
-                const double kk = 0.5 * ((u * u + v * v) + w * w);
-                const double kappa = S.E[F3KAPPA][face];
-                const double ykappa = S.E[F3YKAPPA][face];
-                double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut1 * at1;
-                en = en + ut2 * at2;
-#pragma unroll
-                for (int sp = 0; sp < NS; ++sp) {
-                    const double th = S.E[F3Y0 + NS + sp][face];
-                    en += S.amp[1 + sp][face] *
-                          (2.0 * kk - fdiv(th, kappa, ykappa));
-                }
-                r = en;
-            }
-        }
-        out[fl * fplane + o] = r;
-    }
+    if (CHAR) assemble_group(NC - 1);
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR, int TM>
@@ -638,8 +628,11 @@ inline int launch_faces3d_tm(const KParams& P, const double* Ut, int stage, int 
         else
             grid = dim3((P.nx + 1 + NF - 1) / NF, P.ny, P.nz);
     }
-    else if (DIR == 1) grid = dim3((P.nx + 31) / 32, (f_hi - f_lo + NC - 1) / NC, P.nz);
-    else grid = dim3((P.nx + 31) / 32, P.ny, (f_hi - f_lo + NC - 1) / NC);
+    else {
+        constexpr int TW = FaceSmem3<NS, DIR, TENO, CHAR>::TW, LN = NF / TW;
+        if (DIR == 1) grid = dim3((P.nx + TW - 1) / TW, (f_hi - f_lo + LN - 1) / LN, P.nz);
+        else grid = dim3((P.nx + TW - 1) / TW, P.ny, (f_hi - f_lo + LN - 1) / LN);
+    }
     kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step, f_lo, f_hi);
     return 1;
 }
