@@ -31,6 +31,14 @@
 
 namespace ign {
 
+// y tile width (columns): see FaceSmem::TW.  One species: 8 columns (the window's
+// halo lines shrink, one more CTA fits per SM); several: 32 (those kernels are
+// held at 2 CTAs/SM by registers, and the wider tile keeps the launch in
+// whole waves at 512^2)
+template <int NS, int DIR> __host__ __device__ constexpr int tile_w() {
+    return DIR == 0 || NS > 1 ? 32 : 8;
+}
+
 // CHAR = false (componentwise) needs only the node window and one LLF speed
 // per face: the characteristic tables shrink to one row so more CTAs fit
 template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
@@ -38,8 +46,11 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
     static constexpr int NF = 32 * NC;  // faces per CTA
+    // y tiles: TW columns x NF/TW face rows (few halo rows in the window)
+    static constexpr int TW = tile_w<NS, DIR>();
+    static constexpr int LINES = NF / TW;
     // x: up to two row segments of the flattened face order (see k_faces3)
-    static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : 32 * (NC + W - 1);
+    static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : TW * (LINES + W - 1);
     static constexpr int NE_CHAR = 11 + 2 * NS;
     static constexpr int NE = CHAR ? NE_CHAR : 1;
     static constexpr int NV = 2 * W;  // stencil vectors: F and U of each node
@@ -50,8 +61,10 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
     double F[NC][NT];
     double u[NT], v[NT], c[NT];
     double E[NE][NF];         // eigen data per face (char); [0] alpha, [1] sf (comp)
-    double L[NV_S][3][32];      // dp, dun, dut of one group's vectors
-    double amp[NA_S][NF];
+    // characteristic values of one group's stencil vectors, every field: row
+    // fl of L F and L U (EigenSystem::project, flux.hpp:107-119)
+    double Wc[NV_S][NA_S][32];
+    double amp[NA_S][32];  // one group (phase 3 follows each group)
     double alpha[NK_S][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
     int bad[NF];
 };
@@ -74,15 +87,15 @@ template <class Sm> __device__ __forceinline__ double eigen_k(const Sm& S, int f
     return 0.5 * (S.E[EU][f] * S.E[EU][f] + S.E[EV][f] * S.E[EV][f]);
 }
 
-// window slot of stencil node k of face (g, lane); x faces past the first row
-// segment (q >= L0) sit W-1 slots further (their segment's own halo)
-template <int DIR, int W>
+// window slot of stencil node k of face slot q = 32 g + lane; x faces past the
+// first row segment (q >= L0) sit W-1 slots further (their segment's own
+// halo); y: slot q is column q % TW of face row q / TW, its node k lies k rows
+// further
+template <int NS, int DIR, int W>
 __device__ __forceinline__ int tile_node(int g, int lane, int k, int L0) {
-    if (DIR == 0) {
-        const int q = g * 32 + lane;
-        return q + k + (q >= L0 ? W - 1 : 0);
-    }
-    return (g + k) * 32 + lane;
+    const int q = g * 32 + lane;
+    if (DIR == 0) return q + k + (q >= L0 ? W - 1 : 0);
+    return q + k * tile_w<NS, DIR>();
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR, int TM>
@@ -124,9 +137,10 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         }
     } else {
         // y faces [f_lo, f_hi) of the line (a slab splits interior and halo faces)
-        f0 = f_lo + blockIdx.y * NC;
+        f0 = f_lo + blockIdx.y * Smem::LINES;
     }
-    const int i0 = blockIdx.x * 32;
+    constexpr int TW = Smem::TW;
+    const int i0 = blockIdx.x * TW;
     const long long win0 = DIR == 0 ? 0 : pidx(P, i0, f0 - H);
     // x face q of this CTA -> (row, f)
     auto xface = [&](int q, int& row, int& f) {
@@ -165,7 +179,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 id = pidx(P, a, row);
                 ok = ok && a < P.nx + P.g && row < P.ny && (t < n0 || t - n0 < NF - L0 + W - 1);
             } else {
-                const int r = t / 32, l = t % 32;
+                const int r = t / TW, l = t % TW;
                 id = win0 + (long long)r * P.sx + l;
                 ok = ok && i0 + l < P.nx && f0 - H + r < P.ny + P.g;
             }
@@ -219,7 +233,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 id = pidx(P, a, row);
                 ok = a < P.nx + P.g && row < P.ny && (t < n0 || t - n0 < NF - L0 + W - 1);
             } else {
-                const int r = t / 32, l = t % 32;
+                const int r = t / TW, l = t % TW;
                 id = win0 + (long long)r * P.sx + l;
                 ok = i0 + l < P.nx && f0 - H + r < P.ny + P.g;
             }
@@ -246,8 +260,8 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     if (DIR == 0) {
         xface(threadIdx.x, my_col, my_f);
     } else {
-        my_f = f0 + warp;
-        my_col = i0 + lane;
+        my_f = f0 + (int)threadIdx.x / TW;
+        my_col = i0 + (int)threadIdx.x % TW;
     }
     const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < P.ny)
                                     : (my_col < P.nx && my_f < f_hi);
@@ -317,7 +331,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node<DIR, W>(warp, lane, k, L0);
+                const int t = tile_node<NS, DIR, W>(warp, lane, k, L0);
                 const double un = (m1f * S.u[t] + m2f * S.v[t]) / sf;
                 alpha = smax(alpha, sf * (fabs(un) + S.c[t]));
             }
@@ -335,33 +349,89 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     double* out = DIR == 0 ? P.Fx : P.Gy;
     const long long fplane = (long long)(P.nx + 1 - DIR) * (P.ny + DIR);
     const int fl = warp;  // field / component this warp evaluates
-    for (int g = 0; g < NC; ++g) {
-        const int face = g * 32 + lane;  // slot in the CTA
-        int f, col;
+    // face slot q = 32 g + lane -> (face index along the line, row / column)
+    auto slot_face = [&](int q, int& f, int& col) {
         if (DIR == 0) {
-            xface(face, col, f);
+            xface(q, col, f);
         } else {
-            f = f0 + g;
-            col = i0 + lane;
+            f = f0 + q / TW;
+            col = i0 + q % TW;
         }
-        const bool live = !S.bad[face];
-        const long long o = DIR == 0 ? (long long)col * (P.nx + 1) + f : (long long)f * P.nx + col;
-        if (!CHAR) {
-            // componentwise: component fl of the LLF-split TENO sum
-            if (live) {
-                const double alpha = S.E[0][face];
-                double wp[W], wm[W];
+    };
+    auto out_at = [&](int f, int col) -> long long {
+        return DIR == 0 ? (long long)col * (P.nx + 1) + f : (long long)f * P.nx + col;
+    };
+    if constexpr (!CHAR) {
+        // componentwise: component fl of the LLF-split TENO sum
+        for (int g = 0; g < NC; ++g) {
+            const int face = g * 32 + lane;
+            if (S.bad[face]) continue;
+            int f, col;
+            slot_face(face, f, col);
+            const double alpha = S.E[0][face];
+            double wp[W], wm[W];
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    const int t = tile_node<DIR, W>(g, lane, k, L0);
-                    wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
-                    wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
-                }
-                out[fl * fplane + o] = face_pm<TENO>(wp, wm, P.rp);
+            for (int k = 0; k < W; ++k) {
+                const int t = tile_node<NS, DIR, W>(g, lane, k, L0);
+                wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
+                wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
             }
-            continue;
+            out[fl * fplane + out_at(f, col)] = face_pm<TENO>(wp, wm, P.rp);
         }
-        // (a) field-independent parts of L q for this group's stencil vectors
+        return;
+    }
+    // ---------------- phase 3: component fl of R * amp of group g
+    // (flux.hpp:123-139), run while the next group's vectors are built: the
+    // amplitude table holds one group
+    auto assemble_group = [&](int g) {
+        const int face = g * 32 + lane;
+        if (S.bad[face]) return;
+        int f, col;
+        slot_face(face, f, col);
+        const double am = S.amp[0][lane];
+        const double ap = S.amp[2 + NS][lane];
+        const double at = S.amp[1 + NS][lane];
+        const double c = S.E[EC][face];
+        double r;
+        if (fl < NS) {
+            r = S.E[EY0 + fl][face] * (am + ap) + S.amp[1 + fl][lane];
+        } else {
+            double asum = 0.0;
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp) asum += S.amp[1 + sp][lane];
+            if (fl == NS) {
+                const double u = S.E[EU][face], n1 = S.E[EN1][face], n2 = S.E[EN2][face];
+                r = (u - c * n1) * am + (u + c * n1) * ap + u * asum - n2 * at;
+            } else if (fl == NS + 1) {
+                const double v = S.E[EV][face], n1 = S.E[EN1][face], n2 = S.E[EN2][face];
+                r = (v - c * n2) * am + (v + c * n2) * ap + v * asum + n1 * at;
+            } else {
+                const double Hh = S.E[EH][face], un = eigen_un(S, face), ut = eigen_ut(S, face);
+                const double kk = eigen_k(S, face), kappa = S.E[EKAPPA][face];
+                const double ykappa = S.E[EYKAPPA][face];
+                double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut * at;
+#pragma unroll
+                for (int sp = 0; sp < NS; ++sp) {
+                    const double th = S.E[EY0 + NS + sp][face];
+                    en += S.amp[1 + sp][lane] * (2.0 * kk - fdiv(th, kappa, ykappa));
+                }
+                r = en;
+            }
+        }
+        out[fl * fplane + out_at(f, col)] = r;
+    };
+    for (int g = 0; g < NC; ++g) {
+        if (g > 0) assemble_group(g - 1);
+        const int face = g * 32 + lane;  // slot in the CTA
+        const bool live = !S.bad[face];
+        int f, col;
+        slot_face(face, f, col);
+        // (a) L q for this group's stencil vectors (flux.hpp:107-119): the
+        // field-independent parts and every field's projection row, so each
+        // warp's (b) is the same split + reconstruction work.  acoustic
+        // w = (dp -+ c dun) / (2c^2), written as dp + s*(c dun) with s = -+1
+        // (exact negation); species w = q_s - Y_s dp / c^2; shear w = dut.
+        // One validity flag per vector (exact redo if unset).
         const double kap = S.E[EKAPPA][face], eu = S.E[EU][face], ev = S.E[EV][face];
         const double n1 = S.E[EN1][face], n2 = S.E[EN2][face];
         const double un = eigen_un(S, face), ut = eigen_ut(S, face);
@@ -369,17 +439,17 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         const double keu = kap * eu, kev = kap * ev;
         // the three distinct LLF wave speeds of the face (EigenSystem::field_speed,
         // flux.hpp:143-147; the convective one serves species and shear fields)
-        // work split of (a): the shear warps (no projection quotients in (b))
-        // take the extra stencil vectors, the three lightest other warps the
-        // LLF speeds — the fields then reach the group barrier together
+        // by the warps with one vector fewer
         const int rot = (warp + 2) % NC;
-        if (rot >= NC - 3 && !S.bad[face]) {
-            const int kind = NC - 1 - rot;  // 0: un - c, 1: un, 2: un + c
+        // the warps with one vector fewer (rot >= REM) take the three LLF
+        // speed kinds (0: un - c, 1: un, 2: un + c), two each if fewer than 3
+        constexpr int REM = NV % NC, NFEW = REM == 0 ? NC : NC - REM;
+        for (int kind = rot - REM; live && kind >= 0 && kind < 3; kind += NFEW) {
             const double es = S.E[ES][face];
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node<DIR, W>(g, lane, k, L0);
+                const int t = tile_node<NS, DIR, W>(g, lane, k, L0);
                 const double unk = n1 * S.u[t] + n2 * S.v[t];
                 const double ck = S.c[t];
                 // kind is warp-uniform: the selects pick one expression
@@ -389,9 +459,14 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             }
             S.alpha[kind][lane] = alpha;
         }
-        for (int vec = rot; vec < NV; vec += NC) {
+        const double ec = S.E[EC][face];
+        const double c2 = S.E[EC2][face], yc2 = S.E[EYC2][face];
+        // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
+        const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
+        const unsigned den_bad = (fdiv_pos_divisor_ok(c2) && fdiv_pos_divisor_ok(c2x2)) ? 0u : 1u;
+        for (int vec = live ? rot : NV; vec < NV; vec += NC) {
             const int k = vec >> 1;
-            const int t = tile_node<DIR, W>(g, lane, k, L0);
+            const int t = tile_node<NS, DIR, W>(g, lane, k, L0);
             double q[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) q[c] = (vec & 1) ? S.U[c][t] : S.F[c][t];
@@ -401,76 +476,36 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             double dp = kap * q[NS + 2] - keu * q[NS] - kev * q[NS + 1];
 #pragma unroll
             for (int sp = 0; sp < NS; ++sp) dp += S.E[EY0 + NS + sp][face] * q[sp];
-            S.L[vec][0][lane] = dp;
-            S.L[vec][1][lane] = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
-            S.L[vec][2][lane] = -n2 * q[NS] + n1 * q[NS + 1] - ut * drho;
+            const double dun = n1 * q[NS] + n2 * q[NS + 1] - un * drho;
+            const double dut = -n2 * q[NS] + n1 * q[NS + 1] - ut * drho;
+            unsigned bad = den_bad;
+            const double cdun = ec * dun;
+            double wv[NC];
+            wv[0] = fdiv_pos_try(dp + -1.0 * cdun, c2x2, y2c2, bad);
+            wv[NC - 1] = fdiv_pos_try(dp + 1.0 * cdun, c2x2, y2c2, bad);
+#pragma unroll
+            for (int sp = 0; sp < NS; ++sp)
+                wv[1 + sp] = q[sp] - fdiv_pos_try(S.E[EY0 + sp][face] * dp, c2, yc2, bad);
+            if (bad) {  // exact redo (rare): plain IEEE quotients
+                wv[0] = div_cold(dp + -1.0 * cdun, c2x2);
+                wv[NC - 1] = div_cold(dp + 1.0 * cdun, c2x2);
+#pragma unroll
+                for (int sp = 0; sp < NS; ++sp)
+                    wv[1 + sp] = q[sp] - div_cold(S.E[EY0 + sp][face] * dp, c2);
+            }
+            wv[NC - 2] = dut;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) S.Wc[vec][c][lane] = wv[c];
         }
         __syncthreads();
-        // (b) row fl of L on the stencil, wave speed, split, reconstruction
+        // (b) field fl: wave speed, LLF split, reconstruction
         double amp = 0.0;
         if (live) {
-            const double ec = S.E[EC][face];
-            const double c2 = S.E[EC2][face], yc2 = S.E[EYC2][face];
-            // 2c^2 and RN(1/(2c^2)) = RN(1/c^2)/2: scaling by 2 is exact
-            const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
             double lf[W], lu[W];
-            // Row fl of EigenSystem::project (flux.hpp:116-119), one
-            // warp-uniform branch per field kind: acoustic w = (dp -+ c dun) /
-            // (2c^2), written as dp + s*(c dun) with s = -+1 (exact negation);
-            // species w = q_s - Y_s dp / c^2; shear w = dut.  The 2W quotients
-            // share one validity flag (one branch, exact redo on the rare failure).
-            const bool ac = fl == 0 || fl == NC - 1, sh = fl == NC - 2;
-            const int sp_i = ac || sh ? 0 : fl - 1;
-            const double sgn = fl == 0 ? -1.0 : 1.0;
-            const double Ys = S.E[EY0 + sp_i][face];
-            const double den = ac ? c2x2 : c2, yden = ac ? y2c2 : yc2;
-            if (sh) {
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    lf[k] = S.L[2 * k][2][lane];
-                    lu[k] = S.L[2 * k + 1][2][lane];
-                }
-            } else if (ac) {
-                // acoustic fields: w = (dp -+ c dun) / (2c^2) as dp + s (c dun)
-                // (warp-uniform branch: no selects, no unused products)
-                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
-#pragma unroll
-                for (int vec = 0; vec < NV; ++vec) {
-                    const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
-                    const double fd = fdiv_pos_try(num, den, yden, bad);
-                    if (vec & 1) lu[vec >> 1] = fd;
-                    else lf[vec >> 1] = fd;
-                }
-                if (bad) {  // exact redo (rare): plain IEEE quotients
-#pragma unroll
-                    for (int vec = 0; vec < NV; ++vec) {
-                        const double num = S.L[vec][0][lane] + sgn * (ec * S.L[vec][1][lane]);
-                        const double fd = div_cold(num, den);
-                        if (vec & 1) lu[vec >> 1] = fd;
-                        else lf[vec >> 1] = fd;
-                    }
-                }
-            } else {
-                // species fields: w = q_s - Y_s dp / c^2
-                unsigned bad = fdiv_pos_divisor_ok(den) ? 0u : 1u;
-#pragma unroll
-                for (int vec = 0; vec < NV; ++vec) {
-                    const int t = tile_node<DIR, W>(g, lane, vec >> 1, L0);
-                    const double fd = fdiv_pos_try(Ys * S.L[vec][0][lane], den, yden, bad);
-                    const double w = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
-                    if (vec & 1) lu[vec >> 1] = w;
-                    else lf[vec >> 1] = w;
-                }
-                if (bad) {  // exact redo (rare): plain IEEE quotients
-#pragma unroll
-                    for (int vec = 0; vec < NV; ++vec) {
-                        const int t = tile_node<DIR, W>(g, lane, vec >> 1, L0);
-                        const double fd = div_cold(Ys * S.L[vec][0][lane], den);
-                        const double w = ((vec & 1) ? S.U[sp_i][t] : S.F[sp_i][t]) - fd;
-                        if (vec & 1) lu[vec >> 1] = w;
-                        else lf[vec >> 1] = w;
-                    }
-                }
+            for (int k = 0; k < W; ++k) {
+                lf[k] = S.Wc[2 * k][fl][lane];
+                lu[k] = S.Wc[2 * k + 1][fl][lane];
             }
             // EigenSystem::field_speed (flux.hpp:143-147), computed once per kind
             const double alpha = S.alpha[fl == 0 ? 0 : fl == NC - 1 ? 2 : 1][lane];
@@ -486,56 +521,10 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 amp = face_pm<TENO>(wp, wm, P.rp);
             }
         }
-        S.amp[fl][face] = amp;
-        __syncthreads();  // amp complete; L may be overwritten by the next group
+        S.amp[fl][lane] = amp;
+        __syncthreads();  // amp complete; Wc may be overwritten by the next group
     }
-    if (!CHAR) return;
-
-    // ---------------- phase 3: component fl of R * amp (flux.hpp:123-139)
-    for (int g = 0; g < NC; ++g) {
-        const int face = g * 32 + lane;
-        if (S.bad[face]) continue;
-        int f, col;
-        if (DIR == 0) {
-            xface(face, col, f);
-        } else {
-            f = f0 + g;
-            col = i0 + lane;
-        }
-        const long long o = DIR == 0 ? (long long)col * (P.nx + 1) + f : (long long)f * P.nx + col;
-        const double am = S.amp[0][face];
-        const double ap = S.amp[2 + NS][face];
-        const double at = S.amp[1 + NS][face];
-        const double c = S.E[EC][face];
-        double r;
-        if (fl < NS) {
-            r = S.E[EY0 + fl][face] * (am + ap) + S.amp[1 + fl][face];
-        } else {
-            double asum = 0.0;
-#pragma unroll
-            for (int sp = 0; sp < NS; ++sp) asum += S.amp[1 + sp][face];
-            if (fl == NS) {
-                const double u = S.E[EU][face], n1 = S.E[EN1][face], n2 = S.E[EN2][face];
-                r = (u - c * n1) * am + (u + c * n1) * ap + u * asum - n2 * at;
-            } else if (fl == NS + 1) {
-                const double v = S.E[EV][face], n1 = S.E[EN1][face], n2 = S.E[EN2][face];
-                r = (v - c * n2) * am + (v + c * n2) * ap + v * asum + n1 * at;
-            } else {
-                const double Hh = S.E[EH][face], un = eigen_un(S, face), ut = eigen_ut(S, face);
-                const double kk = eigen_k(S, face), kappa = S.E[EKAPPA][face];
-                const double ykappa = S.E[EYKAPPA][face];
-                double en = (Hh - c * un) * am + (Hh + c * un) * ap + ut * at;
-#pragma unroll
-                for (int sp = 0; sp < NS; ++sp) {
-                    const double th = S.E[EY0 + NS + sp][face];
-                    en += S.amp[1 + sp][face] *
-                          (2.0 * kk - fdiv(th, kappa, ykappa));
-                }
-                r = en;
-            }
-        }
-        out[fl * fplane + o] = r;
-    }
+    assemble_group(NC - 1);
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR, int TM>
@@ -554,8 +543,10 @@ inline int launch_faces3_tm(const KParams& P, const double* Ut, int stage, int s
         grid = P.nx + 1 >= NF  // flattened rows: (nx+1) ny faces in runs of NF
                    ? dim3((unsigned)(((long long)(P.nx + 1) * P.ny + NF - 1) / NF), 1)
                    : dim3((P.nx + 1 + NF - 1) / NF, P.ny);
-    else
-        grid = dim3((P.nx + 31) / 32, (f_hi - f_lo + NC - 1) / NC);
+    else {
+        constexpr int TW = FaceSmem<NS, DIR, TENO, CHAR>::TW, LN = NF / TW;
+        grid = dim3((P.nx + TW - 1) / TW, (f_hi - f_lo + LN - 1) / LN);
+    }
     kern<<<grid, 32 * NC, smem, s>>>(P, Ut, stage, step, f_lo, f_hi);
     return 1;
 }

@@ -18,8 +18,13 @@ __device__ __forceinline__ long long pidx3(const KParams& P, int i, int j, int k
     return (long long)(k + P.g) * P.sxy + (long long)(j + P.g) * P.sx + (i + P.g);
 }
 
-// y/z tile width (columns): see FaceSmem3::TW
-template <int DIR> __host__ __device__ constexpr int tile_w3() { return DIR == 0 ? 32 : 8; }
+// y/z tile width (columns): see FaceSmem3::TW.  One species: 8 columns (the window's
+// halo lines shrink, one more CTA fits per SM); several: 32 (those kernels are
+// held at 2 CTAs/SM by registers, and the wider tile keeps the launch in
+// whole waves at 512^2)
+template <int NS, int DIR> __host__ __device__ constexpr int tile_w3() {
+    return DIR == 0 || NS > 1 ? 32 : 8;
+}
 
 // CHAR = false (componentwise) needs only the node window and one LLF speed
 // per face: the characteristic tables shrink to one row so more CTAs fit
@@ -30,7 +35,7 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem3 {
     static constexpr int NF = 32 * NC;
     // y/z tiles: TW columns x NF/TW face lines (a narrow tile keeps the
     // window's halo lines few: 4 CTAs/SM fit)
-    static constexpr int TW = tile_w3<DIR>();
+    static constexpr int TW = tile_w3<NS, DIR>();
     static constexpr int LINES = NF / TW;
     // x: up to two row segments of the flattened face order (see k_faces3d)
     static constexpr int NT = DIR == 0 ? NF + 2 * (W - 1) : TW * (LINES + W - 1);
@@ -92,11 +97,11 @@ template <int NS, int DIR> struct ERow {
 // first row segment (q >= L0) sit W-1 slots further (their segment's own
 // halo); y/z: slot q is column q % TW of face line q / TW, its node k lies k
 // lines further
-template <int DIR, int W>
+template <int NS, int DIR, int W>
 __device__ __forceinline__ int tile_node3(int g, int lane, int k, int L0) {
     const int q = g * 32 + lane;
     if (DIR == 0) return q + k + (q >= L0 ? W - 1 : 0);
-    return q + k * tile_w3<DIR>();
+    return q + k * tile_w3<NS, DIR>();
 }
 
 // Registers: a 5-warp CTA needs <= 128 per thread for 3 CTAs/SM (4 warps per
@@ -392,7 +397,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR, W>(warp, lane, k, L0);
+                const int t = tile_node3<NS, DIR, W>(warp, lane, k, L0);
                 const double un = DIR < 2 ? (m1f * S.vel[0][t] + m2f * S.vel[DIR < 2][t]) / sf
                                           : (m1f * S.vel[0][t]) / sf;
                 alpha = smax(alpha, sf * (fabs(un) + S.c[t]));
@@ -489,7 +494,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
                 double wp[W], wm[W];
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int t = tile_node3<DIR, W>(g, lane, k, L0);
+                    const int t = tile_node3<NS, DIR, W>(g, lane, k, L0);
                     wp[k] = 0.5 * (S.F[fl][t] + alpha * S.U[fl][t]);
                     wm[k] = 0.5 * (S.F[fl][t] - alpha * S.U[fl][t]);
                 }
@@ -511,13 +516,15 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         // work split of (a): 2W vectors over NC warps; the warps with one
         // vector fewer take the three LLF speeds
         const int rot = (warp + 3) % NC;
-        if (rot >= NC - 3 && !S.bad[face]) {
-            const int kind = NC - 1 - rot;  // 0: un - c, 1: un, 2: un + c
+        // the warps with one vector fewer (rot >= REM) take the three LLF
+        // speed kinds (0: un - c, 1: un, 2: un + c), two each if fewer than 3
+        constexpr int REM = NV % NC, NFEW = REM == 0 ? NC : NC - REM;
+        for (int kind = rot - REM; !S.bad[face] && kind >= 0 && kind < 3; kind += NFEW) {
             const double es = S.E[F3S][face];
             double alpha = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const int t = tile_node3<DIR, W>(g, lane, k, L0);
+                const int t = tile_node3<NS, DIR, W>(g, lane, k, L0);
                 const double unk =
                     DIR < 2 ? n1 * S.vel[0][t] + n2 * S.vel[DIR < 2][t] : n3 * S.vel[0][t];
                 const double ck = S.c[t];
@@ -541,7 +548,7 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
             (fdiv_pos_divisor_ok(c2) && fdiv_pos_divisor_ok(c2x2)) ? 0u : 1u;
         for (int vec = live ? rot : NV; vec < NV; vec += NC) {
             const int k = vec >> 1;
-            const int t = tile_node3<DIR, W>(g, lane, k, L0);
+            const int t = tile_node3<NS, DIR, W>(g, lane, k, L0);
             double q[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) q[c] = (vec & 1) ? S.U[c][t] : S.F[c][t];
