@@ -27,8 +27,9 @@
 namespace ign {
 
 // ---------------------------------------------------------------- ghost fill
-// fill_ghosts (boundary.hpp:136-258).  One thread per (edge, t) runs the
-// reference's k = 1..g loop.  x edges cover rows 0..ny-1 (launch 1), y edges
+// fill_ghosts (boundary.hpp:136-258).  One thread per (edge, t, ghost layer
+// k) (walls: per (edge, t), the reference's k = 1..g loop).  x edges cover rows
+// 0..ny-1 (launch 1), y edges
 // the full padded range -g..nx+g-1 (launch 2), so corners take the y rule.
 template <int NS, int TM>
 __device__ int bc_prim_at(const KParams& P, const double* Ut, int i, int j, Prim<NS>& pt,
@@ -66,13 +67,23 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
     const int g = P.g, nx = P.nx, ny = P.ny;
     const int tlo = ypass ? -g : 0;
     const int ntr = ypass ? nx + 2 * g : ny;
+    // one thread per (edge, t, ghost layer kk): the layers of an edge node are
+    // independent (each reads interior nodes only) except on walls, whose
+    // layers keep the reference's k order (a failing mirror stops the later
+    // layers), and periodic edges of lines shorter than g (the sources are
+    // ghosts): layer 1's thread runs the k loop there
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= 2 * ntr) return;
-    const int side = tid / ntr;  // 0: left/bottom, 1: right/top
-    const int t = tlo + tid % ntr;
+    const int kk = tid / (2 * ntr) + 1;  // layer-major: a warp's stores are coalesced
+    const int rid = tid % (2 * ntr);
+    if (kk > g) return;
+    const int side = rid / ntr;  // 0: left/bottom, 1: right/top
+    const int t = tlo + rid % ntr;
     const int edge = (ypass ? 2 : 0) + side;
     const int type = P.bc_type[edge];
     const int n = ypass ? ny : nx;
+    const bool serial = type == 1 || type == 2 || (type == 0 && n < g);
+    if (serial && kk != 1) return;
+    const int k_lo = serial ? 1 : kk, k_hi = serial ? g : kk;
     // ghost / mirror / wrap / interior index along the edge normal
     auto ij = [&](int a, int& i, int& j) {
         if (ypass) { i = t; j = a; } else { i = a; j = t; }
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
     case BC_HALO:  // internal slab edge: ghost rows arrived from the neighbour
         return;
     case BC_HALO_WRAP: {  // periodic wrap across slabs: Ut_dst = Ut_src * J_src/J_dst
-        for (int k = 1; k <= g; ++k) {
+        for (int k = k_lo; k <= k_hi; ++k) {
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
             const double ratio = P.wrap[side][(k - 1) * P.sx + (t + g)];
             const long long d = pidx(P, gi, gj);
@@ -96,7 +107,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
         return;
     }
     case 0: {  // Periodic (boundary.hpp:203-209)
-        for (int k = 1; k <= g; ++k) {
+        for (int k = k_lo; k <= k_hi; ++k) {
             int si, sj;
             ij(side == 0 ? n - k : k - 1, si, sj);
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
@@ -106,7 +117,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
     }
     case 1:
     case 2: {  // No-slip walls (boundary.hpp:210-226)
-        for (int k = 1; k <= g; ++k) {
+        for (int k = k_lo; k <= k_hi; ++k) {
             int mi, mj;
             ij(side == 0 ? k - 1 : n - k, mi, mj);
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
@@ -139,7 +150,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
             return;
         }
         const double* prof = P.inflow[edge] + (long long)(t - tlo) * g * (3 + NS);
-        for (int k = 1; k <= g; ++k) {
+        for (int k = k_lo; k <= k_hi; ++k) {
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
             const double* q = prof + (k - 1) * (3 + NS);
             Prim<NS> pt;
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(128) k_bc(const __grid_constant__ KParams P, d
     default: {  // Outflow (boundary.hpp:242-249)
         int ii, ji;
         ij(side == 0 ? 0 : n - 1, ii, ji);
-        for (int k = 1; k <= g; ++k) {
+        for (int k = k_lo; k <= k_hi; ++k) {
             ij(side == 0 ? -k : n - 1 + k, gi, gj);
             bc_copy_scaled<NS>(P, Ut, ii, ji, gi, gj);
         }
@@ -560,7 +571,7 @@ template <int NS> struct Launch {
     // the full padded width (ypass 1) — boundary.hpp:254-257
     static int bc(const KParams& P, double* Ut, int ypass, int stage, int step, cudaStream_t s) {
         const int n = ypass ? P.nx + 2 * P.g : P.ny;
-        const unsigned nb = (2 * n + 127) / 128;
+        const unsigned nb = (2 * n * P.g + 127) / 128;  // (edge, t, ghost layer)
         switch (thermo_mode<NS>(P.mix)) {
         case 1: k_bc<NS, 1><<<nb, 128, 0, s>>>(P, Ut, ypass, stage, step); break;
         case 2: k_bc<NS, 2><<<nb, 128, 0, s>>>(P, Ut, ypass, stage, step); break;

@@ -502,8 +502,10 @@ __device__ __forceinline__ void finish_node3(const KParams& P, const double* __r
 // EDGE = false: every padded node except, when LODI is on, the right-edge
 // column; EDGE = true: that column alone (grid over its (j, k)), with the LODI
 // x-flux difference — so the LODI code never enters the bulk update.
+// Bulk update, 1-4 species: 3 CTAs/SM (<= 80 registers; the finish_node3
+// factoring had let it grow to 104, 2 CTAs/SM, jet update +17%)
 template <int NS, int MODE, bool EDGE>
-__global__ void __launch_bounds__(256) k_assemble3(const __grid_constant__ KParams P,
+__global__ void __launch_bounds__(256, (NS <= 4 && !EDGE) ? 3 : 1) k_assemble3(const __grid_constant__ KParams P,
                                                    const double* __restrict__ U0,
                                                    const double* __restrict__ Ucur,
                                                    double* __restrict__ Uout, double dt,
