@@ -31,10 +31,10 @@
 
 namespace ign {
 
-// y tile width (columns): see FaceSmem::TW.  One species: 8 columns (the window's
-// halo lines shrink, one more CTA fits per SM); several: 32 (those kernels are
-// held at 2 CTAs/SM by registers, and the wider tile keeps the launch in
-// whole waves at 512^2)
+// y tile width (columns): see FaceSmem::TW.  One species: 8 columns (the
+// window's halo rows shrink, one more CTA fits per SM); several: 32 (those
+// CTAs are held at 2 CTAs/SM, and the wider tile keeps the launch in whole
+// waves at 512^2)
 template <int NS, int DIR> __host__ __device__ constexpr int tile_w() {
     return DIR == 0 || NS > 1 ? 32 : 8;
 }
@@ -45,7 +45,14 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
     static constexpr int NC = NS + 3;
     static constexpr int H = TENO ? 3 : 2;
     static constexpr int W = 2 * H;
-    static constexpr int NF = 32 * NC;  // faces per CTA
+    // groups of 32 faces per CTA: one per warp, except the x faces of
+    // multi-species tables (NC >= 6), whose CTA of NC warps owns 5 groups —
+    // the eigen table and window shrink so 3 CTAs/SM fit (phase 1 leaves the
+    // extra threads idle): H2/O2 x faces -5% (the y faces, held by their
+    // 32-column window, stay at NC groups and 2 CTAs/SM)
+    static constexpr int G = (NC >= 6 && DIR == 0) ? 5 : NC;
+    static constexpr int NTH = 32 * NC;  // threads
+    static constexpr int NF = 32 * G;    // faces per CTA
     // y tiles: TW columns x NF/TW face rows (few halo rows in the window)
     static constexpr int TW = tile_w<NS, DIR>();
     static constexpr int LINES = NF / TW;
@@ -66,7 +73,7 @@ template <int NS, int DIR, bool TENO, bool CHAR = true> struct FaceSmem {
     double Wc[NV_S][NA_S][32];
     double amp[NA_S][32];  // one group (phase 3 follows each group)
     double alpha[NK_S][32];  // per face of the group: LLF speeds of acoustic-, convective, acoustic+
-    int bad[NF];
+    unsigned char bad[NF];
 };
 
 // Eigen data slots in FaceSmem::E
@@ -102,11 +109,13 @@ template <int NS, int DIR, bool TENO, bool CHAR, int TM>
 #ifndef IGN_FACES_MINB
 #define IGN_FACES_MINB 4
 #endif
-__global__ void __launch_bounds__(32 * (NS + 3), (NS == 1 ? IGN_FACES_MINB : 1))
+__global__ void __launch_bounds__(32 * (NS + 3),
+                                  (NS == 1 ? IGN_FACES_MINB : (NS >= 3 && DIR == 0) ? 3 : 1))
 k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int stage, int step,
          int f_lo, int f_hi) {
     using Smem = FaceSmem<NS, DIR, TENO, CHAR>;
     constexpr int NC = Smem::NC, H = Smem::H, W = Smem::W, NF = Smem::NF, NT = Smem::NT;
+    constexpr int G = Smem::G, NTH = Smem::NTH;
     constexpr int NV = Smem::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -156,14 +165,14 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     // ---------------- phase 1a: node window -> shared memory
     if constexpr (CHAR) {
         // ---------------- phase 1a: node window -> shared memory.  Each thread
-        // stages NIT nodes (NIT = ceil(NT / NF)); every node's loads are issued
+        // stages NIT nodes (NIT = ceil(NT / NTH)); every node's loads are issued
         // before any is consumed, so their latencies overlap
-        constexpr int NIT = (NT + NF - 1) / NF;
+        constexpr int NIT = (NT + NTH - 1) / NTH;
         double raw[NIT][NC + 7];
         int slot_t[NIT];
     #pragma unroll
         for (int it = 0; it < NIT; ++it) {
-            const int t = threadIdx.x + it * NF;
+            const int t = threadIdx.x + it * NTH;
             long long id = 0;
             bool ok = t < NT;
             if (DIR == 0) {
@@ -263,8 +272,9 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         my_f = f0 + (int)threadIdx.x / TW;
         my_col = i0 + (int)threadIdx.x % TW;
     }
-    const bool my_active = DIR == 0 ? (my_f <= P.nx && my_col < P.ny)
-                                    : (my_col < P.nx && my_f < f_hi);
+    const bool my_slot = threadIdx.x < NF;  // the thread owns a face in phase 1
+    const bool my_active = my_slot && (DIR == 0 ? (my_f <= P.nx && my_col < P.ny)
+                                                : (my_col < P.nx && my_f < f_hi));
     const unsigned phase = DIR == 0 ? PH_INVX : PH_INVY;
     auto err_index = [&](int f, int col) -> unsigned long long {
         // global (line, face) order of inviscid_direction (solver.hpp:450-481)
@@ -318,7 +328,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
                 S.E[EY0 + NS + s][t] = es.Theta[s];
             }
         }
-        S.bad[threadIdx.x] = my_active ? bad : 1;
+        if (my_slot) S.bad[threadIdx.x] = my_active ? bad : 1;
     }
     if (threadIdx.x == 0) s_dead = dead0;
     __syncthreads();
@@ -342,7 +352,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
             }
             S.E[0][threadIdx.x] = alpha;
         }
-        S.bad[threadIdx.x] = bad;
+        if (my_slot) S.bad[threadIdx.x] = bad;
         __syncthreads();
     }
 
@@ -363,7 +373,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
     };
     if constexpr (!CHAR) {
         // componentwise: component fl of the LLF-split TENO sum
-        for (int g = 0; g < NC; ++g) {
+        for (int g = 0; g < G; ++g) {
             const int face = g * 32 + lane;
             if (S.bad[face]) continue;
             int f, col;
@@ -420,7 +430,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         }
         out[fl * fplane + out_at(f, col)] = r;
     };
-    for (int g = 0; g < NC; ++g) {
+    for (int g = 0; g < G; ++g) {
         if (g > 0) assemble_group(g - 1);
         const int face = g * 32 + lane;  // slot in the CTA
         const bool live = !S.bad[face];
@@ -524,7 +534,7 @@ k_faces3(const __grid_constant__ KParams P, const double* __restrict__ Ut, int s
         S.amp[fl][lane] = amp;
         __syncthreads();  // amp complete; Wc may be overwritten by the next group
     }
-    assemble_group(NC - 1);
+    assemble_group(G - 1);
 }
 
 template <int NS, int DIR, bool TENO, bool CHAR, int TM>
@@ -535,7 +545,7 @@ inline int launch_faces3_tm(const KParams& P, const double* Ut, int stage, int s
     auto kern = k_faces3<NS, DIR, TENO, CHAR, TM>;
     static std::atomic<unsigned long long> configured{0};  // per instantiation, per device
     configure_kernel(kern, smem, NC, configured, "k_faces3");
-    const int NF = 32 * NC;
+    const int NF = FaceSmem<NS, DIR, TENO, CHAR>::NF;
     if (f_hi < 0) f_hi = (DIR == 0 ? P.nx : P.ny) + 1;
     if (f_hi <= f_lo) return 0;
     dim3 grid;
