@@ -1,9 +1,9 @@
 # round-2 measurement pass after the face-kernel restructure (run under
 # gpurun): every bench case, the reference arm, the H2/O2 size scan against
 # the ensemble, the launch list of the default bench.  Outputs in gpurun_out/r2b/.
-mkdir -p gpurun_out/r2b
+mkdir -p gpurun_out/${R2B:-r2b}
 cd $GRAFT_REPO_ROOT
-D=gpurun_out/r2b
+D=gpurun_out/${R2B:-r2b}
 python bench.py > $D/bench_tgv3d.json 2> $D/bench_tgv3d.err || exit 1
 python bench.py --case tgv --no-cpu > $D/bench_tgv2d.json 2>/dev/null
 python bench.py --case h2o2 > $D/bench_h2o2.json 2>/dev/null
