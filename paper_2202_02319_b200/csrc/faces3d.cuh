@@ -546,7 +546,12 @@ k_faces3d(const __grid_constant__ KParams P, const double* __restrict__ Ut, int 
         const double c2x2 = 2.0 * c2, y2c2 = 0.5 * yc2;
         const unsigned den_bad =
             (fdiv_pos_divisor_ok(c2) && fdiv_pos_divisor_ok(c2x2)) ? 0u : 1u;
-        for (int vec = live ? rot : NV; vec < NV; vec += NC) {
+        // fixed trip count (the warp's 2-3 vectors): unrolled, the vectors'
+        // independent chains interleave
+#pragma unroll
+        for (int it = 0; it < (NV + NC - 1) / NC; ++it) {
+            const int vec = rot + it * NC;
+            if (!live || vec >= NV) continue;
             const int k = vec >> 1;
             const int t = tile_node3<NS, DIR, W>(g, lane, k, L0);
             double q[NC];
