@@ -455,6 +455,9 @@ def _inviscid(cfg):
 
 FULL3D = {
     "tgv3d_char_teno6": lambda: configs.tgv3d(16, nz=14, viscous=False),
+    # nx, ny not multiples of the 8-column y/z tiles, nz not of the 20-line
+    # blocks: partial tiles in every direction
+    "tgv3d_char_teno6_ragged": lambda: configs.tgv3d(18, nz=13, viscous=False),
     "tgv3d_comp_teno6": lambda: configs.tgv3d(16, nz=14, viscous=False, split="comp"),
     "tgv3d_char_weno3z": lambda: configs.tgv3d(16, nz=14, viscous=False, scheme="weno3z"),
     "tgv3d_comp_weno3z": lambda: configs.tgv3d(16, nz=14, viscous=False, scheme="weno3z",
