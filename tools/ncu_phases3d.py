@@ -1,5 +1,5 @@
 """Warp-stall samples and executed instructions of the 3D face kernels by phase
-(source-line attribution; line ranges of faces3d.cuh at commit 9afd489; dev tool).
+(source-line attribution; line ranges of faces3d.cuh at the round-2 final commit; dev tool).
 usage: ncu -i REPORT --page source --csv --print-source cuda,sass > /tmp/src_all.csv;
        python tools/ncu_phases3d.py 'k_faces3d<(int)1, (int)1'
 """
@@ -16,9 +16,9 @@ def phase(f, ln):
         if ln<424: return 'barrier1'
         if ln<479: return '3 assembly'
         if ln<505: return 'loop'
-        if ln<591: return '2a vectors+proj'
-        if ln<592: return 'barrier a'
-        if ln<615: return '2b field'
+        if ln<596: return '2a vectors+proj'
+        if ln<597: return 'barrier a'
+        if ln<620: return '2b field'
         return 'barrier b'
     if f=='physics.cuh':
         if ln>=650: return '2b TENO'
