@@ -301,6 +301,18 @@ void* ign_stream_handle(const ign_context* ctx);
  * (2 flops per FMA); the roofline denominator of the FP64-bound path. */
 int ign_probe_fp64_peak(int device, double* tflops);
 
+/* Red-zone guard (memory-safety check in place of compute-sanitizer, which
+ * the GPU pool does not run).  With IGN_GUARD=1 in the environment every
+ * device buffer a context allocates gets 32 KB of signalling-NaN canary on
+ * each side; frees and this call scan them.  *enabled = guard mode on,
+ * *checked = guarded buffers scanned so far (freed + live on the current
+ * device), *corrupted = canary words found overwritten (0 = no out-of-bounds
+ * write seen).  No reference counterpart. */
+int ign_guard_status(int* enabled, unsigned long long* checked, unsigned long long* corrupted);
+/* Detector self-test: writes one word past the end and one before the start
+ * of a guarded scratch buffer; *detected = canary words the scan saw changed (2). */
+int ign_guard_selftest(int device, unsigned long long* detected);
+
 /* ---- multi-GPU slabs --------------------------------------- */
 /* One process per GPU: rank 0 creates an NCCL unique id, every rank passes it
  * to ign_attach_nccl with its slab config (slab_count/slab_rank).  Halo rows

@@ -186,6 +186,8 @@ PRODUCT_ONLY = {
     "profile_read": (_I, [_P, _D, C.POINTER(C.c_int64)]),
     "stream_handle": (C.c_void_p, [_P]),
     "probe_fp64_peak": (_I, [_I, _D]),
+    "guard_status": (_I, [C.POINTER(C.c_int), C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
+    "guard_selftest": (_I, [_I, C.POINTER(C.c_ulonglong)]),
     "dims3": (_I, [_P, _I32P, _I32P, _I32P]),
     # multi-GPU slabs
     "nccl_unique_id": (_I, [C.c_char_p]),

@@ -24,6 +24,15 @@ extern "C" {
 
 uint64_t ign_config_size(void) { return sizeof(ign_config); }
 
+int ign_guard_status(int* enabled, unsigned long long* checked, unsigned long long* corrupted) {
+    return guarded_err(nullptr, -1, [&] { guard_status(enabled, checked, corrupted); });
+}
+
+int ign_guard_selftest(int device, unsigned long long* detected) {
+    if (!detected) return IGN_USAGE_ERROR;
+    return guarded_err(nullptr, device, [&] { *detected = guard_selftest(); });
+}
+
 int ign_create(const ign_config* cfg, ign_context** out) {
     if (!out) return IGN_USAGE_ERROR;
     *out = nullptr;

@@ -152,6 +152,10 @@ const char* pstatus_msg(unsigned sub);
 cudaEvent_t prof_event(ign_context* ctx);
 void prof_harvest(ign_context* ctx);
 double* dalloc(size_t n);
+void* dmalloc(size_t bytes);
+void dfree(void* p);
+void guard_status(int* enabled, unsigned long long* checked, unsigned long long* bad);
+unsigned long long guard_selftest();
 
 template <class F> int guarded_err(ign_error* err, int device, F&& f) {
     try {

@@ -42,10 +42,10 @@ void fold_ranks(const Team& T, std::vector<double>& acc,
                                    c->stream), "fold");
         cuda_check(cudaStreamSynchronize(c->stream), "fold");
     } catch (...) {
-        cudaFree(d);
+        dfree(d);
         throw;
     }
-    cudaFree(d);
+    dfree(d);
 }
 
 // ---------------------------------------------------------------- device tree sums
@@ -301,10 +301,10 @@ void t_sample(const Team& T) {
                 pr.rows.insert(pr.rows.end(), row.begin(), row.end());
             }
         } catch (...) {
-            cudaFree(d);
+            dfree(d);
             throw;
         }
-        cudaFree(d);
+        dfree(d);
     }
     if (want_trace) {
         L->trace_t.push_back(L->time);
@@ -365,7 +365,7 @@ void t_gather(const Team& T, bool tcache, std::vector<double>& out) {
             }
         }
     }
-    if (stage) cudaFree(stage);
+    if (stage) dfree(stage);
 }
 
 // write_snapshot (snapshot.hpp:52-76): version 1 = the reference's format

@@ -5,6 +5,10 @@
 // stable_dt; advance; the ensemble runner.
 #include "context_internal.hpp"
 
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+
 namespace ign {
 namespace rt {
 
@@ -94,10 +98,142 @@ void prof_harvest(ign_context* ctx) {
     ctx->prof_pending.clear();
 }
 
-double* dalloc(size_t n) {
-    void* p = nullptr;
-    cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)), "cudaMalloc");
-    return static_cast<double*>(p);
+// ---------------------------------------------------------------- allocation
+// Red-zone guard mode (IGN_GUARD=1 in the environment when a buffer is
+// allocated).  compute-sanitizer is closed on the GPU pool, so out-of-bounds
+// accesses are caught by the allocator instead: every device buffer of a
+// context gets kGuardWords words of canary on each side — a signalling-NaN bit
+// pattern, so a kernel that READS past a buffer and uses the value turns the
+// step non-finite (the error word / the oracle parity catch it), and a kernel
+// that WRITES past one changes a canary, which dfree() and ign_guard_status()
+// count.  Off by default (the product allocates exactly what it uses).
+namespace {
+constexpr size_t kGuardWords = 4096;  // 32 KB per side: the user pointer keeps 32 KB alignment
+constexpr unsigned long long kCanary = 0x7ff4dead0badf00dull;
+struct GuardRec {
+    char* base;
+    size_t words;  // user words (bytes rounded up to 8)
+};
+std::mutex g_guard_mu;
+std::unordered_map<void*, GuardRec> g_guard_live;
+unsigned long long g_guard_checked = 0, g_guard_bad = 0;
+
+bool guard_on() {
+    const char* e = std::getenv("IGN_GUARD");
+    return e && *e && *e != '0';
+}
+
+// canary words changed in the two zones of one buffer
+unsigned long long guard_scan(const GuardRec& r) {
+    std::vector<unsigned long long> h(kGuardWords);
+    unsigned long long bad = 0;
+    for (int side = 0; side < 2; ++side) {
+        const char* z = r.base + (side ? (kGuardWords + r.words) * 8 : 0);
+        cuda_check(cudaMemcpy(h.data(), z, kGuardWords * 8, cudaMemcpyDeviceToHost),
+                   "guard scan");
+        for (unsigned long long w : h) bad += w != kCanary;
+    }
+    return bad;
+}
+}  // namespace
+
+void* dmalloc(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 1);
+    if (!guard_on()) {
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+        return p;
+    }
+    GuardRec r{nullptr, (bytes + 7) / 8};
+    void* b = nullptr;
+    cuda_check(cudaMalloc(&b, (2 * kGuardWords + r.words) * 8), "cudaMalloc");
+    r.base = static_cast<char*>(b);
+    const std::vector<unsigned long long> can(kGuardWords, kCanary);
+    cuda_check(cudaMemcpy(r.base, can.data(), kGuardWords * 8, cudaMemcpyHostToDevice), "guard");
+    cuda_check(cudaMemcpy(r.base + (kGuardWords + r.words) * 8, can.data(), kGuardWords * 8,
+                          cudaMemcpyHostToDevice),
+               "guard");
+    void* user = r.base + kGuardWords * 8;
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guard_live[user] = r;
+    return user;
+}
+
+double* dalloc(size_t n) { return static_cast<double*>(dmalloc(n * sizeof(double))); }
+
+// Frees a dmalloc() buffer (nullptr is a no-op); a guarded one has its canaries
+// checked first (the device is synchronised so pending kernels have written).
+void dfree(void* p) {
+    if (!p) return;
+    GuardRec r{nullptr, 0};
+    {
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        auto it = g_guard_live.find(p);
+        if (it != g_guard_live.end()) {
+            r = it->second;
+            g_guard_live.erase(it);
+        }
+    }
+    if (!r.base) {
+        cudaFree(p);
+        return;
+    }
+    unsigned long long bad = 0;
+    if (cudaDeviceSynchronize() == cudaSuccess) {
+        try {
+            bad = guard_scan(r);
+        } catch (const Error&) {
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        ++g_guard_checked;
+        g_guard_bad += bad;
+        if (bad) std::fprintf(stderr, "ignis_b200 guard: %llu canary words overwritten around a "
+                                      "%zu-byte buffer\n", bad, r.words * 8);
+    }
+    cudaFree(r.base);
+}
+
+// Scans every live guarded buffer (of the current device) and reports the
+// totals including freed buffers.
+void guard_status(int* enabled, unsigned long long* checked, unsigned long long* bad) {
+    std::vector<GuardRec> live;
+    {
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        for (auto& kv : g_guard_live) live.push_back(kv.second);
+    }
+    cuda_check(cudaDeviceSynchronize(), "guard sync");
+    unsigned long long b = 0, n = 0;
+    for (const GuardRec& r : live) {
+        cudaPointerAttributes a{};
+        int dev = -1;
+        cudaGetDevice(&dev);
+        if (cudaPointerGetAttributes(&a, r.base) != cudaSuccess || a.device != dev) continue;
+        b += guard_scan(r);
+        ++n;
+    }
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    if (enabled) *enabled = guard_on() ? 1 : 0;
+    if (checked) *checked = g_guard_checked + n;
+    if (bad) *bad = g_guard_bad + b;
+}
+
+// Self-test of the detector: one guarded buffer, one word written past its end
+// and one before its start; returns the canary words the scan saw changed (2).
+unsigned long long guard_selftest() {
+    GuardRec r{nullptr, 3};
+    void* b = nullptr;
+    cuda_check(cudaMalloc(&b, (2 * kGuardWords + r.words) * 8), "cudaMalloc");
+    r.base = static_cast<char*>(b);
+    const std::vector<unsigned long long> can(2 * kGuardWords + r.words, kCanary);
+    cuda_check(cudaMemcpy(r.base, can.data(), can.size() * 8, cudaMemcpyHostToDevice), "guard");
+    double* user = reinterpret_cast<double*>(r.base + kGuardWords * 8);
+    cuda_check(cudaMemset(user + r.words, 0, 8), "guard");  // one past the end
+    cuda_check(cudaMemset(user - 1, 0, 8), "guard");        // one before the start
+    const unsigned long long bad = guard_scan(r);
+    cudaFree(b);
+    return bad;
 }
 
 // ---------------------------------------------------------------- teams

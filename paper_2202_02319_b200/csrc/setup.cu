@@ -128,20 +128,20 @@ void upload_state(ign_context* ctx, const std::vector<double>& Ut) {
 
 void destroy_impl(ign_context* ctx) {
     if (!ctx) return;
-    for (double* p : ctx->S) cudaFree(p);
-    cudaFree(ctx->prim);
-    cudaFree(ctx->geom);
-    cudaFree(ctx->Fx);
-    cudaFree(ctx->Gy);
-    cudaFree(ctx->Fv);
-    cudaFree(ctx->Gv);
-    cudaFree(ctx->Hz);
-    cudaFree(ctx->Hv);
-    cudaFree(ctx->rhs);
-    for (double* p : ctx->inflow) cudaFree(p);
-    for (double* p : ctx->wrap) cudaFree(p);
-    cudaFree(ctx->own_err);
-    cudaFree(ctx->red);
+    for (double* p : ctx->S) dfree(p);
+    dfree(ctx->prim);
+    dfree(ctx->geom);
+    dfree(ctx->Fx);
+    dfree(ctx->Gy);
+    dfree(ctx->Fv);
+    dfree(ctx->Gv);
+    dfree(ctx->Hz);
+    dfree(ctx->Hv);
+    dfree(ctx->rhs);
+    for (double* p : ctx->inflow) dfree(p);
+    for (double* p : ctx->wrap) dfree(p);
+    dfree(ctx->own_err);
+    dfree(ctx->red);
     for (auto& r : ctx->prof_pending) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -150,7 +150,7 @@ void destroy_impl(ign_context* ctx) {
     if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
-    if (ctx->diag_buf) cudaFree(ctx->diag_buf);
+    if (ctx->diag_buf) dfree(ctx->diag_buf);
     if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     delete ctx;
@@ -329,12 +329,11 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
                               cudaMemcpyHostToDevice),
                    "wrap upload");
     }
-    void* p = nullptr;
-    cuda_check(cudaMalloc(&p, sizeof(ErrRec)), "cudaMalloc");
+    void* p = dmalloc(sizeof(ErrRec));
     ctx->own_err = static_cast<ErrRec*>(p);
     ctx->err = ctx->own_err;
     cuda_check(cudaMemset(ctx->err, 0xff, sizeof(ErrRec)), "memset");
-    cuda_check(cudaMalloc(&p, kRedSlots * sizeof(unsigned long long)), "cudaMalloc");
+    p = dmalloc(kRedSlots * sizeof(unsigned long long));
     ctx->red = static_cast<unsigned long long*>(p);
     cuda_check(cudaMemset(ctx->red, 0, kRedSlots * sizeof(unsigned long long)), "memset");
 

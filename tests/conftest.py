@@ -42,3 +42,32 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return 0
+
+
+def guard_status(api):
+    """(enabled, buffers checked, canary words overwritten) of the red-zone
+    guard (IGN_GUARD=1; runtime.cu dmalloc/dfree)."""
+    import ctypes as C
+    en, chk, bad = C.c_int(), C.c_ulonglong(), C.c_ulonglong()
+    st = api["guard_status"](C.byref(en), C.byref(chk), C.byref(bad))
+    assert st == 0, st
+    return en.value, chk.value, bad.value
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Under IGN_GUARD=1 the whole session is a memory-safety run: fail it if
+    any device buffer's red zone was overwritten."""
+    if not os.environ.get("IGN_GUARD"):
+        return
+    from paper_2202_02319_b200 import native
+    if native._lib is None:  # the library never loaded (CPU-only session)
+        return
+    en, chk, bad = guard_status(native.api())
+    msg = f"ignis_b200 guard: enabled={en} buffers_checked={chk} corrupted_words={bad}"
+    print("\n" + msg)
+    out = os.environ.get("IGN_GUARD_REPORT")
+    if out:
+        with open(out, "w") as f:
+            f.write(msg + "\n")
+    if bad:
+        session.exitstatus = 1

@@ -1,7 +1,9 @@
 """Small cases over every kernel family for compute-sanitizer (one tool per
 call): 2D gamma-gas TENO6 char + viscous, 2D H2/O2 inflow/outflow/laser (WENO3Z
 comp too), 3D TGV, the 3D jet (inflow, LODI, walls, shaped 3D laser), slab
-groups (2D and 3D, halo overlap) and the ensemble runner."""
+groups (2D and 3D, halo overlap) and the ensemble runner.  compute-sanitizer
+is closed on the GPU pool: run with IGN_GUARD=1 (red-zone allocator) instead;
+the script exits 1 if any buffer's canaries were overwritten."""
 import sys
 sys.path.insert(0, '.')
 from paper_2202_02319_b200 import Ensemble, Simulation, configs
@@ -47,4 +49,12 @@ for m, c in zip(ens.members, configs.ensemble_members(4, nxy=(40, 20), count=2))
     m.prepare_stage(1)
 ens.rk3_steps(1e-8, 2)
 ens.close()
+# red-zone guard (IGN_GUARD=1): every freed and live buffer's canaries
+import ctypes as C  # noqa: E402
+from paper_2202_02319_b200 import native  # noqa: E402
+en, chk, bad = C.c_int(), C.c_ulonglong(), C.c_ulonglong()
+native.api()["guard_status"](C.byref(en), C.byref(chk), C.byref(bad))
+print(f"guard enabled={en.value} buffers_checked={chk.value} corrupted_words={bad.value}")
+if bad.value:
+    sys.exit(1)
 print("sanitize cases ok")
