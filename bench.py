@@ -328,11 +328,24 @@ def run_ensemble(args, rank, world, local, dist):
 
     def timed_steps():
         # members' states together fit in L2: flush before every timed step
-        tot = 0.0
+        # (streams[0], after every member's previous step), then an event pair
+        # per step spanning all member streams; no host sync between steps
+        torch.cuda.synchronize()
+        marks = []
         for _ in range(args.steps):
             l2_flush(streams[0], local)
-            tot += timed(lambda: ens.rk3_steps(dts, 1))
-        return tot
+            a = torch.cuda.Event(enable_timing=True)
+            a.record(streams[0])
+            for st in streams[1:]:
+                st.wait_event(a)
+            ens.rk3_steps(dts, 1)
+            ends = [torch.cuda.Event(enable_timing=True) for _ in streams]
+            for e, st in zip(ends, streams):
+                e.record(st)
+                streams[0].wait_event(e)
+            marks.append((a, ends))
+        torch.cuda.synchronize()
+        return sum(max(a.elapsed_time(e) for e in ends) for a, ends in marks)
 
     def timed(fn):
         ev0 = torch.cuda.Event(enable_timing=True)

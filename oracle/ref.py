@@ -76,3 +76,21 @@ def inviscid_rhs3(cfg: abi.Config, Ut, prim):
     if st != abi.IGN_OK:
         raise RuntimeError(f"ref3d: status {st}: {err.msg.decode()}")
     return out
+
+
+def viscous_rhs3(cfg: abi.Config, prim):
+    """The 3D extension's viscous divergence (dVx + dVy) + dVz from
+    oracle/ref3d_viscous.hpp (the reference's compute_viscous restated with the
+    z terms) for the product's primitive cache; interior written, ghosts 0."""
+    import numpy as np
+    f = lib().ignref3d_viscous_rhs
+    f.argtypes = [C.POINTER(abi.Config), C.c_void_p, C.c_void_p, C.POINTER(abi.Error)]
+    f.restype = C.c_int
+    prim = np.ascontiguousarray(prim, dtype=np.float64)
+    nc = cfg.mix.ns + 4
+    out = np.zeros((nc,) + prim.shape[1:], dtype=np.float64)
+    err = abi.Error()
+    st = f(C.byref(cfg), prim.ctypes.data, out.ctypes.data, C.byref(err))
+    if st != abi.IGN_OK:
+        raise RuntimeError(f"ref3d: status {st}: {err.msg.decode()}")
+    return out

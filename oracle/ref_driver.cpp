@@ -21,6 +21,7 @@
 #include "ignis_b200.h"
 
 #include "ref3d_faces.hpp"
+#include "ref3d_viscous.hpp"
 
 using namespace ignis;
 
@@ -441,6 +442,24 @@ int ignref3d_inviscid_rhs(const ign_config* cfg, const double* Ut, const double*
         G.sxy = G.sx * (cfg->ny + 2 * cfg->g);
         G.plane = G.sxy * (cfg->nz + 2 * cfg->g);
         ref3d::inviscid_rhs(G, M, mix, sc, Ut, prim, rhs);
+    });
+}
+
+// The 3D extension's viscous divergence (oracle/ref3d_viscous.hpp) from the
+// product's primitive cache; interior of the returned planes written.
+int ignref3d_viscous_rhs(const ign_config* cfg, const double* prim, double* dv,
+                         ign_error* err) {
+    return guarded(err, [&] {
+        if (cfg->nz <= 0) throw UsageError("ref3d: nz must be > 0");
+        const Mesh mesh = make_mesh(*cfg);
+        const MetricField metv = compute_metrics(mesh, MetricMode::Central2);
+        const ref3d::Met3 Mv = ref3d::extrude(metv, cfg->lz / cfg->nz);
+        const MixtureModel mix = to_mix(cfg->mix);
+        ref3d::Grid G{cfg->nx, cfg->ny, cfg->nz, cfg->g, mix.ns(), 0, 0, 0};
+        G.sx = cfg->nx + 2 * cfg->g;
+        G.sxy = G.sx * (cfg->ny + 2 * cfg->g);
+        G.plane = G.sxy * (cfg->nz + 2 * cfg->g);
+        ref3d::viscous_rhs(G, Mv, mix, prim, dv);
     });
 }
 

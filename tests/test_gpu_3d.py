@@ -502,6 +502,73 @@ def test_full_3d_faces_bitwise_vs_ref3d(name, oracle_api, cuda_device):
         np.abs(a - b).max(axis=(1, 2, 3))
 
 
+# ---------------------------------------------- fully 3D viscous vs ref3d
+def _viscous_only(cfg):
+    c = clone_cfg(cfg)
+    c.viscous = 1
+    c.mech.present = 0
+    c.laser.present = 0
+    return c
+
+
+def _species3d_visc():
+    case = configs.extrude_z(configs.species_box(4, 16), 12)
+    case.cfg.lz = 0.01 * 12 / 16  # dz = dx
+    return case
+
+
+def _skew3d_visc():
+    case = configs.extrude_z(configs.tgv2d(16, skew=0.08), 12)
+    case.cfg.lz = 2.0 * np.pi * 12 / 16  # dz = dx
+    return case
+
+
+VISC3D = {
+    "tgv3d_visc": lambda: configs.tgv3d(16, nz=14),
+    "tgv3d_visc_ragged": lambda: configs.tgv3d(18, nz=13),
+    "tgv_skew_visc": _skew3d_visc,
+    "h2o2_4sp_visc": _species3d_visc,
+}
+
+
+@pytest.mark.parametrize("name", sorted(VISC3D))
+def test_full_3d_viscous_rhs_bitwise_vs_ref3d(name, oracle_api, cuda_device):
+    """The viscous node kernel k_visc3 and the viscous part of the update
+    (k_assemble3) on a genuinely 3D state (w != 0, z variation) against
+    oracle/ref3d_viscous.hpp — the reference's compute_viscous restated with
+    the z terms, serial, with the reference's own transport() / thermo — plus
+    the ref3d inviscid RHS: the full RHS of BASELINE configs[1]'s viscous path
+    BITWISE (until now anchored on z-extrusions and an x-z plane at 1e-11)."""
+    from oracle import ref
+    case = VISC3D[name]()
+    case.cfg = _viscous_only(case.cfg)
+    sim = _fully_3d(case)
+    Ut = sim.Ut
+    names = ("rho", "u", "v", "w", "p", "T", "c")
+    cache = sim.cache()
+    prim = np.concatenate([np.stack([cache[k] for k in names]), cache["Y"]])
+    got = sim.compute_rhs(0.0, 1)
+    inv = ref.inviscid_rhs3(case.cfg, Ut, prim)
+    dv = ref.viscous_rhs3(case.cfg, prim)
+    want = inv + dv  # r = -((dF + dG) + dH); r += (dVx + dVy) + dVz
+    g = sim.g
+    a, b = got[:, g:-g, g:-g, g:-g], want[:, g:-g, g:-g, g:-g]
+    d = dv[:, g:-g, g:-g, g:-g]
+    ns = case.cfg.mix.ns
+    assert np.abs(d[ns + 2]).max() > 0.0  # z-momentum viscous flux moves
+    assert np.abs(d[ns + 3]).max() > 0.0
+    if ns == 1:
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), \
+            np.abs(a - b).max(axis=(1, 2, 3))
+    else:
+        # Wilke's pow(T/T_ref, n) and pow(W_j/W_i, 1/4) (thermo.hpp:235-250)
+        # are not correctly rounded on the device: last-ulp differences, the
+        # 2D species cases' RHS gate (test_gpu_species.py RHS_TOL)
+        scale = np.abs(b).max(axis=(1, 2, 3))
+        err = np.abs(a - b).max(axis=(1, 2, 3)) / np.where(scale > 0, scale, 1.0)
+        assert err.max() <= 1e-13, err
+
+
 def test_z_edge_validation(cuda_device):
     """z edges: periodic_z needs periodic zlo / zhi, a bounded z needs walls or
     outflow on both sides (inflow is not supported on z edges)."""
