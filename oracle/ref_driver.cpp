@@ -22,6 +22,7 @@
 
 #include "ref3d_faces.hpp"
 #include "ref3d_viscous.hpp"
+#include "ref3d_step.hpp"
 
 using namespace ignis;
 
@@ -460,6 +461,42 @@ int ignref3d_viscous_rhs(const ign_config* cfg, const double* prim, double* dv,
         G.sxy = G.sx * (cfg->ny + 2 * cfg->g);
         G.plane = G.sxy * (cfg->nz + 2 * cfg->g);
         ref3d::viscous_rhs(G, Mv, mix, prim, dv);
+    });
+}
+
+// n advance() steps of the 3D extension on a fully periodic box
+// (oracle/ref3d_step.hpp) from the product's state and primitive cache
+// (Ut: nc planes, prim: rho, u, v, w, p, T, c, Y_s planes; both in/out).
+int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double dt, int n,
+                   ign_error* err) {
+    return guarded(err, [&] {
+        if (cfg->nz <= 0) throw UsageError("ref3d: nz must be > 0");
+        const ign_edge* e[4] = {&cfg->bc.left, &cfg->bc.right, &cfg->bc.bottom, &cfg->bc.top};
+        for (const ign_edge* x : e)
+            if (x->type != 0) throw UsageError("ref3d_steps: periodic x / y edges only");
+        if (!cfg->periodic_z) throw UsageError("ref3d_steps: periodic z only");
+        if (cfg->mech.present || cfg->laser.present)
+            throw UsageError("ref3d_steps: no chemistry / laser");
+        const Mesh mesh = make_mesh(*cfg);
+        const SchemeConfig sc = to_scheme(cfg->scheme);
+        const double dz = cfg->lz / cfg->nz;
+        ref3d::Run3 R;
+        R.M = ref3d::extrude(compute_metrics(mesh, inviscid_mode(*cfg, sc), cfg->skew_beta), dz);
+        R.Mv = ref3d::extrude(compute_metrics(mesh, MetricMode::Central2), dz);
+        R.mix = to_mix(cfg->mix);
+        R.sc = sc;
+        R.viscous = cfg->viscous != 0;
+        ref3d::Grid& G = R.G;
+        G = ref3d::Grid{cfg->nx, cfg->ny, cfg->nz, cfg->g, R.mix.ns(), 0, 0, 0};
+        G.sx = cfg->nx + 2 * cfg->g;
+        G.sxy = G.sx * (cfg->ny + 2 * cfg->g);
+        G.plane = G.sxy * (cfg->nz + 2 * cfg->g);
+        const size_t nU = size_t(G.ns + 4) * G.plane, nP = size_t(G.ns + 7) * G.plane;
+        R.Ut.assign(Ut, Ut + nU);
+        R.prim.assign(prim, prim + nP);
+        R.steps(dt, n);
+        std::copy(R.Ut.begin(), R.Ut.end(), Ut);
+        std::copy(R.prim.begin(), R.prim.end(), prim);
     });
 }
 

@@ -569,6 +569,61 @@ def test_full_3d_viscous_rhs_bitwise_vs_ref3d(name, oracle_api, cuda_device):
         assert err.max() <= 1e-13, err
 
 
+# ------------------------------------- fully 3D trajectories vs ref3d_step
+STEPS3D = {
+    "tgv3d_visc_char_teno6": lambda: configs.tgv3d(16, nz=14),
+    "tgv3d_visc_ragged": lambda: configs.tgv3d(18, nz=13),
+    "tgv3d_visc_comp_weno3z": lambda: configs.tgv3d(16, nz=14, scheme="weno3z", split="comp"),
+    "tgv_skew_visc": _skew3d_visc,
+    "h2o2_4sp_visc": _species3d_visc,
+}
+
+
+@pytest.mark.parametrize("name", sorted(STEPS3D))
+def test_3d_steps_vs_ref3d(name, oracle_api, cuda_device):
+    """Ten rk3_steps of the whole 3D path — ghost fill (x, y, z periodic
+    edges), primitives with the T cache, the three face kernels, the viscous
+    kernels, the fused update / clip — from a genuinely 3D state against
+    oracle/ref3d_step.hpp, the reference's advance() loop body restated with
+    the z terms: state and T cache over the whole padded box BITWISE for the
+    gamma-gas (BASELINE configs[1]'s path); 4 species <= 1e-10 (device pow in
+    Wilke's rule)."""
+    _steps_check(STEPS3D[name](), 10)
+
+
+@pytest.mark.slow
+def test_3d_steps_vs_ref3d_64cube_20_steps(oracle_api, cuda_device):
+    """The same at 64^3 (262k cells: several waves of every face kernel), 20
+    steps: BASELINE configs[1]'s path bitwise over a longer trajectory."""
+    _steps_check(configs.tgv3d(64, nz=64), 20)
+
+
+def _steps_check(case, n):
+    from oracle import ref
+    case.cfg = _viscous_only(case.cfg)
+    sim = _fully_3d(case, n_steps=0)
+    names = ("rho", "u", "v", "w", "p", "T", "c")
+
+    def prim_of(s):
+        cache = s.cache()
+        return np.concatenate([np.stack([cache[k] for k in names]), cache["Y"]])
+    U0, P0 = sim.Ut, prim_of(sim)
+    sim.rk3_steps(case.dt, n)
+    want_U, want_P = ref.steps3(case.cfg, U0, P0, case.dt, n)
+    got_U, got_P = sim.Ut, prim_of(sim)
+    assert np.abs(got_U - U0).max() > 0.0
+    ns = case.cfg.mix.ns
+    if ns == 1:
+        assert np.array_equal(got_U.view(np.uint64), want_U.view(np.uint64)), \
+            np.abs(got_U - want_U).max(axis=(1, 2, 3))
+        assert np.array_equal(got_P[5].view(np.uint64), want_P[5].view(np.uint64))
+    else:
+        scale = np.abs(want_U).max(axis=(1, 2, 3))
+        err = np.abs(got_U - want_U).max(axis=(1, 2, 3)) / np.where(scale > 0, scale, 1.0)
+        assert err.max() <= 1e-10, err
+        assert np.abs(got_P[5] - want_P[5]).max() <= 1e-10 * np.abs(want_P[5]).max()
+
+
 def test_z_edge_validation(cuda_device):
     """z edges: periodic_z needs periodic zlo / zhi, a bounded z needs walls or
     outflow on both sides (inflow is not supported on z edges)."""
