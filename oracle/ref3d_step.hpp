@@ -1,14 +1,17 @@
 // oracle/ref3d_step.hpp — TEST INFRASTRUCTURE (CPU checker, never the product).
 //
-// The reference's time loop restated for the 3D extension on fully periodic
-// boxes (BASELINE configs[1], the TGV): the advance() loop body
+// The reference's time loop restated for the 3D extension (BASELINE
+// configs[1], the TGV, and walled / outflow boxes — configs[3]'s edge rules):
+// the advance() loop body
 // (solver.hpp:336-345) — rk3_step (:304-332) with compute_rhs (:185-232, no
 // chemistry / laser), axpy / blend on the interior, post_stage (:826-849:
 // clip, finiteness, prepare_stage of the next stage) and the trailing
 // prepare_stage(1) — where prepare_stage (:422-425) is fill_ghosts
-// (boundary.hpp:203-209 periodic copies scaled by J_src/J_dst on the x edges
-// over rows 0..ny-1, the y edges over the padded width, then the z edges over
-// the padded (x, y) plane) and refresh_primitives (:148-178) on every padded
+// (boundary.hpp:136-258: periodic copies scaled by J_src/J_dst, no-slip walls
+// with every velocity component negated, outflow copies; the x edges over rows
+// 0..ny-1, the y edges over the padded width, then the z edges over the padded
+// (x, y) plane; inflow and the right-edge LODI are not restated) and
+// refresh_primitives (:148-178) on every padded
 // node with the T cache as the Newton guess.  3D expressions follow the
 // extension's convention ("the reference's 2D expression, then the z terms":
 // e = E/rho - 0.5 ((u u + v v) + w w)); the RHS is ref3d::inviscid_rhs +
@@ -38,7 +41,68 @@ struct Run3 {
     double& U(int c, long id) { return Ut[size_t(c) * G.plane + id]; }
     double& Pf(int f, long id) { return prim[size_t(f) * G.plane + id]; }
 
-    // fill_ghosts, periodic edges (boundary.hpp:203-209, :254-257 order)
+    // edge rules: x / y edges left, right, bottom, top; z edges back, front
+    // (0 periodic, 1 no-slip isothermal, 2 no-slip adiabatic, 4 outflow)
+    int etype[4] = {0, 0, 0, 0}, ztype[2] = {0, 0};
+    double Twall[4] = {0, 0, 0, 0}, Tzwall[2] = {0, 0};
+
+    // primitives_from_conservative (state.hpp:26-44) + w at a node, guess 300 K
+    struct Prim {
+        double rho, u, v, w, p, T;
+        SpeciesArray Y;
+    };
+    Prim prim_at(int i, int j, int k) {
+        const int ns = G.ns;
+        const long id = G.at(i, j, k);
+        const double J = M.jac[G.at2(i, j)];
+        std::vector<double> Uc(nc());
+        for (int c = 0; c < nc(); ++c) Uc[c] = U(c, id) * J;
+        Prim pt{};
+        double rho = 0.0;
+        for (int s = 0; s < ns; ++s) rho += Uc[s];
+        if (!(rho > 0.0)) throw ignis::StateError("primitives: non-positive density");
+        pt.rho = rho;
+        for (int s = 0; s < ns; ++s) pt.Y[s] = Uc[s] / rho;
+        pt.u = Uc[ns] / rho;
+        pt.v = Uc[ns + 1] / rho;
+        pt.w = Uc[ns + 2] / rho;
+        const double e = Uc[ns + 3] / rho - 0.5 * ((pt.u * pt.u + pt.v * pt.v) + pt.w * pt.w);
+        pt.T = ignis::temperature_from_energy(e, pt.Y, mix, 300.0);
+        pt.p = pt.rho * ignis::thermo::r_specific(pt.Y, mix) * pt.T;
+        return pt;
+    }
+    // store_prim (boundary.hpp:158-162) with conservative_from_primitives
+    // (state.hpp:47-57) + w
+    void store_prim(const Prim& pt, int i, int j, int k) {
+        const int ns = G.ns;
+        std::vector<double> Uc(nc());
+        for (int s = 0; s < ns; ++s) Uc[s] = pt.rho * pt.Y[s];
+        Uc[ns] = pt.rho * pt.u;
+        Uc[ns + 1] = pt.rho * pt.v;
+        Uc[ns + 2] = pt.rho * pt.w;
+        const double e = ignis::thermo::e_mass(pt.T, pt.Y, mix);
+        Uc[ns + 3] = pt.rho * (e + 0.5 * ((pt.u * pt.u + pt.v * pt.v) + pt.w * pt.w));
+        const double invJ = 1.0 / M.jac[G.at2(i, j)];
+        const long id = G.at(i, j, k);
+        for (int c = 0; c < nc(); ++c) U(c, id) = Uc[c] * invJ;
+    }
+    // no-slip wall (boundary.hpp:210-226): mirror, every velocity component negated
+    void wall(int type, double Tw, int im, int jm, int km, int ig, int jg, int kg) {
+        Prim pt = prim_at(im, jm, km);
+        pt.u = -pt.u;
+        pt.v = -pt.v;
+        pt.w = -pt.w;
+        if (type == 1) {
+            const double tg = 2.0 * Tw - pt.T;
+            pt.T = std::max(tg, 0.05 * Tw);
+        }
+        pt.rho = pt.p / (ignis::thermo::r_specific(pt.Y, mix) * pt.T);
+        store_prim(pt, ig, jg, kg);
+    }
+
+    // fill_ghosts (boundary.hpp:136-258) + z: the x edges over rows 0..ny-1,
+    // the y edges over the padded width (every interior plane), then the z
+    // edges over the padded (x, y) plane
     void fill_ghosts() {
         const int g = G.g, nx = G.nx, ny = G.ny, nz = G.nz;
         auto copy = [&](int is, int js, int ks, int id_, int jd, int kd) {
@@ -46,24 +110,44 @@ struct Run3 {
             const long s = G.at(is, js, ks), d = G.at(id_, jd, kd);
             for (int c = 0; c < nc(); ++c) U(c, d) = U(c, s) * ratio;
         };
-        for (int k = 0; k < nz; ++k)  // x edges, rows 0..ny-1
-            for (int j = 0; j < ny; ++j)
-                for (int l = 1; l <= g; ++l) {
-                    copy(nx - l, j, k, -l, j, k);
-                    copy(l - 1, j, k, nx - 1 + l, j, k);
+        // edge e (0 left, 1 right, 2 bottom, 3 top), transverse t, plane k
+        auto edge = [&](int e, int t, int k) {
+            const bool xe = e < 2, lo = e % 2 == 0;
+            const int n = xe ? nx : ny;
+            auto ij = [&](int a, int& i, int& j) {
+                if (xe) { i = a; j = t; } else { i = t; j = a; }
+            };
+            for (int l = 1; l <= g; ++l) {
+                int gi, gj, si, sj;
+                ij(lo ? -l : n - 1 + l, gi, gj);
+                switch (etype[e]) {
+                case 0: ij(lo ? n - l : l - 1, si, sj); copy(si, sj, k, gi, gj, k); break;
+                case 1:
+                case 2: ij(lo ? l - 1 : n - l, si, sj); wall(etype[e], Twall[e], si, sj, k, gi, gj, k); break;
+                case 4: ij(lo ? 0 : n - 1, si, sj); copy(si, sj, k, gi, gj, k); break;
+                default: throw std::runtime_error("ref3d_step: unsupported edge type");
                 }
-        for (int k = 0; k < nz; ++k)  // y edges, the padded width
-            for (int i = -g; i < nx + g; ++i)
-                for (int l = 1; l <= g; ++l) {
-                    copy(i, ny - l, k, i, -l, k);
-                    copy(i, l - 1, k, i, ny - 1 + l, k);
-                }
-        for (int j = -g; j < ny + g; ++j)  // z edges, the padded (x, y) plane
-            for (int i = -g; i < nx + g; ++i)
-                for (int l = 1; l <= g; ++l) {
-                    copy(i, j, nz - l, i, j, -l);
-                    copy(i, j, l - 1, i, j, nz - 1 + l);
-                }
+            }
+        };
+        for (int e = 0; e < 2; ++e)
+            for (int k = 0; k < nz; ++k)
+                for (int j = 0; j < ny; ++j) edge(e, j, k);
+        for (int e = 2; e < 4; ++e)
+            for (int k = 0; k < nz; ++k)
+                for (int i = -g; i < nx + g; ++i) edge(e, i, k);
+        for (int side = 0; side < 2; ++side)
+            for (int j = -g; j < ny + g; ++j)
+                for (int i = -g; i < nx + g; ++i)
+                    for (int l = 1; l <= g; ++l) {
+                        const int kg = side == 0 ? -l : nz - 1 + l;
+                        switch (ztype[side]) {
+                        case 0: copy(i, j, side == 0 ? nz - l : l - 1, i, j, kg); break;
+                        case 1:
+                        case 2: wall(ztype[side], Tzwall[side], i, j, side == 0 ? l - 1 : nz - l, i, j, kg); break;
+                        case 4: copy(i, j, side == 0 ? 0 : nz - 1, i, j, kg); break;
+                        default: throw std::runtime_error("ref3d_step: unsupported z edge type");
+                        }
+                    }
     }
 
     // refresh_primitives (solver.hpp:148-178) + z

@@ -464,7 +464,7 @@ int ignref3d_viscous_rhs(const ign_config* cfg, const double* prim, double* dv,
     });
 }
 
-// n advance() steps of the 3D extension on a fully periodic box
+// n advance() steps of the 3D extension (periodic, wall and non-LODI outflow edges)
 // (oracle/ref3d_step.hpp) from the product's state and primitive cache
 // (Ut: nc planes, prim: rho, u, v, w, p, T, c, Y_s planes; both in/out).
 int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double dt, int n,
@@ -472,9 +472,11 @@ int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double dt, i
     return guarded(err, [&] {
         if (cfg->nz <= 0) throw UsageError("ref3d: nz must be > 0");
         const ign_edge* e[4] = {&cfg->bc.left, &cfg->bc.right, &cfg->bc.bottom, &cfg->bc.top};
-        for (const ign_edge* x : e)
-            if (x->type != 0) throw UsageError("ref3d_steps: periodic x / y edges only");
-        if (!cfg->periodic_z) throw UsageError("ref3d_steps: periodic z only");
+        for (int q = 0; q < 4; ++q) {
+            const int t = e[q]->type;
+            if (t == 3 || (q == 1 && t == 4))  // inflow; right outflow = LODI
+                throw UsageError("ref3d_steps: no inflow / right-edge outflow (LODI)");
+        }
         if (cfg->mech.present || cfg->laser.present)
             throw UsageError("ref3d_steps: no chemistry / laser");
         const Mesh mesh = make_mesh(*cfg);
@@ -486,6 +488,18 @@ int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double dt, i
         R.mix = to_mix(cfg->mix);
         R.sc = sc;
         R.viscous = cfg->viscous != 0;
+        for (int q = 0; q < 4; ++q) {
+            R.etype[q] = e[q]->type;
+            R.Twall[q] = e[q]->T_wall;
+        }
+        if (!cfg->periodic_z) {
+            R.ztype[0] = cfg->zlo.type;
+            R.ztype[1] = cfg->zhi.type;
+            R.Tzwall[0] = cfg->zlo.T_wall;
+            R.Tzwall[1] = cfg->zhi.T_wall;
+            if (R.ztype[0] == 0 || R.ztype[1] == 0 || R.ztype[0] == 3 || R.ztype[1] == 3)
+                throw UsageError("ref3d_steps: z edges periodic_z or walls / outflow");
+        }
         ref3d::Grid& G = R.G;
         G = ref3d::Grid{cfg->nx, cfg->ny, cfg->nz, cfg->g, R.mix.ns(), 0, 0, 0};
         G.sx = cfg->nx + 2 * cfg->g;

@@ -570,7 +570,33 @@ def test_full_3d_viscous_rhs_bitwise_vs_ref3d(name, oracle_api, cuda_device):
 
 
 # ------------------------------------- fully 3D trajectories vs ref3d_step
+def _duct3d(outflow=False):
+    """The TGV box walled (configs[3]'s edge rules on fully 3D data): isothermal
+    bottom / back walls, adiabatic top / front walls; outflow=True swaps x
+    periodicity for a left outflow / right wall and the back wall for an
+    outflow z edge (the right-edge outflow is LODI, not restated in ref3d)."""
+    case = configs.tgv3d(16, nz=14)
+    cfg = case.cfg
+    T0 = float(np.mean(case.ic(np.zeros(4), np.zeros(4), np.zeros(4))[4]))
+    cfg.periodic_y = 0
+    cfg.periodic_z = 0
+    cfg.bc.bottom.type = abi.NOSLIP_ISOTHERMAL
+    cfg.bc.bottom.T_wall = 1.05 * T0
+    cfg.bc.top.type = abi.NOSLIP_ADIABATIC
+    cfg.zlo.type = abi.NOSLIP_ISOTHERMAL
+    cfg.zlo.T_wall = 0.97 * T0
+    cfg.zhi.type = abi.NOSLIP_ADIABATIC
+    if outflow:
+        cfg.periodic_x = 0
+        cfg.bc.left.type = abi.OUTFLOW
+        cfg.bc.right.type = abi.NOSLIP_ADIABATIC
+        cfg.zlo.type = abi.OUTFLOW
+    return case
+
+
 STEPS3D = {
+    "duct3d_walls": _duct3d,
+    "duct3d_walls_outflow": lambda: _duct3d(outflow=True),
     "tgv3d_visc_char_teno6": lambda: configs.tgv3d(16, nz=14),
     "tgv3d_visc_ragged": lambda: configs.tgv3d(18, nz=13),
     "tgv3d_visc_comp_weno3z": lambda: configs.tgv3d(16, nz=14, scheme="weno3z", split="comp"),
