@@ -96,19 +96,19 @@ def viscous_rhs3(cfg: abi.Config, prim):
     return out
 
 
-def steps3(cfg: abi.Config, Ut, prim, dt: float, n: int):
+def steps3(cfg: abi.Config, Ut, prim, dt: float, n: int, t0: float = 0.0):
     """n advance() steps of the 3D extension on a fully periodic box from
     oracle/ref3d_step.hpp (the reference's rk3_step / post_stage /
     prepare_stage restated with the z terms); returns (Ut, prim) after them."""
     import numpy as np
     f = lib().ignref3d_steps
-    f.argtypes = [C.POINTER(abi.Config), C.c_void_p, C.c_void_p, C.c_double, C.c_int,
-                  C.POINTER(abi.Error)]
+    f.argtypes = [C.POINTER(abi.Config), C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                  C.c_int, C.POINTER(abi.Error)]
     f.restype = C.c_int
     Ut = np.array(Ut, dtype=np.float64, order="C", copy=True)
     prim = np.array(prim, dtype=np.float64, order="C", copy=True)
     err = abi.Error()
-    st = f(C.byref(cfg), Ut.ctypes.data, prim.ctypes.data, dt, n, C.byref(err))
+    st = f(C.byref(cfg), Ut.ctypes.data, prim.ctypes.data, t0, dt, n, C.byref(err))
     if st != abi.IGN_OK:
         raise RuntimeError(f"ref3d: status {st}: {err.msg.decode()}")
     return Ut, prim

@@ -203,9 +203,11 @@ inline void roe_average3(double rl, const SpeciesArray& Yl, double Tl, double ul
 // inviscid_direction (solver.hpp:441-579) along every line, then
 // rhs = -((dF + dG) + dH) on the interior (the product's assembly order).
 // prim: rho, u, v, w, p, T, c, Y_s planes over the padded box.
+// lodi_dF (optional): the right-edge column's replacement of the xi flux
+// difference (lodi_outflow_override, solver.hpp:717-788), [c][k][j] at i = nx-1.
 inline void inviscid_rhs(const Grid& G, const Met3& M, const MixtureModel& mix,
                          const ignis::SchemeConfig& sc, const double* Ut, const double* prim,
-                         double* rhs) {
+                         double* rhs, const std::vector<double>* lodi_dF = nullptr) {
     const int ns = G.ns, nc = ns + 4, g = G.g, h = sc.stencil_half();
     const bool chr = sc.split == ignis::FluxSplit::Characteristic;
     auto P = [&](int f, long id) { return prim[long(f) * G.plane + id]; };
@@ -346,6 +348,12 @@ inline void inviscid_rhs(const Grid& G, const Met3& M, const MixtureModel& mix,
             }
     }
     const size_t ncell = size_t(G.nx) * G.ny * G.nz;
+    if (lodi_dF)
+        for (int cc = 0; cc < nc; ++cc)
+            for (int k = 0; k < G.nz; ++k)
+                for (int j = 0; j < G.ny; ++j)
+                    dH[0][size_t(cc) * ncell + (size_t(k) * G.ny + j) * G.nx + (G.nx - 1)] =
+                        (*lodi_dF)[(size_t(cc) * G.nz + k) * G.ny + j];
     for (int cc = 0; cc < nc; ++cc)
         for (int k = 0; k < G.nz; ++k)
             for (int j = 0; j < G.ny; ++j)

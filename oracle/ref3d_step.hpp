@@ -3,14 +3,14 @@
 // The reference's time loop restated for the 3D extension (BASELINE
 // configs[1], the TGV, and walled / outflow boxes — configs[3]'s edge rules):
 // the advance() loop body
-// (solver.hpp:336-345) — rk3_step (:304-332) with compute_rhs (:185-232, no
-// chemistry / laser), axpy / blend on the interior, post_stage (:826-849:
+// (solver.hpp:336-345) — rk3_step (:304-332) with compute_rhs (:185-232: the
+// LODI column on a right outflow, chemistry, laser), axpy / blend on the interior, post_stage (:826-849:
 // clip, finiteness, prepare_stage of the next stage) and the trailing
 // prepare_stage(1) — where prepare_stage (:422-425) is fill_ghosts
 // (boundary.hpp:136-258: periodic copies scaled by J_src/J_dst, no-slip walls
 // with every velocity component negated, outflow copies; the x edges over rows
 // 0..ny-1, the y edges over the padded width, then the z edges over the padded
-// (x, y) plane; inflow and the right-edge LODI are not restated) and
+// (x, y) plane; inflow with w = 0) and
 // refresh_primitives (:148-178) on every padded
 // node with the T cache as the Newton guess.  3D expressions follow the
 // extension's convention ("the reference's 2D expression, then the z terms":
@@ -19,6 +19,7 @@
 // the reference's own functions.
 #pragma once
 
+#include <cmath>
 #include <stdexcept>
 #include <vector>
 
@@ -42,9 +43,19 @@ struct Run3 {
     double& Pf(int f, long id) { return prim[size_t(f) * G.plane + id]; }
 
     // edge rules: x / y edges left, right, bottom, top; z edges back, front
-    // (0 periodic, 1 no-slip isothermal, 2 no-slip adiabatic, 4 outflow)
+    // (0 periodic, 1 no-slip isothermal, 2 no-slip adiabatic, 3 inflow (x / y
+    // edges), 4 outflow; a right-edge outflow brings the LODI column)
     int etype[4] = {0, 0, 0, 0}, ztype[2] = {0, 0};
     double Twall[4] = {0, 0, 0, 0}, Tzwall[2] = {0, 0};
+    // the reference Simulation built from the same config: its mesh (inflow
+    // coordinates, laser node coordinates, lx), bc (inflow / LODI specs),
+    // mech and laser
+    const ignis::Simulation* S = nullptr;
+    // the extension's 3D laser placement: zmode 0 = the reference's 2D kernel
+    // on every plane, 1 = the point kernel at z0; node z = zc0 + (k + 1/2) dz
+    int laser_zmode = 0;
+    double laser_z0 = 0.0, zc0 = 0.0, dz = 1.0;
+    double time = 0.0;
 
     // primitives_from_conservative (state.hpp:26-44) + w at a node, guess 300 K
     struct Prim {
@@ -117,6 +128,25 @@ struct Run3 {
             auto ij = [&](int a, int& i, int& j) {
                 if (xe) { i = a; j = t; } else { i = t; j = a; }
             };
+            if (etype[e] == 3) {  // inflow (boundary.hpp:227-241), w = 0
+                const ignis::EdgeSpec& es =
+                    e == 0 ? S->bc.left : e == 1 ? S->bc.right : e == 2 ? S->bc.bottom : S->bc.top;
+                int ii, ji;
+                ij(lo ? 0 : n - 1, ii, ji);
+                const Prim inner = prim_at(ii, ji, k);
+                for (int l = 1; l <= g; ++l) {
+                    int gi, gj;
+                    ij(lo ? -l : n - 1 + l, gi, gj);
+                    const double yc = xe ? S->mesh.eta(gj) : S->mesh.xi(gi);
+                    Prim pt{};
+                    ignis::detail::inflow_profile(es, yc, G.ns, pt.u, pt.v, pt.T, pt.Y);
+                    pt.w = 0.0;
+                    pt.p = inner.p;
+                    pt.rho = pt.p / (ignis::thermo::r_specific(pt.Y, mix) * pt.T);
+                    store_prim(pt, gi, gj, k);
+                }
+                return;
+            }
             for (int l = 1; l <= g; ++l) {
                 int gi, gj, si, sj;
                 ij(lo ? -l : n - 1 + l, gi, gj);
@@ -192,26 +222,152 @@ struct Run3 {
         refresh_primitives(stage);
     }
 
-    // compute_rhs (solver.hpp:185-232) without chemistry / laser; interior
-    void compute_rhs(std::vector<double>& r) {
+    // lodi_outflow_override (solver.hpp:717-788) on the right-edge column of
+    // every plane, the second transverse wave (w) appended: L4 = out dw/dn,
+    // dw/dt = -L4.  Returns -dU/J as [c][k][j].
+    std::vector<double> lodi_dF() {
+        const int ns = G.ns, i = G.nx - 1;
+        const ignis::EdgeSpec& es = S->bc.right;
+        std::vector<double> out(size_t(nc()) * G.nz * G.ny);
+        for (int k = 0; k < G.nz; ++k)
+            for (int j = 0; j < G.ny; ++j) {
+                const int q = G.at2(i, j);
+                const long id = G.at(i, j, k);
+                const double xi_x = Mv.mxx[q] * Mv.jac[q];
+                const double xi_y = Mv.mxy[q] * Mv.jac[q];
+                const double sn = std::hypot(xi_x, xi_y);
+                const double n1 = xi_x / sn, n2 = xi_y / sn;
+                auto ddn = [&](int f) {
+                    const double* a = prim.data() + size_t(f) * G.plane;
+                    return sn * 0.5 * (3.0 * a[id] - 4.0 * a[id - 1] + a[id - 2]);
+                };
+                const double rr = Pf(0, id), cc0 = Pf(6, id), pp = Pf(4, id);
+                const double uu = Pf(1, id), vv = Pf(2, id), ww = Pf(3, id);
+                const double un = n1 * uu + n2 * vv;
+                const double Ma = std::min(std::abs(un) / cc0, 0.99);
+                const double drdn = ddn(0);
+                const double dpdn = ddn(4);
+                const double dundn = n1 * ddn(1) + n2 * ddn(2);
+                const double dutdn = -n2 * ddn(1) + n1 * ddn(2);
+                const double dwdn = ddn(3);
+                const double K = es.sigma_out * cc0 * (1.0 - Ma * Ma) / S->mesh.lx;
+                const double L1 = K * (pp - es.p_target);
+                const double o = un > 0.0 ? un : 0.0;
+                const double L2 = o * (cc0 * cc0 * drdn - dpdn);
+                const double L3 = o * dutdn;
+                const double L4 = o * dwdn;
+                const double L5 = (un + cc0) * (dpdn + rr * cc0 * dundn);
+                const double drdt = -(L2 + 0.5 * (L5 + L1)) / (cc0 * cc0);
+                const double dundt = -(L5 - L1) / (2.0 * rr * cc0);
+                const double dutdt = -L3;
+                const double dwdt = -L4;
+                const double dpdt = -0.5 * (L5 + L1);
+                SpeciesArray Y{}, dYdt{};
+                double sumRdY = 0.0;
+                for (int sp = 0; sp < ns; ++sp) {
+                    Y[sp] = Pf(7 + sp, id);
+                    dYdt[sp] = -o * ddn(7 + sp);
+                    sumRdY += (mix.R / mix.species[sp].W) * dYdt[sp];
+                }
+                const double rbar = ignis::thermo::r_specific(Y, mix);
+                const double Tt = Pf(5, id);
+                const double dTdt = Tt * (dpdt / pp - drdt / rr - sumRdY / rbar);
+                const double dudt = n1 * dundt - n2 * dutdt;
+                const double dvdt = n2 * dundt + n1 * dutdt;
+                const double kin = 0.5 * ((uu * uu + vv * vv) + ww * ww);
+                const double e = ignis::thermo::e_mass(Tt, Y, mix);
+                const double cv = ignis::thermo::cv_mass(Tt, Y, mix);
+                double sum_es_dY = 0.0;
+                for (int sp = 0; sp < ns; ++sp) {
+                    const double esn = ignis::thermo::h_species(Tt, sp, mix) -
+                                       (mix.R / mix.species[sp].W) * Tt;
+                    sum_es_dY += esn * dYdt[sp];
+                }
+                std::vector<double> dU(nc());
+                for (int sp = 0; sp < ns; ++sp) dU[sp] = Y[sp] * drdt + rr * dYdt[sp];
+                dU[ns] = uu * drdt + rr * dudt;
+                dU[ns + 1] = vv * drdt + rr * dvdt;
+                dU[ns + 2] = ww * drdt + rr * dwdt;
+                dU[ns + 3] = (e + kin) * drdt + rr * cv * dTdt + rr * sum_es_dY +
+                             rr * ((uu * dudt + vv * dvdt) + ww * dwdt);
+                const double invJ = 1.0 / M.jac[q];
+                for (int c = 0; c < nc(); ++c)
+                    out[(size_t(c) * G.nz + k) * G.ny + j] = -dU[c] * invJ;
+            }
+        return out;
+    }
+
+    // the extension's point kernel (zmode 1): the reference's q_gaussian /
+    // q_shaped (laser.hpp:53-85) with z in the radial distance, (2 pi)^2
+    // normalisation of the 3D Gaussian
+    double laser3(double x, double y, double z, double t) const {
+        const ignis::LaserParams& p = *S->laser;
+        if (laser_zmode == 0) return ignis::laser_power(x, y, t, p);
+        const double dtn = (t - p.t0) / p.sigma_t;
+        if (p.kernel == ignis::LaserKernel::Gaussian) {
+            const double r2 = ((x - p.x0) * (x - p.x0) + (y - p.y0) * (y - p.y0)) +
+                              (z - laser_z0) * (z - laser_z0);
+            const double pow2pi2 = (2.0 * M_PI) * (2.0 * M_PI);
+            const double norm =
+                p.energy / (pow2pi2 * p.sigma_r * p.sigma_r * p.sigma_r * p.sigma_t);
+            return norm * std::exp(-0.5 * r2 / (p.sigma_r * p.sigma_r)) *
+                   std::exp(-0.5 * dtn * dtn);
+        }
+        const auto& sp = p.profile;
+        const double dx = x - p.x0;
+        const double dy = (y - p.y0) / sp.width_radial;
+        const double dzr = (z - laser_z0) / sp.width_radial;
+        const double zu = (dx + sp.lobe_sep) / sp.width_up;
+        const double zd = (dx - sp.lobe_sep) / sp.width_down;
+        const double up = std::exp(-0.5 * (zu * zu));
+        const double dn = sp.amp_down * std::exp(-0.5 * (zd * zd));
+        double f = (up + dn) * std::exp(-0.5 * (dy * dy + dzr * dzr));
+        f = f > 1.0 ? 1.0 : f;
+        return p.edot_rate * f * std::exp(-0.5 * dtn * dtn);
+    }
+
+    // compute_rhs (solver.hpp:185-232) + z: -((dF + dG) + dH) (LODI column on
+    // a right outflow), + (dVx + dVy) + dVz, chemistry, laser; interior
+    void compute_rhs(std::vector<double>& r, double t_stage) {
         r.assign(Ut.size(), 0.0);
-        inviscid_rhs(G, M, mix, sc, Ut.data(), prim.data(), r.data());
-        if (!viscous) return;
-        std::vector<double> dv(Ut.size(), 0.0);
-        viscous_rhs(G, Mv, mix, prim.data(), dv.data());
-        for (int c = 0; c < nc(); ++c)
-            for (int k = 0; k < G.nz; ++k)
-                for (int j = 0; j < G.ny; ++j)
-                    for (int i = 0; i < G.nx; ++i) {
-                        const size_t q = size_t(c) * G.plane + G.at(i, j, k);
-                        r[q] += dv[q];
+        std::vector<double> ldf;
+        const bool lodi = S && S->bc.right.type == ignis::BCType::Outflow;
+        if (lodi) ldf = lodi_dF();
+        inviscid_rhs(G, M, mix, sc, Ut.data(), prim.data(), r.data(), lodi ? &ldf : nullptr);
+        if (viscous) {
+            std::vector<double> dv(Ut.size(), 0.0);
+            viscous_rhs(G, Mv, mix, prim.data(), dv.data());
+            for (int c = 0; c < nc(); ++c)
+                for (int k = 0; k < G.nz; ++k)
+                    for (int j = 0; j < G.ny; ++j)
+                        for (int i = 0; i < G.nx; ++i) {
+                            const size_t q = size_t(c) * G.plane + G.at(i, j, k);
+                            r[q] += dv[q];
+                        }
+        }
+        const bool chem = S && S->mech.has_value();
+        const bool las = S && S->laser.has_value() && S->laser->energy != 0.0;
+        const int ns = G.ns;
+        for (int k = 0; k < G.nz; ++k)
+            for (int j = 0; j < G.ny; ++j)
+                for (int i = 0; i < G.nx; ++i) {
+                    const long id = G.at(i, j, k);
+                    const double invJ = 1.0 / M.jac[G.at2(i, j)];
+                    if (chem) {
+                        SpeciesArray Y{}, wdot{};
+                        for (int sp = 0; sp < ns; ++sp) Y[sp] = Pf(7 + sp, id);
+                        ignis::source_terms(Pf(0, id), Pf(5, id), Y, mix, *S->mech, wdot);
+                        for (int sp = 0; sp < ns; ++sp) r[size_t(sp) * G.plane + id] += wdot[sp] * invJ;
                     }
-        for (int c = 0; c < nc(); ++c)
-            for (int k = 0; k < G.nz; ++k)
-                for (int j = 0; j < G.ny; ++j)
-                    for (int i = 0; i < G.nx; ++i)
-                        if (!std::isfinite(r[size_t(c) * G.plane + G.at(i, j, k)]))
+                    if (las) {
+                        const double z = zc0 + (k + 0.5) * dz;
+                        r[size_t(ns + 3) * G.plane + id] +=
+                            laser3(S->mesh.x(i, j), S->mesh.y(i, j), z, t_stage) * invJ;
+                    }
+                    for (int c = 0; c < nc(); ++c)
+                        if (!std::isfinite(r[size_t(c) * G.plane + id]))
                             throw ignis::StepFailure("non-finite RHS", 0, i, j);
+                }
     }
 
     // post_stage (solver.hpp:826-849)
@@ -245,8 +401,9 @@ struct Run3 {
         const std::vector<double> U0 = Ut;
         std::vector<double> r;
         const double wts[3] = {0.0, 0.25, 2.0 / 3.0};
+        const double ts[3] = {time, time + dt, time + 0.5 * dt};
         for (int stage = 1; stage <= 3; ++stage) {
-            compute_rhs(r);
+            compute_rhs(r, ts[stage - 1]);
             for (int c = 0; c < nc(); ++c)
                 for (int k = 0; k < G.nz; ++k)
                     for (int j = 0; j < G.ny; ++j)
@@ -258,6 +415,7 @@ struct Run3 {
                         }
             post_stage(stage);
         }
+        time += dt;
     }
 
     // the advance() loop body with a pinned dt (solver.hpp:336-345)

@@ -170,6 +170,55 @@ void copy_field(const Field& f, double* out, std::size_t plane) {
 
 } // namespace
 
+void init_sim(Simulation& sim, const ign_config* cfg) {
+    const SchemeConfig sc = to_scheme(cfg->scheme);
+    BoundarySpec bs;
+    bs.left = to_edge(cfg->bc.left);
+    bs.right = to_edge(cfg->bc.right);
+    bs.bottom = to_edge(cfg->bc.bottom);
+    bs.top = to_edge(cfg->bc.top);
+    sim.init(make_mesh(*cfg), inviscid_mode(*cfg, sc), cfg->skew_beta,
+             to_mix(cfg->mix), sc, bs);
+    sim.viscous = cfg->viscous != 0;
+    if (cfg->mech.present) {
+        ReactionMechanism m;
+        m.A = cfg->mech.A;
+        m.Ta = cfg->mech.Ta;
+        m.a = cfg->mech.a;
+        m.b = cfg->mech.b;
+        m.T_cutoff = cfg->mech.T_cutoff;
+        m.i_fuel = cfg->mech.i_fuel;
+        m.i_ox = cfg->mech.i_ox;
+        m.i_co2 = cfg->mech.i_co2;
+        m.i_h2o = cfg->mech.i_h2o;
+        for (int s = 0; s < IGN_MAX_SPECIES; ++s) m.nu[s] = cfg->mech.nu[s];
+        sim.mech = m;
+    }
+    if (cfg->laser.present) {
+        LaserParams p;
+        p.energy = cfg->laser.energy;
+        p.sigma_r = cfg->laser.sigma_r;
+        p.sigma_t = cfg->laser.sigma_t;
+        p.x0 = cfg->laser.x0;
+        p.y0 = cfg->laser.y0;
+        p.t0 = cfg->laser.t0;
+        p.kernel = static_cast<LaserKernel>(cfg->laser.kernel);
+        p.edot_rate = cfg->laser.edot_rate;
+        p.profile.lobe_sep = cfg->laser.lobe_sep;
+        p.profile.width_up = cfg->laser.width_up;
+        p.profile.width_down = cfg->laser.width_down;
+        p.profile.amp_down = cfg->laser.amp_down;
+        p.profile.width_radial = cfg->laser.width_radial;
+        sim.laser = p;
+    }
+    sim.integ.fixed_dt = cfg->integ.fixed_dt;
+    sim.integ.t_end = cfg->integ.t_end;
+    sim.integ.max_iter = cfg->integ.max_iter;
+    sim.integ.chem_dt_limit = cfg->integ.chem_dt_limit != 0;
+    sim.integ.chem_dt_factor = cfg->integ.chem_dt_factor;
+    sim.partitions = cfg->partitions > 0 ? cfg->partitions : 1;
+}
+
 extern "C" {
 
 uint64_t ignref_config_size(void) { return sizeof(ign_config); }
@@ -181,52 +230,7 @@ int ignref_create(const ign_config* cfg, ref_ctx** out) {
     auto ctx = std::make_unique<ref_ctx>();
     const int st = guarded(&e, [&] {
         Simulation& sim = ctx->sim;
-        const SchemeConfig sc = to_scheme(cfg->scheme);
-        BoundarySpec bs;
-        bs.left = to_edge(cfg->bc.left);
-        bs.right = to_edge(cfg->bc.right);
-        bs.bottom = to_edge(cfg->bc.bottom);
-        bs.top = to_edge(cfg->bc.top);
-        sim.init(make_mesh(*cfg), inviscid_mode(*cfg, sc), cfg->skew_beta,
-                 to_mix(cfg->mix), sc, bs);
-        sim.viscous = cfg->viscous != 0;
-        if (cfg->mech.present) {
-            ReactionMechanism m;
-            m.A = cfg->mech.A;
-            m.Ta = cfg->mech.Ta;
-            m.a = cfg->mech.a;
-            m.b = cfg->mech.b;
-            m.T_cutoff = cfg->mech.T_cutoff;
-            m.i_fuel = cfg->mech.i_fuel;
-            m.i_ox = cfg->mech.i_ox;
-            m.i_co2 = cfg->mech.i_co2;
-            m.i_h2o = cfg->mech.i_h2o;
-            for (int s = 0; s < IGN_MAX_SPECIES; ++s) m.nu[s] = cfg->mech.nu[s];
-            sim.mech = m;
-        }
-        if (cfg->laser.present) {
-            LaserParams p;
-            p.energy = cfg->laser.energy;
-            p.sigma_r = cfg->laser.sigma_r;
-            p.sigma_t = cfg->laser.sigma_t;
-            p.x0 = cfg->laser.x0;
-            p.y0 = cfg->laser.y0;
-            p.t0 = cfg->laser.t0;
-            p.kernel = static_cast<LaserKernel>(cfg->laser.kernel);
-            p.edot_rate = cfg->laser.edot_rate;
-            p.profile.lobe_sep = cfg->laser.lobe_sep;
-            p.profile.width_up = cfg->laser.width_up;
-            p.profile.width_down = cfg->laser.width_down;
-            p.profile.amp_down = cfg->laser.amp_down;
-            p.profile.width_radial = cfg->laser.width_radial;
-            sim.laser = p;
-        }
-        sim.integ.fixed_dt = cfg->integ.fixed_dt;
-        sim.integ.t_end = cfg->integ.t_end;
-        sim.integ.max_iter = cfg->integ.max_iter;
-        sim.integ.chem_dt_limit = cfg->integ.chem_dt_limit != 0;
-        sim.integ.chem_dt_factor = cfg->integ.chem_dt_factor;
-        sim.partitions = cfg->partitions > 0 ? cfg->partitions : 1;
+        init_sim(sim, cfg);
         ctx->ns = sim.ns();
         ctx->plane = sim.Ut[0].raw().size();
     });
@@ -464,22 +468,17 @@ int ignref3d_viscous_rhs(const ign_config* cfg, const double* prim, double* dv,
     });
 }
 
-// n advance() steps of the 3D extension (periodic, wall and non-LODI outflow edges)
+// n advance() steps of the 3D extension (every edge rule, LODI, chemistry, laser)
 // (oracle/ref3d_step.hpp) from the product's state and primitive cache
 // (Ut: nc planes, prim: rho, u, v, w, p, T, c, Y_s planes; both in/out).
-int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double dt, int n,
+int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double t0, double dt, int n,
                    ign_error* err) {
     return guarded(err, [&] {
         if (cfg->nz <= 0) throw UsageError("ref3d: nz must be > 0");
         const ign_edge* e[4] = {&cfg->bc.left, &cfg->bc.right, &cfg->bc.bottom, &cfg->bc.top};
-        for (int q = 0; q < 4; ++q) {
-            const int t = e[q]->type;
-            if (t == 3 || (q == 1 && t == 4))  // inflow; right outflow = LODI
-                throw UsageError("ref3d_steps: no inflow / right-edge outflow (LODI)");
-        }
-        if (cfg->mech.present || cfg->laser.present)
-            throw UsageError("ref3d_steps: no chemistry / laser");
-        const Mesh mesh = make_mesh(*cfg);
+        Simulation sim;  // the reference's mesh, bc, mech, laser for this config
+        init_sim(sim, cfg);
+        const Mesh& mesh = sim.mesh;
         const SchemeConfig sc = to_scheme(cfg->scheme);
         const double dz = cfg->lz / cfg->nz;
         ref3d::Run3 R;
@@ -488,6 +487,12 @@ int ignref3d_steps(const ign_config* cfg, double* Ut, double* prim, double dt, i
         R.mix = to_mix(cfg->mix);
         R.sc = sc;
         R.viscous = cfg->viscous != 0;
+        R.S = &sim;
+        R.laser_zmode = cfg->laser.zmode;
+        R.laser_z0 = cfg->laser.z0;
+        R.zc0 = cfg->center_z - 0.5 * cfg->lz;
+        R.dz = dz;
+        R.time = t0;
         for (int q = 0; q < 4; ++q) {
             R.etype[q] = e[q]->type;
             R.Twall[q] = e[q]->T_wall;
