@@ -139,31 +139,23 @@ int ign_set_initial_primitives(ign_context* ctx, const double* prim) {
 
 int ign_set_state(ign_context* ctx, const double* Ut, const double* Tc) {
     return guarded_err(&ctx->lasterr, ctx->device, [&] {
-        cuda_check(cudaMemcpy(ctx->S[ctx->cur], Ut, ctx->nc * ctx->plane * sizeof(double),
-                              cudaMemcpyHostToDevice),
-                   "set_state");
+        h2d(ctx, ctx->S[ctx->cur], Ut, ctx->nc * ctx->plane * sizeof(double), "set_state");
         if (Tc)
-            cuda_check(cudaMemcpy(ctx->prim + (ctx->nz > 0 ? 5 : 4) * ctx->plane, Tc,
-                                  ctx->plane * sizeof(double),
-                                  cudaMemcpyHostToDevice),
-                       "set_state T");
+            h2d(ctx, ctx->prim + (ctx->nz > 0 ? 5 : 4) * ctx->plane, Tc,
+                ctx->plane * sizeof(double), "set_state T");
     });
 }
 
 int ign_get_state(ign_context* ctx, double* Ut) {
     return guarded_err(&ctx->lasterr, ctx->device, [&] {
-        cuda_check(cudaMemcpy(Ut, ctx->S[ctx->cur], ctx->nc * ctx->plane * sizeof(double),
-                              cudaMemcpyDeviceToHost),
-                   "get_state");
+        d2h(ctx, Ut, ctx->S[ctx->cur], ctx->nc * ctx->plane * sizeof(double), "get_state");
     });
 }
 
 int ign_get_cache(ign_context* ctx, double* prim) {
     return guarded_err(&ctx->lasterr, ctx->device, [&] {
-        cuda_check(cudaMemcpy(prim, ctx->prim,
-                              ((ctx->nz > 0 ? 7 : 6) + ctx->ns) * ctx->plane * sizeof(double),
-                              cudaMemcpyDeviceToHost),
-                   "get_cache");
+        d2h(ctx, prim, ctx->prim, ((ctx->nz > 0 ? 7 : 6) + ctx->ns) * ctx->plane * sizeof(double),
+            "get_cache");
     });
 }
 
@@ -224,8 +216,7 @@ int ign_compute_rhs(ign_context* ctx, double t_stage, int stage, double* rhs) {
         t_errsync(T);
         check(T);
         if (rhs)
-            cuda_check(cudaMemcpy(rhs, ctx->rhs, n * sizeof(double), cudaMemcpyDeviceToHost),
-                       "rhs readback");
+            d2h(ctx, rhs, ctx->rhs, n * sizeof(double), "rhs readback");
     });
 }
 

@@ -153,6 +153,8 @@ cudaEvent_t prof_event(ign_context* ctx);
 void prof_harvest(ign_context* ctx);
 double* dalloc(size_t n);
 void* dmalloc(size_t bytes);
+void h2d(ign_context* c, void* dst, const void* src, size_t bytes, const char* what);
+void d2h(const ign_context* c, void* dst, const void* src, size_t bytes, const char* what);
 void dfree(void* p);
 void guard_status(int* enabled, unsigned long long* checked, unsigned long long* bad);
 unsigned long long guard_selftest();

@@ -188,8 +188,7 @@ void t_conserved_totals(const Team& T, double* tot) {
         fold_ranks(T, a1, [&](ign_context* c, std::vector<double>& a) {
             const size_t P = c->plane;
             std::vector<double> U(P);
-            cuda_check(cudaMemcpy(U.data(), c->S[c->cur] + comp * P, P * 8, cudaMemcpyDeviceToHost),
-                       "totals");
+            d2h(c, U.data(), c->S[c->cur] + comp * P, P * 8, "totals");
             const int sx = c->nx + 2 * c->g, g = c->g;
             const size_t sxy = size_t(sx) * (c->ny + 2 * g);
             double s = a[0];
@@ -231,9 +230,7 @@ double t_product_fraction(const Team& T) {
     fold_ranks(T, acc, [&](ign_context* c, std::vector<double>& a) {
         const size_t P = c->plane;
         std::vector<double> Y(c->ns * P);
-        cuda_check(cudaMemcpy(Y.data(), c->prim + (c->nz > 0 ? 7 : 6) * P, Y.size() * 8,
-                              cudaMemcpyDeviceToHost),
-                   "Y readback");
+        d2h(c, Y.data(), c->prim + (c->nz > 0 ? 7 : 6) * P, Y.size() * 8, "Y readback");
         const DMix& m = c->kp.mix;
         const int sx = c->nx + 2 * c->g, g = c->g;
         const size_t sxy = size_t(sx) * (c->ny + 2 * g);
@@ -353,7 +350,7 @@ void t_gather(const Team& T, bool tcache, std::vector<double>& out) {
             if (T.local() || r == 0) {
                 const double* src = (tcache ? m->prim + (three_d ? 5 : 4) * m->plane
                                             : m->S[m->cur] + c * m->plane) + p0 * st;
-                cuda_check(cudaMemcpy(dst, src, cnt * 8, cudaMemcpyDeviceToHost), "gather");
+                d2h(m, dst, src, cnt * 8, "gather");
             } else {
                 if (!stage) stage = dalloc(static_cast<size_t>(NG / N + 2 + 2 * g) * st);
                 NcclApi& n = nccl();
@@ -429,14 +426,11 @@ void t_read_snapshot(const Team& T, const std::string& path) {
         const int lo = three_d ? c->k0 : c->mesh.j0;  // global interior start
         const size_t cnt = (halo_count(c) + 2 * c->g) * st;
         for (int comp = 0; comp < c->nc; ++comp)
-            cuda_check(cudaMemcpy(c->S[c->cur] + comp * c->plane,
-                                  s.state.data() + comp * gplane + lo * st, cnt * 8,
-                                  cudaMemcpyHostToDevice),
-                       "snapshot upload");
+            h2d(c, c->S[c->cur] + comp * c->plane, s.state.data() + comp * gplane + lo * st,
+                cnt * 8, "snapshot upload");
         if (s.flags & 1u)
-            cuda_check(cudaMemcpy(c->prim + (three_d ? 5 : 4) * c->plane,
-                                  s.tcache.data() + lo * st, cnt * 8, cudaMemcpyHostToDevice),
-                       "snapshot upload");
+            h2d(c, c->prim + (three_d ? 5 : 4) * c->plane, s.tcache.data() + lo * st, cnt * 8,
+                "snapshot upload");
         c->time = s.time;
         c->iter = s.iteration;
         c->config_hash = s.config_hash;

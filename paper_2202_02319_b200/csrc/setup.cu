@@ -121,9 +121,7 @@ void cons_from_prim3(const DMix& m, const Prim3<kMaxSpecies>& pt, const double* 
 }
 
 void upload_state(ign_context* ctx, const std::vector<double>& Ut) {
-    cuda_check(cudaMemcpy(ctx->S[ctx->cur], Ut.data(), Ut.size() * sizeof(double),
-                          cudaMemcpyHostToDevice),
-               "state upload");
+    h2d(ctx, ctx->S[ctx->cur], Ut.data(), Ut.size() * sizeof(double), "state upload");
 }
 
 void destroy_impl(ign_context* ctx) {
@@ -414,6 +412,9 @@ void create_impl(const ign_config* cfg, ign_context* ctx) {
     k.mech = build_mech(cfg->mech);
     k.laser = build_laser(cfg->laser);
     ctx->ks = nz > 0 ? kernel_set3(ns) : kernel_set(ns);
+    // the uploads and memsets above ran on the legacy stream, which the
+    // context's non-blocking stream does not wait for: finish them here
+    cuda_check(cudaDeviceSynchronize(), "setup");
 }
 
 void copy_hfield(const HField& f, double* out) { std::memcpy(out, f.d.data(), f.d.size() * 8); }
