@@ -106,7 +106,9 @@ void prof_harvest(ign_context* ctx) {
 // pattern, so a kernel that READS past a buffer and uses the value turns the
 // step non-finite (the error word / the oracle parity catch it), and a kernel
 // that WRITES past one changes a canary, which dfree() and ign_guard_status()
-// count.  Off by default (the product allocates exactly what it uses).
+// count.  The buffer itself starts filled with the same NaN, so a read of a
+// word nothing wrote shows up the same way.  Off by default (the product
+// allocates exactly what it uses).
 namespace {
 constexpr size_t kGuardWords = 4096;  // 32 KB per side: the user pointer keeps 32 KB alignment
 constexpr unsigned long long kCanary = 0x7ff4dead0badf00dull;
@@ -137,6 +139,14 @@ unsigned long long guard_scan(const GuardRec& r) {
 }
 }  // namespace
 
+// guard mode: the user region starts poisoned too (the same signalling NaN),
+// so a kernel that reads a word nothing wrote turns the step non-finite
+__global__ void k_poison(unsigned long long* p, size_t n) {
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
+         q += (size_t)gridDim.x * blockDim.x)
+        p[q] = kCanary;
+}
+
 void* dmalloc(size_t bytes) {
     bytes = std::max<size_t>(bytes, 1);
     if (!guard_on()) {
@@ -153,6 +163,10 @@ void* dmalloc(size_t bytes) {
     cuda_check(cudaMemcpy(r.base + (kGuardWords + r.words) * 8, can.data(), kGuardWords * 8,
                           cudaMemcpyHostToDevice),
                "guard");
+    k_poison<<<1184, 256>>>(reinterpret_cast<unsigned long long*>(r.base + kGuardWords * 8),
+                            r.words);
+    cuda_check(cudaGetLastError(), "guard poison");
+    cuda_check(cudaDeviceSynchronize(), "guard");  // canaries in place before any kernel
     void* user = r.base + kGuardWords * 8;
     std::lock_guard<std::mutex> lk(g_guard_mu);
     g_guard_live[user] = r;
@@ -160,6 +174,23 @@ void* dmalloc(size_t bytes) {
 }
 
 double* dalloc(size_t n) { return static_cast<double*>(dmalloc(n * sizeof(double))); }
+
+// Host -> device upload ordered on the context's stream.  The context's
+// stream is non-blocking, so it is NOT ordered after the legacy default
+// stream: a plain cudaMemcpy from pageable memory may return before its DMA
+// lands, and the next kernel on the stream could read the old contents.
+// The stream sync also makes the host buffer reusable on return.
+void h2d(ign_context* c, void* dst, const void* src, size_t bytes, const char* what) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream), what);
+    cuda_check(cudaStreamSynchronize(c->stream), what);
+}
+
+// Device -> host read after the context's stream has drained (the legacy
+// stream a plain cudaMemcpy runs on does not wait for the non-blocking one).
+void d2h(const ign_context* c, void* dst, const void* src, size_t bytes, const char* what) {
+    cuda_check(cudaStreamSynchronize(c->stream), what);
+    cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), what);
+}
 
 // Frees a dmalloc() buffer (nullptr is a no-op); a guarded one has its canaries
 // checked first (the device is synchronised so pending kernels have written).
@@ -263,7 +294,7 @@ DevFail sync_and_read(const Team& T) {
     f.idx = (h.key >> 3) & ((1ull << 35) - 1);
     f.sub = (unsigned)(h.key & 7);
     for (ign_context* c : T.m)
-        cuda_check(cudaMemset(c->own_err, 0xff, sizeof(ErrRec)), "error reset");
+        cuda_check(cudaMemsetAsync(c->own_err, 0xff, sizeof(ErrRec), c->stream), "error reset");
     return f;
 }
 
