@@ -594,8 +594,22 @@ def _duct3d(outflow=False):
     return case
 
 
+def _wall4sp_zwalls():
+    """configs' 4-species CH4/O2 wall channel extruded, z walls added
+    (isothermal back at 900 K — the channel spans 300-900 K, so 2 T_w - T stays
+    inside the thermo tables — adiabatic front)."""
+    case = configs.extrude_z(configs.wall_channel(16), 12)
+    case.cfg.lz = 0.01 * 12 / 16  # dz = dx
+    case.cfg.periodic_z = 0
+    case.cfg.zlo.type = abi.NOSLIP_ISOTHERMAL
+    case.cfg.zlo.T_wall = 900.0
+    case.cfg.zhi.type = abi.NOSLIP_ADIABATIC
+    return case
+
+
 STEPS3D = {
     "duct3d_walls": _duct3d,
+    "wall4sp_zwalls": _wall4sp_zwalls,
     "duct3d_walls_outflow": lambda: _duct3d(outflow=True),
     "tgv3d_visc_char_teno6": lambda: configs.tgv3d(16, nz=14),
     "tgv3d_visc_ragged": lambda: configs.tgv3d(18, nz=13),
