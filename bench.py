@@ -75,9 +75,12 @@ OPS = {  # case -> (inviscid face ops per cell-stage, whole-step ops per cell)
     "h2o2": (7904.9, 28111.7),
     "jet3d": (None, None),      # 4 species, 3D, WENO3Z componentwise: not counted
 }
-TRAFFIC = {("tgv3d", 256): (1.790489 + 1.820969 + 2.120700 + 0.652935 + 0.657080 + 0.659103) * 1e9}
+TRAFFIC = {("tgv3d", 256): (1.790489 + 1.820969 + 2.120700 + 0.652935 + 0.657080 + 0.659103) * 1e9,
+           ("h2o2", 512): (42.504704 + 42.905344) * 1e6 + (301.056 + 630.016) * 1e3}
 TRAFFIC_SOURCE = {("tgv3d", 256): "ncu --set full capture of the three k_faces3d launches of one "
-                                  "stage at 256^3 (profiles/r2d_ncu_faces3d_256.txt), not this run"}
+                                  "stage at 256^3 (profiles/r2d_ncu_faces3d_256.txt), not this run",
+                  ("h2o2", 512): "ncu --set full capture of the x and y k_faces3 launches of one "
+                                 "stage at 512^2 (profiles/r2d_ncu_faces_h2o2_512.txt), not this run"}
 OPS_SOURCE = {
     "tgv": "reference's own code, counted-double run at 256^2 (profiles/r2_opcount_ref2d.json)",
     "tgv3d": ("counted-double run of oracle/ref3d_faces.hpp (the reference's per-face "
